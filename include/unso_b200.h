@@ -1,0 +1,136 @@
+/*
+ * unso_b200.h -- C ABI of the B200-native UNSO orthogonalization hot path.
+ *
+ * The reference (arXiv 2602.02500, /root/reference/pkg/src/unso) is a pure
+ * Python/numpy package with no FFI; its drop-in boundary is the Python API of
+ * `unso.ortho` (re-exported in unso/__init__.py:31-42).  Each entry point below
+ * replaces one reference function; the Python host package
+ * `paper_2602_02500_b200` binds them with ctypes.
+ *
+ * Conventions
+ *   - Plain pointers and sizes; every call is stream-ordered on `stream`
+ *     (a cudaStream_t passed as void*), never synchronises the host, never throws.
+ *   - The caller owns all memory (inputs, outputs, workspace; device memory).
+ *   - Matrices are strided batches of row-major rows x cols matrices.
+ *   - Host-detectable errors are returned as unso_status; data-dependent
+ *     errors (zero input / non-finite scale, ortho.py:147-148,164-165) are
+ *     written per matrix to the device int32 array `d_status` (may be NULL).
+ */
+#ifndef UNSO_B200_H
+#define UNSO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum unso_status {
+  UNSO_OK = 0,
+  UNSO_ERR_SHAPE = 1,        /* ShapeError            (errors.py:4-5)          */
+  UNSO_ERR_DEGENERATE = 2,   /* DegenerateInputError  (errors.py:12-13)        */
+  UNSO_ERR_VALUE = 3,        /* ValueError            (ortho.py:85-110)        */
+  UNSO_ERR_CUDA = 4,         /* CUDA launch / driver failure                    */
+  UNSO_ERR_UNSUPPORTED = 5,  /* valid request this build does not implement     */
+  UNSO_ERR_WORKSPACE = 6     /* workspace smaller than unso_workspace_size()    */
+} unso_status;
+
+typedef enum unso_dtype { UNSO_DTYPE_F32 = 0, UNSO_DTYPE_BF16 = 1, UNSO_DTYPE_F64 = 2 } unso_dtype;
+
+/* Arithmetic recipe.
+ *   FP32: fp32 I/O, fp64-grade Gram + squaring chain (DFMA), fp64-accumulated apply;
+ *         parity <= 1e-5 against the fp64 reference on every config.
+ *   BF16: tcgen05 tensor cores, bf16 operands / f32 accumulation; the h x h chain in
+ *         C-form with bf16x3 split products, the apply with a bf16x2 split P;
+ *         parity <= 2e-2 against the reference fed the same bf16-rounded input. */
+typedef enum unso_precision { UNSO_PREC_FP32 = 0, UNSO_PREC_BF16 = 1 } unso_precision;
+
+/* Scaling (ortho.py:54-57): gram = A/||AA^T||_F^(1/2), plain = A/||A||_F, gelfand. */
+typedef enum unso_scaling {
+  UNSO_SCALING_GRAM = 0,
+  UNSO_SCALING_PLAIN = 1,
+  UNSO_SCALING_GELFAND = 2,
+  UNSO_SCALING_NONE = 3 /* input already scaled: the bare kernels unso()/muon_ns()/... (ortho.py:171-256) */
+} unso_scaling;
+
+/* Kernel families (ortho.py:60-65): UNSO, original cubic NS, and the quintic
+ * step family (muon / cesista / external differ only in their (a,b,c) rows). */
+typedef enum unso_method { UNSO_METHOD_UNSO = 0, UNSO_METHOD_ORIGINAL_NS = 1, UNSO_METHOD_QUINTIC = 2 } unso_method;
+
+/* flags */
+#define UNSO_FLAG_SINGLE_TERM_APPLY 0x1 /* BF16: apply with P rounded to one bf16 term (faster, less accurate) */
+
+typedef struct unso_matrix_desc {
+  int64_t rows, cols;    /* per matrix, as given (orientation is chosen internally, ortho.py:149-150) */
+  int64_t ld;            /* leading dimension in elements, >= cols */
+  int64_t batch;         /* number of matrices, >= 1 */
+  int64_t batch_stride;  /* elements between consecutive matrices */
+  int32_t dtype;         /* unso_dtype of the input and of the output */
+  int32_t reserved;
+} unso_matrix_desc;
+
+typedef struct unso_method_desc {
+  int32_t method;        /* unso_method */
+  int32_t scaling;       /* unso_scaling (already resolved: UNSO -> gram, NS -> plain, ortho.py:112-118) */
+  int32_t gelfand_power; /* >= 1 (ortho.py:78,85-86) */
+  int32_t precision;     /* unso_precision */
+  int32_t order;         /* UNSO: N (number of polynomial terms, scalarpoly.py:39-61) */
+  int32_t steps;         /* ORIGINAL_NS: iterations; QUINTIC: number of (a,b,c) rows */
+  const double* coeffs;  /* host memory. UNSO: N values a_1..a_{N-1}, b (b = derive_b, scalarpoly.py:117-127);
+                            QUINTIC: 3*steps values, row-major (a,b,c) (ortho.py:221-231); ORIGINAL: unused */
+  int32_t flags;         /* UNSO_FLAG_* */
+  int32_t reserved;
+} unso_method_desc;
+
+/* Library identity. */
+const char* unso_version(void);
+const char* unso_status_string(int32_t status);
+
+/* Bytes of device workspace `unso_orthogonalize` / `unso_orthogonalize_from_gram` /
+ * `unso_gram` / `unso_ortho_error` need for this problem (0 on invalid input). */
+size_t unso_workspace_size(const unso_matrix_desc* x, const unso_method_desc* method);
+
+/* Y = orthogonalize(X): preprocess -> kernel -> restore orientation.
+ * Replaces unso.ortho.orthogonalize (ortho.py:267-283) together with
+ * preprocess (ortho.py:140-168) and unso / original_ns / _quintic_steps
+ * (ortho.py:171-231).  y has x's shape and dtype, contiguous (ld = cols). */
+int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y_ptr,
+                           const unso_method_desc* method, void* workspace, size_t workspace_bytes,
+                           int32_t* d_status, void* stream);
+
+/* Row-sharded path, stage 1: the un-normalised short-side Gram of the local rows
+ * (ortho.py:156, 198 without the 1/denom).  g_ptr: batch x h x h, element type
+ * unso_gram_dtype(method) (f64 for FP32 precision, f32 for BF16).  The caller sums
+ * it over ranks (one all-reduce) before stage 2.  UNSO method only. */
+int32_t unso_gram(const unso_matrix_desc* x, const void* x_ptr, void* g_ptr, const unso_method_desc* method,
+                  void* workspace, size_t workspace_bytes, void* stream);
+int32_t unso_gram_dtype(const unso_method_desc* method);
+
+/* Row-sharded path, stage 2: given the (globally reduced) Gram, scale, form P
+ * with the squaring chain (ortho.py:197-204) and apply it to the local rows
+ * (ortho.py:205).  Every rank forms the same P redundantly. */
+int32_t unso_orthogonalize_from_gram(const unso_matrix_desc* x, const void* x_ptr, const void* g_ptr, void* y_ptr,
+                                     const unso_method_desc* method, void* workspace, size_t workspace_bytes,
+                                     int32_t* d_status, void* stream);
+
+/* The preprocess denominator alone (ortho.py:140-168): d_denom[b] = ||A A^T||_F^(1/2) (gram),
+ * ||A||_F (plain) or ||(A A^T)^k||_F^(1/2k) (gelfand), fp64 accumulation; d_status[b] = 2 when the
+ * input is zero or the denominator is not positive and finite. Only scaling/gelfand_power are read. */
+int32_t unso_scale_denominator(const unso_matrix_desc* x, const void* x_ptr, const unso_method_desc* method,
+                               double* d_denom, void* workspace, size_t workspace_bytes, int32_t* d_status,
+                               void* stream);
+
+/* ||Y Y^T - I||_F on the short side (bench.py:71-82), fp64 accumulation;
+ * writes `batch` doubles to device memory d_err. */
+int32_t unso_ortho_error(const unso_matrix_desc* y, const void* y_ptr, double* d_err, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
+/* Number of CUDA kernels launched by the last successful call on this thread. */
+int32_t unso_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UNSO_B200_H */

@@ -1,0 +1,56 @@
+// Shared device helpers: element loads/stores by dtype, bf16 hi/lo split, reductions.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace unso {
+
+enum Dtype : int { DT_F32 = 0, DT_BF16 = 1, DT_F64 = 2 };
+
+__host__ __device__ inline int dtype_size(int dt) { return dt == DT_F32 ? 4 : (dt == DT_BF16 ? 2 : 8); }
+
+__device__ __forceinline__ double load_as_f64(const void* p, int64_t i, int dt) {
+  if (dt == DT_F32) return static_cast<double>(static_cast<const float*>(p)[i]);
+  if (dt == DT_BF16) return static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]));
+  return static_cast<const double*>(p)[i];
+}
+__device__ __forceinline__ void store_from_f64(void* p, int64_t i, int dt, double v) {
+  if (dt == DT_F32)
+    static_cast<float*>(p)[i] = static_cast<float>(v);
+  else if (dt == DT_BF16)
+    static_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(static_cast<float>(v));
+  else
+    static_cast<double*>(p)[i] = v;
+}
+
+// x ~= hi + lo with hi = bf16(x), lo = bf16(x - hi): 16 significant bits, the operand
+// split used by the bf16x3 / bf16x2 tensor-core products.
+__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum (blockDim.x multiple of 32, <= 1024); result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double* scratch /* >= 32 */) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < nw ? scratch[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  return t;
+}
+
+}  // namespace unso

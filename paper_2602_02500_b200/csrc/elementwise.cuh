@@ -1,0 +1,290 @@
+// HBM-bound helper kernels around the contractions: dtype conversion, split-K
+// finalize (+ symmetric mirror), Gram norm reductions, per-matrix scalars,
+// the C-form chain prologue (C_1 = G/s^2, P = alpha I - a_1 C_1) and the
+// symmetric P finalisation (scale by 1/s, split for the apply).
+#pragma once
+#include "common.cuh"
+
+namespace unso {
+
+constexpr int NORM_BLOCKS = 64;  // per-matrix partial-reduction blocks (fixed -> deterministic)
+
+// scal[b * SCAL_STRIDE + ...]
+enum ScalSlot : int { S_TRACE = 0, S_FRO2 = 1, S_DEV2 = 2, S_S2 = 3, S_INV_S = 4, S_ERR = 5 };
+constexpr int SCAL_STRIDE = 8;
+
+// ------------------------------------------------------------------ conversion
+// dst[b](r, c) = src[b](r, c) * (scal ? scal[b].inv_s : 1), any dtype -> any dtype.
+__global__ void convert_kernel(const void* __restrict__ src, int sdt, int64_t sld, int64_t sbs, void* __restrict__ dst,
+                               int ddt, int64_t dld, int64_t dbs, int64_t rows, int64_t cols, int batch,
+                               const double* __restrict__ scal) {
+  const int64_t per = rows * cols;
+  const int64_t total = per * batch;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = i / per, rc = i - b * per, r = rc / cols, c = rc - r * cols;
+    double v = load_as_f64(src, b * sbs + r * sld + c, sdt);
+    if (scal) v *= scal[b * SCAL_STRIDE + S_INV_S];
+    store_from_f64(dst, b * dbs + r * dld + c, ddt, v);
+  }
+}
+
+// fast path: f32 -> bf16 (row-contiguous source), 4 elements per thread
+__global__ void f32_to_bf16_kernel(const float* __restrict__ src, int64_t sld, int64_t sbs,
+                                   __nv_bfloat16* __restrict__ dst, int64_t dld, int64_t dbs, int64_t rows,
+                                   int64_t cols, int batch) {
+  const int64_t cq = cols / 4;
+  const int64_t per = rows * cq;
+  const int64_t total = per * batch;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = i / per, rc = i - b * per, r = rc / cq, c = (rc - r * cq) * 4;
+    const float4 v = *reinterpret_cast<const float4*>(src + b * sbs + r * sld + c);
+    __nv_bfloat162 lo2 = __floats2bfloat162_rn(v.x, v.y);
+    __nv_bfloat162 hi2 = __floats2bfloat162_rn(v.z, v.w);
+    __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(dst + b * dbs + r * dld + c);
+    d[0] = lo2;
+    d[1] = hi2;
+  }
+}
+
+// ------------------------------------------------------------------ symmetric tiles
+// 32x32 upper tiles (ti <= tj) of a batch of h x h matrices; the load functor
+// produces tile values, the store functor writes (r, c) in both triangles.
+__device__ __forceinline__ void sym_tile_coords(int t, int nt, int& ti, int& tj) {
+  int row = 0, len = nt;
+  while (t >= len) {
+    t -= len;
+    ++row;
+    --len;
+  }
+  ti = row;
+  tj = row + t;
+}
+
+// G[b] = sum_s part[s][b]  (upper values mirrored into the lower triangle)
+template <typename T>
+__global__ void finalize_sum_kernel(const T* __restrict__ part, int splits, int batch, int h, int64_t ld,
+                                    T* __restrict__ G) {
+  __shared__ double tile[32][33];
+  const int nt = (h + 31) / 32;
+  int ti, tj;
+  sym_tile_coords(blockIdx.x, nt, ti, tj);
+  const int b = blockIdx.y;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t mat = static_cast<int64_t>(h) * ld;
+  for (int r = ty; r < 32; r += 8) {
+    const int gr = ti * 32 + r, gc = tj * 32 + tx;
+    double s = 0.0;
+    if (gr < h && gc < h) {
+      for (int sp = 0; sp < splits; ++sp)
+        s += static_cast<double>(part[(static_cast<int64_t>(sp) * batch + b) * mat + static_cast<int64_t>(gr) * ld + gc]);
+    }
+    tile[r][tx] = s;
+  }
+  __syncthreads();
+  T* g = G + static_cast<int64_t>(b) * mat;
+  for (int r = ty; r < 32; r += 8) {
+    const int gr = ti * 32 + r, gc = tj * 32 + tx;
+    if (gr < h && gc < h) g[static_cast<int64_t>(gr) * ld + gc] = static_cast<T>((ti == tj && r > tx) ? tile[tx][r] : tile[r][tx]);
+    if (ti != tj) {
+      const int mr = tj * 32 + r, mc = ti * 32 + tx;
+      if (mr < h && mc < h) g[static_cast<int64_t>(mr) * ld + mc] = static_cast<T>(tile[tx][r]);
+    }
+  }
+}
+
+// Per-block partial sums over a full symmetric h x h matrix: trace, ||G||_F^2, ||G - I||_F^2.
+template <typename T>
+__global__ void gram_norms_kernel(const T* __restrict__ G, int h, int64_t ld, double* __restrict__ blk) {
+  __shared__ double scratch[32];
+  const int b = blockIdx.y;
+  const T* g = G + static_cast<int64_t>(b) * h * ld;
+  double tr = 0.0, fr = 0.0, dv = 0.0;
+  const int64_t total = static_cast<int64_t>(h) * h;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / h, c = i - r * h;
+    const double v = static_cast<double>(g[r * ld + c]);
+    const double d = (r == c) ? v - 1.0 : v;
+    if (r == c) tr += v;
+    fr += v * v;
+    dv += d * d;
+  }
+  tr = block_sum(tr, scratch);
+  if (threadIdx.x == 0) blk[(static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * 3 + 0] = tr;
+  fr = block_sum(fr, scratch);
+  if (threadIdx.x == 0) blk[(static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * 3 + 1] = fr;
+  dv = block_sum(dv, scratch);
+  if (threadIdx.x == 0) blk[(static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * 3 + 2] = dv;
+}
+
+// sum of squares of a rows x cols input (plain scaling, ortho.py:153-154) -> slot 0
+__global__ void sumsq_kernel(const void* __restrict__ x, int dt, int64_t rows, int64_t cols, int64_t ld, int64_t bs,
+                             double* __restrict__ blk) {
+  __shared__ double scratch[32];
+  const int b = blockIdx.y;
+  const int64_t total = rows * cols;
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const double v = load_as_f64(x, b * bs + r * ld + c, dt);
+    s += v * v;
+  }
+  s = block_sum(s, scratch);
+  if (threadIdx.x == 0) {
+    double* o = blk + (static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * 3;
+    o[0] = s;
+    o[1] = 0.0;
+    o[2] = 0.0;
+  }
+}
+
+enum ScalarsMode : int { SM_GRAM = 0, SM_PLAIN = 1, SM_GELFAND = 2, SM_ERROR = 3, SM_NONE = 4 };
+
+// One block per matrix: fixed-order reduction of the partials, then the scale
+// denominator of preprocess (ortho.py:153-165) and the degenerate-input status.
+__global__ void scalars_kernel(const double* __restrict__ blk, int nblk, int mode, int gelfand_power,
+                               double* __restrict__ scal, int32_t* __restrict__ status) {
+  __shared__ double scratch[32];
+  const int b = blockIdx.x;
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    const double* p = blk + (static_cast<int64_t>(b) * nblk + i) * 3;
+    t0 += p[0];
+    t1 += p[1];
+    t2 += p[2];
+  }
+  t0 = block_sum(t0, scratch);
+  const double s0 = t0;
+  t1 = block_sum(t1, scratch);
+  const double s1 = t1;
+  t2 = block_sum(t2, scratch);
+  const double s2v = t2;
+  if (threadIdx.x != 0) return;
+  double* o = scal + static_cast<int64_t>(b) * SCAL_STRIDE;
+  if (mode == SM_ERROR) {
+    o[S_ERR] = sqrt(s2v);
+    return;
+  }
+  if (mode == SM_GELFAND) {
+    // s0/s1 are the norms of G^k: denom = ||G^k||_F^(1/2k) -> s^2 = ||G^k||_F^(1/k)
+    const double s2 = pow(sqrt(s1), 1.0 / gelfand_power);
+    o[S_S2] = s2;
+    o[S_INV_S] = 1.0 / sqrt(s2);
+    const bool bad = !(s2 > 0.0) || !isfinite(s2) || !isfinite(o[S_INV_S]);
+    if (status && bad) status[b] = 2;
+    return;
+  }
+  o[S_TRACE] = s0;
+  o[S_FRO2] = s1;
+  o[S_DEV2] = s2v;
+  if (mode == SM_NONE) {  // bare kernel on pre-scaled input: no rescale, no degenerate check
+    o[S_S2] = 1.0;
+    o[S_INV_S] = 1.0;
+    if (status) status[b] = 0;
+    return;
+  }
+  const double s2 = (mode == SM_PLAIN) ? s0 : sqrt(s1);
+  o[S_S2] = s2;
+  o[S_INV_S] = 1.0 / sqrt(s2);
+  // zero input <=> trace(A A^T) = ||A||_F^2 = 0 (ortho.py:147-148); bad denominator (ortho.py:164-165)
+  const bool bad = !(s0 > 0.0) || !isfinite(s0) || !(s2 > 0.0) || !isfinite(s2) || !isfinite(o[S_INV_S]);
+  if (status) status[b] = bad ? 2 : 0;
+}
+
+__global__ void copy_err_kernel(const double* __restrict__ scal, int batch, double* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < batch) out[b] = scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_ERR];
+}
+
+__global__ void copy_denom_kernel(const double* __restrict__ scal, int batch, double* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < batch) out[b] = sqrt(scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_S2]);
+}
+
+// ------------------------------------------------------------------ chain prologue
+// C_1 = G / s^2 (C-form state), P = alpha I - coef1 C_1 with
+// alpha = 1 + sum(a) + b.  fp64 variant (FP32 precision) and bf16 hi/lo variant.
+template <typename TG>
+__global__ void prep_f64_kernel(const TG* __restrict__ G, int h, int64_t ld, const double* __restrict__ scal,
+                                double alpha, double coef1, double* __restrict__ C, double* __restrict__ P) {
+  const int b = blockIdx.y;
+  const int64_t total = static_cast<int64_t>(h) * h;
+  const double inv_s2 = 1.0 / scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_S2];
+  const int64_t off = static_cast<int64_t>(b) * h * ld;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / h, c = i - r * h, o = off + r * ld + c;
+    const double cv = static_cast<double>(G[o]) * inv_s2;
+    C[o] = cv;
+    P[o] = (r == c ? alpha : 0.0) - coef1 * cv;
+  }
+}
+
+__global__ void prep_bf16_kernel(const float* __restrict__ G, int h, int64_t ld, const double* __restrict__ scal,
+                                 double alpha, double coef1, __nv_bfloat16* __restrict__ Chi,
+                                 __nv_bfloat16* __restrict__ Clo, float* __restrict__ P) {
+  const int b = blockIdx.y;
+  const int64_t total = static_cast<int64_t>(h) * h;
+  const double inv_s2 = 1.0 / scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_S2];
+  const int64_t off = static_cast<int64_t>(b) * h * ld;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / h, c = i - r * h, o = off + r * ld + c;
+    const float cv = static_cast<float>(static_cast<double>(G[o]) * inv_s2);
+    __nv_bfloat16 hi, lo;
+    split_bf16(cv, hi, lo);
+    Chi[o] = hi;
+    Clo[o] = lo;
+    P[o] = static_cast<float>((r == c ? alpha : 0.0) - coef1 * static_cast<double>(cv));
+  }
+}
+
+// ------------------------------------------------------------------ P finalisation
+// Reads the upper triangle of P (the only part the chain epilogues maintain),
+// scales by 1/s (ortho.py:167 folded into the apply) and writes it symmetric.
+template <int OUT>  // 0: f64 full, 1: bf16 hi/lo full
+__global__ void finalize_p_kernel(const void* __restrict__ Pin, int h, int64_t ld, const double* __restrict__ scal,
+                                  void* __restrict__ out0, void* __restrict__ out1) {
+  __shared__ double tile[32][33];
+  const int nt = (h + 31) / 32;
+  int ti, tj;
+  sym_tile_coords(blockIdx.x, nt, ti, tj);
+  const int b = blockIdx.y;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t off = static_cast<int64_t>(b) * h * ld;
+  const double inv_s = scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_INV_S];
+  for (int r = ty; r < 32; r += 8) {
+    const int gr = ti * 32 + r, gc = tj * 32 + tx;
+    double v = 0.0;
+    if (gr < h && gc < h) {
+      const int64_t o = off + static_cast<int64_t>(gr) * ld + gc;
+      v = OUT == 0 ? static_cast<const double*>(Pin)[o] : static_cast<double>(static_cast<const float*>(Pin)[o]);
+    }
+    tile[r][tx] = v * inv_s;
+  }
+  __syncthreads();
+  auto put = [&](int gr, int gc, double v) {
+    const int64_t o = off + static_cast<int64_t>(gr) * ld + gc;
+    if (OUT == 0) {
+      static_cast<double*>(out0)[o] = v;
+    } else {
+      __nv_bfloat16 hi, lo;
+      split_bf16(static_cast<float>(v), hi, lo);
+      static_cast<__nv_bfloat16*>(out0)[o] = hi;
+      static_cast<__nv_bfloat16*>(out1)[o] = lo;
+    }
+  };
+  for (int r = ty; r < 32; r += 8) {
+    const int gr = ti * 32 + r, gc = tj * 32 + tx;
+    if (gr < h && gc < h) put(gr, gc, (ti == tj && r > tx) ? tile[tx][r] : tile[r][tx]);
+    if (ti != tj) {
+      const int mr = tj * 32 + r, mc = ti * 32 + tx;
+      if (mr < h && mc < h) put(mr, mc, tile[tx][r]);
+    }
+  }
+}
+
+}  // namespace unso

@@ -1,0 +1,916 @@
+// B200-native UNSO orthogonalization: host orchestration + C ABI (include/unso_b200.h).
+//
+// Reference path (arXiv 2602.02500, /root/reference/pkg/src/unso/ortho.py):
+//   preprocess (:140-168) -> unso (:171-205) | original_ns (:208-218) | _quintic_steps (:221-231)
+// Device pipeline for UNSO (one stream, no host syncs):
+//   [convert]  X -> bf16 copy (BF16 precision with f32 input only)
+//   K1  Gram SYRK over the long side, split-K partials        (ortho.py:156/198 computed ONCE)
+//       finalize: sum partials, mirror                          (deterministic fixed order)
+//       norms + scalars: trace, ||G||_F -> s^2, 1/s, status     (ortho.py:147-165)
+//       prep: C_1 = G/s^2, P = alpha I - a_1 C_1                 (C-form of ortho.py:199-202)
+//   K2  13 x chain SYRK  C_{k+1} = 2 C_k - C_k^2, P -= c_{k+1} C_{k+1}   (ortho.py:201-204)
+//       finalize P: P/s, symmetric, split for the apply          (ortho.py:167 folded)
+//   K3  apply Y = X P (tall) or P X (wide), written in the input dtype   (ortho.py:205, :275-276)
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/unso_b200.h"
+#include "common.cuh"
+#include "elementwise.cuh"
+#include "simt_gemm.cuh"
+#include "umma_gemm.cuh"
+
+#define UNSO_VERSION_STRING "unso_b200 0.1.0 (sm_100a: tcgen05/TMEM/TMA bf16 path + fp64 DFMA parity path)"
+
+namespace unso {
+
+static thread_local int g_launches = 0;
+
+#define UNSO_CHECK_LAUNCH()                          \
+  do {                                               \
+    ++g_launches;                                    \
+    cudaError_t e__ = cudaGetLastError();            \
+    if (e__ != cudaSuccess) return UNSO_ERR_CUDA;    \
+  } while (0)
+
+#define UNSO_TRY(expr)                               \
+  do {                                               \
+    int32_t s__ = (expr);                            \
+    if (s__ != UNSO_OK) return s__;                  \
+  } while (0)
+
+// ==================================================================== tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = []() -> EncodeTiledFn {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+static bool make_map(CUtensorMap* m, const void* base, cuuint64_t d0, cuuint64_t d1, cuuint64_t d2, int64_t ld,
+                     int64_t bstride, cuuint32_t b0, cuuint32_t b1) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(bstride) * 2};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool umma_make_kmajor_map(CUtensorMap* m, const void* base, int64_t rows, int64_t k, int64_t ld, int64_t batch,
+                          int64_t bstride, int box_rows) {
+  if (batch <= 1) bstride = rows * ld;
+  return make_map(m, base, k, rows, batch, ld, bstride, 64, box_rows);
+}
+
+bool umma_make_mnmajor_map(CUtensorMap* m, const void* base, int64_t krows, int64_t mn, int64_t ld, int64_t batch,
+                           int64_t bstride) {
+  if (batch <= 1) bstride = krows * ld;
+  return make_map(m, base, mn, krows, batch, ld, bstride, 64, 64);
+}
+
+int device_sm_count() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  static int cached_dev = -1, cached = 148;
+  if (dev != cached_dev) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached = n;
+    cached_dev = dev;
+  }
+  return cached;
+}
+
+// ==================================================================== epilogues
+// --- SIMT (per element, n >= m on SYRK) ------------------------------------------
+struct EpiPartialF64 {
+  double* part;
+  int64_t bs;  // per matrix
+  int64_t ld;
+  int batch;
+  __device__ void operator()(int b, int split, int m, int n, double acc) const {
+    part[(static_cast<int64_t>(split) * batch + b) * bs + static_cast<int64_t>(m) * ld + n] = acc;
+  }
+};
+
+// C-form squaring step: C' = 2C - C^2 (the reference's B' = B^2 with B = I - C), P -= coef C'
+struct EpiChainF64 {
+  const double* cur;
+  double* nxt;
+  double* P;
+  int64_t ld, bs;
+  double coef;
+  int write_next;
+  __device__ void operator()(int b, int, int m, int n, double acc) const {
+    const int64_t base = static_cast<int64_t>(b) * bs;
+    const int64_t o = base + static_cast<int64_t>(m) * ld + n;
+    const double cn = 2.0 * cur[o] - acc;
+    if (write_next) {
+      nxt[o] = cn;
+      nxt[base + static_cast<int64_t>(n) * ld + m] = cn;
+    }
+    P[o] -= coef * cn;
+  }
+};
+
+// B = bq G + cq G^2 (quintic step operator, ortho.py:226-230 regrouped), symmetric
+struct EpiQuinticB {
+  const double* G;
+  double* Bm;
+  int64_t ld, bs;
+  double bq, cq;
+  __device__ void operator()(int b, int, int m, int n, double acc) const {
+    const int64_t base = static_cast<int64_t>(b) * bs;
+    const double v = bq * G[base + static_cast<int64_t>(m) * ld + n] + cq * acc;
+    Bm[base + static_cast<int64_t>(m) * ld + n] = v;
+    Bm[base + static_cast<int64_t>(n) * ld + m] = v;
+  }
+};
+
+// out = alpha * acc + beta * old  (old may be null)
+struct EpiOut {
+  void* out;
+  int dt;
+  int64_t ld, bs;
+  const double* old;
+  int64_t old_ld, old_bs;
+  double alpha, beta;
+  __device__ void operator()(int b, int, int m, int n, double acc) const {
+    double v = alpha * acc;
+    if (old) v += beta * old[static_cast<int64_t>(b) * old_bs + static_cast<int64_t>(m) * old_ld + n];
+    store_from_f64(out, static_cast<int64_t>(b) * bs + static_cast<int64_t>(m) * ld + n, dt, v);
+  }
+};
+
+// --- tcgen05 (per row, 32 consecutive columns) ---------------------------------------
+struct UEpiPartialF32 {
+  float* part;
+  int64_t bs, ld;
+  int batch, h;
+  __device__ void operator()(int b, int split, int row, int col0, const float* v) const {
+    if (row >= h) return;
+    float* dst = part + (static_cast<int64_t>(split) * batch + b) * bs + static_cast<int64_t>(row) * ld + col0;
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+  }
+};
+
+struct UEpiChainBF16 {
+  const __nv_bfloat16* chi;
+  const __nv_bfloat16* clo;
+  __nv_bfloat16* nhi;
+  __nv_bfloat16* nlo;
+  float* P;
+  int64_t ld, bs;
+  int h;
+  float coef;
+  int write_next;
+  __device__ void operator()(int b, int, int row, int col0, const float* v) const {
+    if (row >= h || col0 + 31 < row) return;
+    const int64_t base = static_cast<int64_t>(b) * bs;
+    const int64_t o = base + static_cast<int64_t>(row) * ld + col0;
+    __align__(16) __nv_bfloat16 hi[32];
+    __align__(16) __nv_bfloat16 lo[32];
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      *reinterpret_cast<uint4*>(hi + j) = *reinterpret_cast<const uint4*>(chi + o + j);
+      *reinterpret_cast<uint4*>(lo + j) = *reinterpret_cast<const uint4*>(clo + o + j);
+    }
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const int col = col0 + j;
+      if (col < row || col >= h) continue;
+      const float c = __bfloat162float(hi[j]) + __bfloat162float(lo[j]);
+      const float cn = 2.0f * c - v[j];
+      if (write_next) {
+        __nv_bfloat16 h2, l2;
+        split_bf16(cn, h2, l2);
+        nhi[o + j] = h2;
+        nlo[o + j] = l2;
+        if (col != row) {
+          const int64_t t = base + static_cast<int64_t>(col) * ld + row;
+          nhi[t] = h2;
+          nlo[t] = l2;
+        }
+      }
+      P[o + j] -= coef * cn;
+    }
+  }
+};
+
+struct UEpiOut {
+  void* out;
+  int dt;  // DT_BF16 or DT_F32
+  int64_t ld, bs;
+  int M, N;
+  __device__ void operator()(int b, int, int row, int col0, const float* v) const {
+    if (row >= M) return;
+    const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + col0;
+    if (dt == DT_BF16) {
+      __nv_bfloat16* y = static_cast<__nv_bfloat16*>(out) + o;
+      if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          __align__(16) __nv_bfloat162 p[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) p[q] = __floats2bfloat162_rn(v[j + 2 * q], v[j + 2 * q + 1]);
+          *reinterpret_cast<uint4*>(y + j) = *reinterpret_cast<uint4*>(p);
+        }
+      } else {
+        for (int j = 0; j < 32 && col0 + j < N; ++j) y[j] = __float2bfloat16_rn(v[j]);
+      }
+    } else {
+      float* y = static_cast<float*>(out) + o;
+      if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(y + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+        for (int j = 0; j < 32 && col0 + j < N; ++j) y[j] = v[j];
+      }
+    }
+  }
+};
+
+// tcgen05 configurations
+using CfgGramK = UmmaCfg<128, 1, 1, 1, TERM(0, 0, 0), false, false, 6>;
+using CfgGramMN = UmmaCfg<128, 1, 1, 1, TERM(0, 0, 0), true, true, 6>;
+// bf16x3: hi*hi + hi*lo + lo*hi
+using CfgChain = UmmaCfg<128, 2, 2, 3, TERM(0, 0, 0) | TERM(1, 0, 1) | TERM(2, 1, 0), false, false, 3>;
+// tall apply: X * (P_hi + P_lo)
+using CfgApplyTall2 = UmmaCfg<128, 1, 2, 2, TERM(0, 0, 0) | TERM(1, 0, 1), false, false, 4>;
+using CfgApplyTall1 = UmmaCfg<128, 1, 1, 1, TERM(0, 0, 0), false, false, 6>;
+// wide apply: (P_hi + P_lo) * X, X read MN-major
+using CfgApplyWide2 = UmmaCfg<128, 2, 1, 2, TERM(0, 0, 0) | TERM(1, 1, 0), false, true, 4>;
+using CfgApplyWide1 = UmmaCfg<128, 1, 1, 1, TERM(0, 0, 0), false, true, 6>;
+
+// ==================================================================== problem + workspace plan
+static inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+struct Problem {
+  int64_t rows, cols, ld, batch, bs;
+  int dt;
+  bool tall;
+  int64_t h, w;
+  int method, scaling, gpow, prec, order, steps, flags;
+  std::vector<double> co;
+};
+
+static int32_t make_problem(const unso_matrix_desc* x, const unso_method_desc* m, Problem& p, bool need_method = true) {
+  if (!x) return UNSO_ERR_VALUE;
+  if (x->rows < 1 || x->cols < 1 || x->batch < 1 || x->ld < x->cols) return UNSO_ERR_SHAPE;
+  if (x->dtype != UNSO_DTYPE_F32 && x->dtype != UNSO_DTYPE_BF16 && x->dtype != UNSO_DTYPE_F64) return UNSO_ERR_VALUE;
+  if (x->rows > (1 << 30) || x->cols > (1 << 30)) return UNSO_ERR_SHAPE;
+  p.rows = x->rows;
+  p.cols = x->cols;
+  p.ld = x->ld;
+  p.batch = x->batch;
+  p.bs = x->batch > 1 ? x->batch_stride : x->rows * x->ld;
+  if (x->batch > 1 && x->batch_stride < x->rows * x->ld) return UNSO_ERR_SHAPE;
+  p.dt = x->dtype;
+  p.tall = x->rows > x->cols;  // ortho.py:149 (square is not transposed)
+  p.h = p.tall ? x->cols : x->rows;
+  p.w = p.tall ? x->rows : x->cols;
+  if (p.h > 65536) return UNSO_ERR_UNSUPPORTED;
+  if (!need_method) return UNSO_OK;
+  if (!m) return UNSO_ERR_VALUE;
+  p.method = m->method;
+  p.scaling = m->scaling;
+  p.gpow = m->gelfand_power;
+  p.prec = m->precision;
+  p.order = m->order;
+  p.steps = m->steps;
+  p.flags = m->flags;
+  if (p.scaling < 0 || p.scaling > 3 || p.gpow < 1) return UNSO_ERR_VALUE;
+  if (p.prec != UNSO_PREC_FP32 && p.prec != UNSO_PREC_BF16) return UNSO_ERR_VALUE;
+  if (p.method == UNSO_METHOD_UNSO) {
+    if (p.order < 1 || !m->coeffs) return UNSO_ERR_VALUE;
+    p.co.assign(m->coeffs, m->coeffs + p.order);
+  } else if (p.method == UNSO_METHOD_ORIGINAL_NS) {
+    if (p.steps < 1) return UNSO_ERR_VALUE;
+  } else if (p.method == UNSO_METHOD_QUINTIC) {
+    if (p.steps < 1 || !m->coeffs) return UNSO_ERR_VALUE;
+    p.co.assign(m->coeffs, m->coeffs + 3 * static_cast<int64_t>(p.steps));
+  } else {
+    return UNSO_ERR_VALUE;
+  }
+  for (double v : p.co)
+    if (!std::isfinite(v)) return UNSO_ERR_VALUE;
+  if (p.method != UNSO_METHOD_UNSO && p.prec == UNSO_PREC_BF16) return UNSO_ERR_UNSUPPORTED;
+  return UNSO_OK;
+}
+
+struct Plan {
+  int64_t ldc;    // leading dimension of every h x h workspace matrix
+  int64_t hh;     // h * ldc (per matrix)
+  int64_t ldx;    // leading dim of the bf16 X copy
+  int splits;
+  bool xcopy;     // BF16: X needs a bf16 (re-)layout copy
+  size_t total = 0;
+  size_t xb = 0, part = 0, G = 0, blk = 0, scal = 0;
+  size_t C[2] = {0, 0}, P = 0, Pout = 0;          // FP32
+  size_t Chi[2] = {0, 0}, Clo[2] = {0, 0}, Phi = 0, Plo = 0;  // BF16 (P reused as f32)
+  size_t Gk[2] = {0, 0};                          // gelfand powers
+  size_t Xs[2] = {0, 0};                          // NS state (f64)
+};
+
+static size_t take(Plan& pl, size_t bytes) {
+  const size_t off = pl.total;
+  pl.total += (bytes + 255) / 256 * 256;
+  return off;
+}
+
+static int gram_splits(const Problem& p) {
+  if (p.prec == UNSO_PREC_BF16) {
+    const int64_t t = (p.h + 127) / 128;
+    const int64_t tiles = t * (t + 1) / 2 * p.batch;
+    const int64_t kt = (p.w + 63) / 64;
+    int64_t s = (2 * 148 + tiles - 1) / tiles;
+    if (s > kt / 4) s = kt / 4;
+    if (s < 1) s = 1;
+    if (s > 32) s = 32;
+    return static_cast<int>(s);
+  }
+  const int64_t t = (p.h + SIMT_BM - 1) / SIMT_BM;
+  return simt_pick_splits(static_cast<int>(t * (t + 1) / 2), static_cast<int>(p.batch), static_cast<int>(p.w));
+}
+
+static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) {
+  Plan pl;
+  pl.ldc = round_up(p.h, 128);
+  pl.hh = p.h * pl.ldc;
+  const int64_t B = p.batch;
+  const bool bf = !for_error && p.prec == UNSO_PREC_BF16;
+  const size_t ge = bf ? 4 : 8;  // Gram element size
+  pl.splits = with_gram ? gram_splits(p) : 1;
+  pl.ldx = p.ld;
+  pl.xcopy = false;
+  if (bf) {
+    pl.xcopy = p.dt != UNSO_DTYPE_BF16 || (p.ld % 8) != 0 || (p.batch > 1 && (p.bs % 8) != 0);
+    if (pl.xcopy) {
+      pl.ldx = round_up(p.cols, 8);
+      pl.xb = take(pl, static_cast<size_t>(B * p.rows * pl.ldx) * 2);
+    }
+  }
+  if (with_gram) pl.part = take(pl, static_cast<size_t>(pl.splits) * B * pl.hh * ge);
+  pl.G = take(pl, static_cast<size_t>(B * pl.hh) * ge);
+  pl.blk = take(pl, static_cast<size_t>(B) * NORM_BLOCKS * 3 * 8);
+  pl.scal = take(pl, static_cast<size_t>(B) * SCAL_STRIDE * 8);
+  if (for_error) return pl;
+  if (p.scaling == UNSO_SCALING_GELFAND && p.gpow > 1) {
+    pl.Gk[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
+    pl.Gk[1] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
+  }
+  if (p.method == UNSO_METHOD_UNSO) {
+    if (bf) {
+      for (int i = 0; i < 2; ++i) {
+        pl.Chi[i] = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+        pl.Clo[i] = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+      }
+      pl.P = take(pl, static_cast<size_t>(B * pl.hh) * 4);
+      pl.Phi = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+      pl.Plo = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+    } else {
+      pl.C[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
+      pl.C[1] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
+      pl.P = take(pl, static_cast<size_t>(B * pl.hh) * 8);
+      pl.Pout = take(pl, static_cast<size_t>(B * pl.hh) * 8);
+    }
+  } else {
+    pl.Xs[0] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 8);
+    pl.Xs[1] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 8);
+    pl.C[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);  // quintic operator B
+  }
+  return pl;
+}
+
+template <typename T>
+static T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+static int grid_for(int64_t n, int per_block = 256, int max_blocks = 148 * 8) {
+  int64_t g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return static_cast<int>(g);
+}
+
+// ==================================================================== stages
+// Gram partials of X (orientation per p.tall) with fp64 accumulation -> part (f64).
+static int32_t gram_simt(const Problem& p, const void* x, int dt, int64_t ld, int64_t bs, const Plan& pl, void* ws,
+                         int splits, cudaStream_t st) {
+  SimtOperand X{x, ld, bs, dt, p.tall ? 0 : 1};
+  EpiPartialF64 epi{at<double>(ws, pl.part), pl.hh, pl.ldc, static_cast<int>(p.batch)};
+  if (launch_simt_gemm(X, X, static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w),
+                       static_cast<int>(p.batch), true, splits, epi, st) != cudaSuccess)
+    return UNSO_ERR_CUDA;
+  ++g_launches;
+  return UNSO_OK;
+}
+
+template <typename T>
+static int32_t finalize_gram(const Problem& p, const Plan& pl, void* ws, int splits, T* G, cudaStream_t st) {
+  const int nt = static_cast<int>((p.h + 31) / 32);
+  dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
+  finalize_sum_kernel<T><<<grid, 256, 0, st>>>(at<T>(ws, pl.part), splits, static_cast<int>(p.batch),
+                                                static_cast<int>(p.h), pl.ldc, G);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+template <typename T>
+static int32_t norms_and_scalars(const Problem& p, const Plan& pl, void* ws, const T* G, int mode, int32_t* status,
+                                 cudaStream_t st) {
+  dim3 grid(NORM_BLOCKS, static_cast<unsigned>(p.batch));
+  gram_norms_kernel<T><<<grid, 256, 0, st>>>(G, static_cast<int>(p.h), pl.ldc, at<double>(ws, pl.blk));
+  UNSO_CHECK_LAUNCH();
+  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, mode, p.gpow,
+                                                                  at<double>(ws, pl.scal), status);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+// Gelfand denominator ||G^k||_F^(1/2k) (ortho.py:158-163): powers on the fp64 engine.
+template <typename T>
+static int32_t gelfand_scale(const Problem& p, const Plan& pl, void* ws, const T* G, int gdt, int32_t* status,
+                             cudaStream_t st) {
+  if (p.gpow <= 1) return UNSO_OK;  // k = 1: ||G||_F^(1/2) == gram scaling, already computed
+  const int h = static_cast<int>(p.h);
+  SimtOperand Gop{G, pl.ldc, pl.hh, gdt, 1};
+  const void* prev = G;
+  int prev_dt = gdt;
+  int cur = 0;
+  for (int j = 2; j <= p.gpow; ++j) {
+    SimtOperand A{prev, pl.ldc, pl.hh, prev_dt, 1};
+    EpiOut epi{at<double>(ws, pl.Gk[cur]), DT_F64, pl.ldc, pl.hh, nullptr, 0, 0, 1.0, 0.0};
+    if (launch_simt_gemm(A, Gop, h, h, h, static_cast<int>(p.batch), false, 1, epi, st) != cudaSuccess)
+      return UNSO_ERR_CUDA;
+    ++g_launches;
+    prev = at<double>(ws, pl.Gk[cur]);
+    prev_dt = DT_F64;
+    cur ^= 1;
+  }
+  dim3 grid(NORM_BLOCKS, static_cast<unsigned>(p.batch));
+  gram_norms_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(prev), h, pl.ldc, at<double>(ws, pl.blk));
+  UNSO_CHECK_LAUNCH();
+  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, SM_GELFAND,
+                                                                  p.gpow, at<double>(ws, pl.scal), status);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+static int scal_mode(int scaling) {
+  return scaling == UNSO_SCALING_PLAIN ? SM_PLAIN : (scaling == UNSO_SCALING_NONE ? SM_NONE : SM_GRAM);
+}
+
+// ---------------------------------------------------------------- UNSO, FP32 precision
+static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, const void* x, const double* G, void* y,
+                                int32_t* status, cudaStream_t st) {
+  UNSO_TRY(norms_and_scalars<double>(p, pl, ws, G, scal_mode(p.scaling), status, st));
+  if (p.scaling == UNSO_SCALING_GELFAND) UNSO_TRY(gelfand_scale<double>(p, pl, ws, G, DT_F64, status, st));
+  const int h = static_cast<int>(p.h);
+  const int N = p.order;
+  double alpha = 1.0;
+  for (double v : p.co) alpha += v;
+  {
+    dim3 grid(grid_for(static_cast<int64_t>(h) * h, 256, 1024), static_cast<unsigned>(p.batch));
+    prep_f64_kernel<double><<<grid, 256, 0, st>>>(G, h, pl.ldc, at<double>(ws, pl.scal), alpha, p.co[0],
+                                                  at<double>(ws, pl.C[0]), at<double>(ws, pl.P));
+    UNSO_CHECK_LAUNCH();
+  }
+  int cur = 0;
+  for (int k = 1; k < N; ++k) {  // produces C_{k+1}
+    SimtOperand C{at<double>(ws, pl.C[cur]), pl.ldc, pl.hh, DT_F64, 1};
+    EpiChainF64 epi{at<double>(ws, pl.C[cur]), at<double>(ws, pl.C[cur ^ 1]), at<double>(ws, pl.P), pl.ldc, pl.hh,
+                    p.co[k], k + 1 < N ? 1 : 0};
+    const int t = (h + SIMT_BM - 1) / SIMT_BM;
+    const int splits = 1;
+    (void)t;
+    if (launch_simt_gemm(C, C, h, h, h, static_cast<int>(p.batch), true, splits, epi, st) != cudaSuccess)
+      return UNSO_ERR_CUDA;
+    ++g_launches;
+    cur ^= 1;
+  }
+  {
+    const int nt = (h + 31) / 32;
+    dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
+    finalize_p_kernel<0><<<grid, 256, 0, st>>>(at<double>(ws, pl.P), h, pl.ldc, at<double>(ws, pl.scal),
+                                               at<double>(ws, pl.Pout), nullptr);
+    UNSO_CHECK_LAUNCH();
+  }
+  // apply: tall Y = X P (A = X K-major over w rows), wide Y = P X (B = X MN-major)
+  SimtOperand Xop{x, p.ld, p.bs, p.dt, 1};
+  SimtOperand Pop{at<double>(ws, pl.Pout), pl.ldc, pl.hh, DT_F64, 1};
+  EpiOut epi{y, p.dt, p.cols, p.rows * p.cols, nullptr, 0, 0, 1.0, 0.0};
+  cudaError_t e;
+  if (p.tall) {
+    e = launch_simt_gemm(Xop, Pop, static_cast<int>(p.rows), h, h, static_cast<int>(p.batch), false, 1, epi, st);
+  } else {
+    Xop.kmajor = 0;
+    e = launch_simt_gemm(Pop, Xop, h, static_cast<int>(p.cols), h, static_cast<int>(p.batch), false, 1, epi, st);
+  }
+  if (e != cudaSuccess) return UNSO_ERR_CUDA;
+  ++g_launches;
+  return UNSO_OK;
+}
+
+// ---------------------------------------------------------------- UNSO, BF16 precision (tcgen05)
+static int32_t ensure_bf16_x(const Problem& p, const Plan& pl, void* ws, const void* x, const __nv_bfloat16*& xb,
+                             int64_t& ldx, int64_t& bsx, cudaStream_t st) {
+  if (!pl.xcopy) {
+    xb = static_cast<const __nv_bfloat16*>(x);
+    ldx = p.ld;
+    bsx = p.bs;
+    return UNSO_OK;
+  }
+  __nv_bfloat16* dst = at<__nv_bfloat16>(ws, pl.xb);
+  ldx = pl.ldx;
+  bsx = p.rows * pl.ldx;
+  const int64_t n = p.batch * p.rows * p.cols;
+  if (p.dt == UNSO_DTYPE_F32 && p.cols % 4 == 0 && p.ld % 4 == 0 && p.bs % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    f32_to_bf16_kernel<<<grid_for(n / 4), 256, 0, st>>>(static_cast<const float*>(x), p.ld, p.bs, dst, ldx, bsx,
+                                                          p.rows, p.cols, static_cast<int>(p.batch));
+  } else {
+    convert_kernel<<<grid_for(n), 256, 0, st>>>(x, p.dt, p.ld, p.bs, dst, DT_BF16, ldx, bsx, p.rows, p.cols,
+                                                static_cast<int>(p.batch), nullptr);
+  }
+  UNSO_CHECK_LAUNCH();
+  xb = dst;
+  return UNSO_OK;
+}
+
+static int32_t gram_bf16(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
+                         int64_t bsx, cudaStream_t st) {
+  CUtensorMap mx;
+  UmmaWork w = umma_make_work(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 128,
+                              static_cast<int>(p.batch), true, pl.splits);
+  UEpiPartialF32 epi{at<float>(ws, pl.part), pl.hh, pl.ldc, static_cast<int>(p.batch), static_cast<int>(p.h)};
+  cudaError_t e;
+  if (p.tall) {
+    if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
+    e = launch_umma<CfgGramMN>(mx, mx, mx, mx, w, epi, st);
+  } else {
+    if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx, 128)) return UNSO_ERR_CUDA;
+    e = launch_umma<CfgGramK>(mx, mx, mx, mx, w, epi, st);
+  }
+  if (e != cudaSuccess) return UNSO_ERR_CUDA;
+  ++g_launches;
+  return UNSO_OK;
+}
+
+static int32_t unso_bf16_from_G(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
+                                int64_t bsx, const float* G, void* y, int32_t* status, cudaStream_t st) {
+  UNSO_TRY(norms_and_scalars<float>(p, pl, ws, G, scal_mode(p.scaling), status, st));
+  if (p.scaling == UNSO_SCALING_GELFAND) UNSO_TRY(gelfand_scale<float>(p, pl, ws, G, DT_F32, status, st));
+  const int h = static_cast<int>(p.h);
+  const int N = p.order;
+  double alpha = 1.0;
+  for (double v : p.co) alpha += v;
+  {
+    dim3 grid(grid_for(static_cast<int64_t>(h) * h, 256, 1024), static_cast<unsigned>(p.batch));
+    prep_bf16_kernel<<<grid, 256, 0, st>>>(G, h, pl.ldc, at<double>(ws, pl.scal), alpha, p.co[0],
+                                           at<__nv_bfloat16>(ws, pl.Chi[0]), at<__nv_bfloat16>(ws, pl.Clo[0]),
+                                           at<float>(ws, pl.P));
+    UNSO_CHECK_LAUNCH();
+  }
+  int cur = 0;
+  const UmmaWork wc = umma_make_work(h, h, h, 128, static_cast<int>(p.batch), true, 1);
+  for (int k = 1; k < N; ++k) {
+    CUtensorMap mh, ml;
+    if (!umma_make_kmajor_map(&mh, at<__nv_bfloat16>(ws, pl.Chi[cur]), h, h, pl.ldc, p.batch, pl.hh, 128) ||
+        !umma_make_kmajor_map(&ml, at<__nv_bfloat16>(ws, pl.Clo[cur]), h, h, pl.ldc, p.batch, pl.hh, 128))
+      return UNSO_ERR_CUDA;
+    UEpiChainBF16 epi{at<__nv_bfloat16>(ws, pl.Chi[cur]), at<__nv_bfloat16>(ws, pl.Clo[cur]),
+                      at<__nv_bfloat16>(ws, pl.Chi[cur ^ 1]), at<__nv_bfloat16>(ws, pl.Clo[cur ^ 1]),
+                      at<float>(ws, pl.P), pl.ldc, pl.hh, h, static_cast<float>(p.co[k]), k + 1 < N ? 1 : 0};
+    if (launch_umma<CfgChain>(mh, ml, mh, ml, wc, epi, st) != cudaSuccess) return UNSO_ERR_CUDA;
+    ++g_launches;
+    cur ^= 1;
+  }
+  {
+    const int nt = (h + 31) / 32;
+    dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
+    finalize_p_kernel<1><<<grid, 256, 0, st>>>(at<float>(ws, pl.P), h, pl.ldc, at<double>(ws, pl.scal),
+                                               at<__nv_bfloat16>(ws, pl.Phi), at<__nv_bfloat16>(ws, pl.Plo));
+    UNSO_CHECK_LAUNCH();
+  }
+  const bool single = (p.flags & UNSO_FLAG_SINGLE_TERM_APPLY) != 0;
+  CUtensorMap mx, mph, mpl;
+  if (!umma_make_kmajor_map(&mph, at<__nv_bfloat16>(ws, pl.Phi), h, h, pl.ldc, p.batch, pl.hh, 128) ||
+      !umma_make_kmajor_map(&mpl, at<__nv_bfloat16>(ws, pl.Plo), h, h, pl.ldc, p.batch, pl.hh, 128))
+    return UNSO_ERR_CUDA;
+  const int ydt = p.dt == UNSO_DTYPE_BF16 ? DT_BF16 : DT_F32;
+  cudaError_t e;
+  if (p.tall) {
+    if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx, 128)) return UNSO_ERR_CUDA;
+    const UmmaWork wa = umma_make_work(static_cast<int>(p.rows), h, h, 128, static_cast<int>(p.batch), false, 1);
+    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, static_cast<int>(p.rows), h};
+    e = single ? launch_umma<CfgApplyTall1>(mx, mx, mph, mph, wa, epi, st)
+               : launch_umma<CfgApplyTall2>(mx, mx, mph, mpl, wa, epi, st);
+  } else {
+    if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
+    const UmmaWork wa = umma_make_work(h, static_cast<int>(p.cols), h, 128, static_cast<int>(p.batch), false, 1);
+    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, h, static_cast<int>(p.cols)};
+    e = single ? launch_umma<CfgApplyWide1>(mph, mph, mx, mx, wa, epi, st)
+               : launch_umma<CfgApplyWide2>(mph, mpl, mx, mx, wa, epi, st);
+  }
+  if (e != cudaSuccess) return UNSO_ERR_CUDA;
+  ++g_launches;
+  return UNSO_OK;
+}
+
+// ---------------------------------------------------------------- NS baselines (FP32 precision)
+static int32_t ns_fp32(const Problem& p, const Plan& pl, void* ws, const void* x, void* y, int32_t* status,
+                       cudaStream_t st) {
+  const int64_t B = p.batch;
+  const int h = static_cast<int>(p.h);
+  const int64_t xsz = p.rows * p.cols;
+  // scale (preprocess, ortho.py:140-168)
+  const double* xscale = at<double>(ws, pl.scal);
+  if (p.scaling == UNSO_SCALING_NONE) {
+    xscale = nullptr;
+  } else if (p.scaling == UNSO_SCALING_PLAIN) {
+    dim3 grid(NORM_BLOCKS, static_cast<unsigned>(B));
+    sumsq_kernel<<<grid, 256, 0, st>>>(x, p.dt, p.rows, p.cols, p.ld, p.bs, at<double>(ws, pl.blk));
+    UNSO_CHECK_LAUNCH();
+    scalars_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, SM_PLAIN, p.gpow,
+                                                            at<double>(ws, pl.scal), status);
+    UNSO_CHECK_LAUNCH();
+  } else {
+    UNSO_TRY(gram_simt(p, x, p.dt, p.ld, p.bs, pl, ws, pl.splits, st));
+    UNSO_TRY(finalize_gram<double>(p, pl, ws, pl.splits, at<double>(ws, pl.G), st));
+    UNSO_TRY(norms_and_scalars<double>(p, pl, ws, at<double>(ws, pl.G), SM_GRAM, status, st));
+    if (p.scaling == UNSO_SCALING_GELFAND)
+      UNSO_TRY(gelfand_scale<double>(p, pl, ws, at<double>(ws, pl.G), DT_F64, status, st));
+  }
+  convert_kernel<<<grid_for(B * xsz), 256, 0, st>>>(x, p.dt, p.ld, p.bs, at<double>(ws, pl.Xs[0]), DT_F64, p.cols, xsz,
+                                                    p.rows, p.cols, static_cast<int>(B), xscale);
+  UNSO_CHECK_LAUNCH();
+  int cur = 0;
+  const int iters = p.steps;
+  for (int it = 0; it < iters; ++it) {
+    const double* X = at<double>(ws, pl.Xs[cur]);
+    UNSO_TRY(gram_simt(p, X, DT_F64, p.cols, xsz, pl, ws, pl.splits, st));
+    UNSO_TRY(finalize_gram<double>(p, pl, ws, pl.splits, at<double>(ws, pl.G), st));
+    const double* Bop = at<double>(ws, pl.G);
+    double a_c, alpha;
+    if (p.method == UNSO_METHOD_ORIGINAL_NS) {  // X <- 1.5 X - 0.5 G X (ortho.py:215-217)
+      a_c = 1.5;
+      alpha = -0.5;
+    } else {  // X <- a X + (b G + c G^2) X (ortho.py:226-230)
+      a_c = p.co[3 * it + 0];
+      alpha = 1.0;
+      SimtOperand Gop{at<double>(ws, pl.G), pl.ldc, pl.hh, DT_F64, 1};
+      EpiQuinticB epi{at<double>(ws, pl.G), at<double>(ws, pl.C[0]), pl.ldc, pl.hh, p.co[3 * it + 1],
+                      p.co[3 * it + 2]};
+      if (launch_simt_gemm(Gop, Gop, h, h, h, static_cast<int>(B), true, 1, epi, st) != cudaSuccess)
+        return UNSO_ERR_CUDA;
+      ++g_launches;
+      Bop = at<double>(ws, pl.C[0]);
+    }
+    SimtOperand Xop{X, p.cols, xsz, DT_F64, 1};
+    SimtOperand Bm{Bop, pl.ldc, pl.hh, DT_F64, 1};
+    EpiOut epi{at<double>(ws, pl.Xs[cur ^ 1]), DT_F64, p.cols, xsz, X, p.cols, xsz, alpha, a_c};
+    cudaError_t e;
+    if (p.tall) {
+      e = launch_simt_gemm(Xop, Bm, static_cast<int>(p.rows), h, h, static_cast<int>(B), false, 1, epi, st);
+    } else {
+      Xop.kmajor = 0;
+      e = launch_simt_gemm(Bm, Xop, h, static_cast<int>(p.cols), h, static_cast<int>(B), false, 1, epi, st);
+    }
+    if (e != cudaSuccess) return UNSO_ERR_CUDA;
+    ++g_launches;
+    cur ^= 1;
+  }
+  convert_kernel<<<grid_for(B * xsz), 256, 0, st>>>(at<double>(ws, pl.Xs[cur]), DT_F64, p.cols, xsz, y, p.dt, p.cols,
+                                                    xsz, p.rows, p.cols, static_cast<int>(B), nullptr);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+static int32_t check_ws(const Plan& pl, void* ws, size_t bytes) {
+  if (bytes < pl.total) return UNSO_ERR_WORKSPACE;
+  if (pl.total > 0 && !ws) return UNSO_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return UNSO_ERR_VALUE;
+  return UNSO_OK;
+}
+
+}  // namespace unso
+
+// ==================================================================== C ABI
+using namespace unso;
+
+extern "C" {
+
+const char* unso_version(void) { return UNSO_VERSION_STRING; }
+
+const char* unso_status_string(int32_t s) {
+  switch (s) {
+    case UNSO_OK: return "ok";
+    case UNSO_ERR_SHAPE: return "shape error";
+    case UNSO_ERR_DEGENERATE: return "degenerate input";
+    case UNSO_ERR_VALUE: return "invalid value";
+    case UNSO_ERR_CUDA: return "CUDA error";
+    case UNSO_ERR_UNSUPPORTED: return "unsupported";
+    case UNSO_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int32_t unso_last_launch_count(void) { return g_launches; }
+
+size_t unso_workspace_size(const unso_matrix_desc* x, const unso_method_desc* method) {
+  Problem p;
+  if (make_problem(x, method, p) != UNSO_OK) return 0;
+  const Plan a = make_plan(p, true);
+  Plan e = make_plan(p, true, true);
+  if (p.scaling == UNSO_SCALING_GELFAND && p.gpow > 1) {
+    take(e, static_cast<size_t>(p.batch * e.hh) * 8);
+    take(e, static_cast<size_t>(p.batch * e.hh) * 8);
+  }
+  return (a.total > e.total ? a.total : e.total) + 256;
+}
+
+int32_t unso_gram_dtype(const unso_method_desc* method) {
+  return (method && method->precision == UNSO_PREC_BF16) ? UNSO_DTYPE_F32 : UNSO_DTYPE_F64;
+}
+
+int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y_ptr, const unso_method_desc* method,
+                           void* workspace, size_t workspace_bytes, int32_t* d_status, void* stream) {
+  g_launches = 0;
+  Problem p;
+  UNSO_TRY(make_problem(x, method, p));
+  if (!x_ptr || !y_ptr) return UNSO_ERR_VALUE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p.method != UNSO_METHOD_UNSO) {
+    const Plan pl = make_plan(p, true);
+    UNSO_TRY(check_ws(pl, workspace, workspace_bytes));
+    return ns_fp32(p, pl, workspace, x_ptr, y_ptr, d_status, st);
+  }
+  const Plan pl = make_plan(p, true);
+  UNSO_TRY(check_ws(pl, workspace, workspace_bytes));
+  if (p.prec == UNSO_PREC_FP32) {
+    UNSO_TRY(gram_simt(p, x_ptr, p.dt, p.ld, p.bs, pl, workspace, pl.splits, st));
+    double* G = at<double>(workspace, pl.G);
+    UNSO_TRY(finalize_gram<double>(p, pl, workspace, pl.splits, G, st));
+    return unso_fp32_from_G(p, pl, workspace, x_ptr, G, y_ptr, d_status, st);
+  }
+  const __nv_bfloat16* xb;
+  int64_t ldx, bsx;
+  UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
+  UNSO_TRY(gram_bf16(p, pl, workspace, xb, ldx, bsx, st));
+  float* G = at<float>(workspace, pl.G);
+  UNSO_TRY(finalize_gram<float>(p, pl, workspace, pl.splits, G, st));
+  return unso_bf16_from_G(p, pl, workspace, xb, ldx, bsx, G, y_ptr, d_status, st);
+}
+
+int32_t unso_gram(const unso_matrix_desc* x, const void* x_ptr, void* g_ptr, const unso_method_desc* method,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  Problem p;
+  UNSO_TRY(make_problem(x, method, p));
+  if (p.method != UNSO_METHOD_UNSO) return UNSO_ERR_UNSUPPORTED;
+  if (!x_ptr || !g_ptr) return UNSO_ERR_VALUE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Plan pl = make_plan(p, true);
+  UNSO_TRY(check_ws(pl, workspace, workspace_bytes));
+  // g_ptr is dense batch x h x h; finalize into the padded workspace G, then compact
+  const int64_t h = p.h;
+  if (p.prec == UNSO_PREC_FP32) {
+    UNSO_TRY(gram_simt(p, x_ptr, p.dt, p.ld, p.bs, pl, workspace, pl.splits, st));
+    UNSO_TRY(finalize_gram<double>(p, pl, workspace, pl.splits, at<double>(workspace, pl.G), st));
+    convert_kernel<<<grid_for(p.batch * h * h), 256, 0, st>>>(at<double>(workspace, pl.G), DT_F64, pl.ldc, pl.hh,
+                                                              g_ptr, DT_F64, h, h * h, h, h,
+                                                              static_cast<int>(p.batch), nullptr);
+    UNSO_CHECK_LAUNCH();
+    return UNSO_OK;
+  }
+  const __nv_bfloat16* xb;
+  int64_t ldx, bsx;
+  UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
+  UNSO_TRY(gram_bf16(p, pl, workspace, xb, ldx, bsx, st));
+  UNSO_TRY(finalize_gram<float>(p, pl, workspace, pl.splits, at<float>(workspace, pl.G), st));
+  convert_kernel<<<grid_for(p.batch * h * h), 256, 0, st>>>(at<float>(workspace, pl.G), DT_F32, pl.ldc, pl.hh, g_ptr,
+                                                            DT_F32, h, h * h, h, h, static_cast<int>(p.batch),
+                                                            nullptr);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+int32_t unso_orthogonalize_from_gram(const unso_matrix_desc* x, const void* x_ptr, const void* g_ptr, void* y_ptr,
+                                     const unso_method_desc* method, void* workspace, size_t workspace_bytes,
+                                     int32_t* d_status, void* stream) {
+  g_launches = 0;
+  Problem p;
+  UNSO_TRY(make_problem(x, method, p));
+  if (p.method != UNSO_METHOD_UNSO) return UNSO_ERR_UNSUPPORTED;
+  if (!x_ptr || !g_ptr || !y_ptr) return UNSO_ERR_VALUE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Plan pl = make_plan(p, false);
+  UNSO_TRY(check_ws(pl, workspace, workspace_bytes));
+  const int64_t h = p.h;
+  // copy the dense reduced Gram into the padded workspace layout
+  if (p.prec == UNSO_PREC_FP32) {
+    convert_kernel<<<grid_for(p.batch * h * h), 256, 0, st>>>(g_ptr, DT_F64, h, h * h, at<double>(workspace, pl.G),
+                                                              DT_F64, pl.ldc, pl.hh, h, h, static_cast<int>(p.batch),
+                                                              nullptr);
+    UNSO_CHECK_LAUNCH();
+    return unso_fp32_from_G(p, pl, workspace, x_ptr, at<double>(workspace, pl.G), y_ptr, d_status, st);
+  }
+  convert_kernel<<<grid_for(p.batch * h * h), 256, 0, st>>>(g_ptr, DT_F32, h, h * h, at<float>(workspace, pl.G), DT_F32,
+                                                            pl.ldc, pl.hh, h, h, static_cast<int>(p.batch), nullptr);
+  UNSO_CHECK_LAUNCH();
+  const __nv_bfloat16* xb;
+  int64_t ldx, bsx;
+  UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
+  return unso_bf16_from_G(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.G), y_ptr, d_status, st);
+}
+
+int32_t unso_scale_denominator(const unso_matrix_desc* x, const void* x_ptr, const unso_method_desc* method,
+                               double* d_denom, void* workspace, size_t workspace_bytes, int32_t* d_status,
+                               void* stream) {
+  g_launches = 0;
+  Problem p;
+  UNSO_TRY(make_problem(x, nullptr, p, false));
+  if (!method || !x_ptr || !d_denom) return UNSO_ERR_VALUE;
+  p.prec = UNSO_PREC_FP32;
+  p.method = UNSO_METHOD_UNSO;
+  p.scaling = method->scaling;
+  p.gpow = method->gelfand_power;
+  if (p.scaling < 0 || p.scaling > 2 || p.gpow < 1) return UNSO_ERR_VALUE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Plan pl = make_plan(p, true, true);
+  Plan plg = pl;
+  if (p.scaling == UNSO_SCALING_GELFAND && p.gpow > 1) {  // room for the power ping-pong
+    plg.Gk[0] = take(plg, static_cast<size_t>(p.batch * pl.hh) * 8);
+    plg.Gk[1] = take(plg, static_cast<size_t>(p.batch * pl.hh) * 8);
+  }
+  UNSO_TRY(check_ws(plg, workspace, workspace_bytes));
+  if (p.scaling == UNSO_SCALING_PLAIN) {
+    dim3 grid(NORM_BLOCKS, static_cast<unsigned>(p.batch));
+    sumsq_kernel<<<grid, 256, 0, st>>>(x_ptr, p.dt, p.rows, p.cols, p.ld, p.bs, at<double>(workspace, pl.blk));
+    UNSO_CHECK_LAUNCH();
+    scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(workspace, pl.blk), NORM_BLOCKS,
+                                                                    SM_PLAIN, 1, at<double>(workspace, pl.scal),
+                                                                    d_status);
+    UNSO_CHECK_LAUNCH();
+  } else {
+    UNSO_TRY(gram_simt(p, x_ptr, p.dt, p.ld, p.bs, pl, workspace, pl.splits, st));
+    UNSO_TRY(finalize_gram<double>(p, pl, workspace, pl.splits, at<double>(workspace, pl.G), st));
+    UNSO_TRY(norms_and_scalars<double>(p, pl, workspace, at<double>(workspace, pl.G), SM_GRAM, d_status, st));
+    if (p.scaling == UNSO_SCALING_GELFAND)
+      UNSO_TRY(gelfand_scale<double>(p, plg, workspace, at<double>(workspace, pl.G), DT_F64, d_status, st));
+  }
+  copy_denom_kernel<<<static_cast<unsigned>((p.batch + 127) / 128), 128, 0, st>>>(at<double>(workspace, pl.scal),
+                                                                                  static_cast<int>(p.batch), d_denom);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+int32_t unso_ortho_error(const unso_matrix_desc* y, const void* y_ptr, double* d_err, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  Problem p;
+  UNSO_TRY(make_problem(y, nullptr, p, false));
+  if (!y_ptr || !d_err) return UNSO_ERR_VALUE;
+  p.prec = UNSO_PREC_FP32;
+  p.method = UNSO_METHOD_UNSO;
+  p.scaling = UNSO_SCALING_GRAM;
+  p.gpow = 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Plan pl = make_plan(p, true, true);
+  UNSO_TRY(check_ws(pl, workspace, workspace_bytes));
+  UNSO_TRY(gram_simt(p, y_ptr, p.dt, p.ld, p.bs, pl, workspace, pl.splits, st));
+  UNSO_TRY(finalize_gram<double>(p, pl, workspace, pl.splits, at<double>(workspace, pl.G), st));
+  dim3 grid(NORM_BLOCKS, static_cast<unsigned>(p.batch));
+  gram_norms_kernel<double><<<grid, 256, 0, st>>>(at<double>(workspace, pl.G), static_cast<int>(p.h), pl.ldc,
+                                                  at<double>(workspace, pl.blk));
+  UNSO_CHECK_LAUNCH();
+  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(workspace, pl.blk), NORM_BLOCKS, SM_ERROR,
+                                                                  1, at<double>(workspace, pl.scal), nullptr);
+  UNSO_CHECK_LAUNCH();
+  copy_err_kernel<<<static_cast<unsigned>((p.batch + 127) / 128), 128, 0, st>>>(at<double>(workspace, pl.scal),
+                                                                                static_cast<int>(p.batch), d_err);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+}  // extern "C"

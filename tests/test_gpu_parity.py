@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference's golden vectors.  Tolerances (BASELINE.json north_star):
+    fp32 mode  ||Y - Y_ref||_F / ||Y_ref||_F <= 1e-5
+    bf16 mode  ... <= 2e-2, the oracle fed the same bf16-rounded input
+fp64 inputs run the fp32-mode pipeline end to end in fp64 and must agree with
+the reference to 1e-10."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_02500_b200 as U
+from oracle import unso_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-5, "bf16": 2e-2}
+DEV = torch.device("cuda:0")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def bf16_round(a):
+    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).double().numpy()
+
+
+def spec_for(name, kats):
+    ces = U.CesistaStepParams(U.default_cesista_triples())
+    return {
+        "unso_default": U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()),
+        "unso_generic": U.MethodSpec(U.MethodKind.UNSO, coeffs=U.CoefficientSet(
+            14, np.array(kats["kat"]["generic_a"]), "approx-abs")),
+        "unso_plain": U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), scaling="plain"),
+        "unso_gelfand": U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), scaling="gelfand"),
+        "original4": U.MethodSpec(U.MethodKind.ORIGINAL_NS, iterations=4),
+        "muon3": U.MethodSpec(U.MethodKind.MUON_NS, iterations=3),
+        "muon5": U.MethodSpec(U.MethodKind.MUON_NS, iterations=5),
+        "cesista": U.MethodSpec(U.MethodKind.CESISTA_NS, step_params=ces),
+        "external": U.MethodSpec(U.MethodKind.EXTERNAL_SCHEDULE,
+                                 schedule=np.tile(np.array(U.MUON_COEFFICIENTS), (3, 1))),
+    }[name]
+
+
+def oracle_kw(name, kats):
+    return dict(
+        unso_default=dict(method="unso"),
+        unso_generic=dict(method="unso", a=kats["kat"]["generic_a"], rule="approx-abs"),
+        unso_plain=dict(method="unso", scaling="plain"),
+        unso_gelfand=dict(method="unso", scaling="gelfand"),
+        original4=dict(method="original", iterations=4),
+        muon3=dict(method="muon", iterations=3),
+        muon5=dict(method="muon", iterations=5),
+        cesista=dict(method="cesista", rows=O.cesista_rows(O.CESISTA_DEFAULT_TRIPLES)),
+        external=dict(method="external", rows=O.muon_rows(3)),
+    )[name]
+
+
+def run(m_np, spec, dtype, precision):
+    x = torch.from_numpy(np.ascontiguousarray(m_np)).to(DEV, dtype)
+    res = U.orthogonalize(x, spec, precision=precision)
+    torch.cuda.synchronize()
+    return res, res.y.double().cpu().numpy()
+
+
+# ------------------------------------------------------------------ golden small cases
+def test_small_cases_fp64_io_match_reference(golden_arrays, golden_kats):
+    """fp64 in/out: the fp32-mode pipeline is fp64 end to end -> 1e-10 against the live reference."""
+    worst = 0.0
+    for case in golden_kats["cases"]:
+        m = golden_arrays[case["input"]]
+        res, y = run(m, spec_for(case["method"], golden_kats), torch.float64, "fp32")
+        ref = golden_arrays["y_" + case["key"]]
+        r = rel(y, ref)
+        worst = max(worst, r)
+        assert r <= 1e-10, (case["key"], r)
+        assert res.flops == case["flops"]
+        assert res.was_transposed == case["was_transposed"]
+    print(f"worst fp64-io rel err over {len(golden_kats['cases'])} cases: {worst:.2e}")
+
+
+def test_small_cases_fp32_mode(golden_arrays, golden_kats):
+    for case in golden_kats["cases"]:
+        m = golden_arrays[case["input"]].astype(np.float32)
+        _, y = run(m, spec_for(case["method"], golden_kats), torch.float32, "fp32")
+        ref = O.run(m.astype(np.float64), **oracle_kw(case["method"], golden_kats))["y"]
+        assert rel(y, ref) <= TOL["fp32"], case["key"]
+
+
+def test_small_cases_bf16_mode_unso(golden_arrays, golden_kats):
+    for case in golden_kats["cases"]:
+        if not case["method"].startswith("unso"):
+            continue
+        m = golden_arrays[case["input"]].astype(np.float32)
+        res, y = run(m, spec_for(case["method"], golden_kats), torch.bfloat16, "bf16")
+        ref = O.run(bf16_round(m), **oracle_kw(case["method"], golden_kats))["y"]
+        r = rel(y, ref)
+        assert r <= TOL["bf16"], (case["key"], r)
+        assert res.precision == "bf16"
+
+
+# ------------------------------------------------------------------ cfg1 (BASELINE configs[0])
+def test_cfg1_fp32_mode(golden_arrays, golden_kats):
+    g = O.gaussian_matrix(512, 128, 0).astype(np.float32)
+    for name, spec in (("unso", U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())),
+                       ("muon5", U.MethodSpec(U.MethodKind.MUON_NS, iterations=5))):
+        res, y = run(g, spec, torch.float32, "fp32")
+        ref = golden_arrays[f"cfg1_fp32_{name}"]
+        r = rel(y, ref)
+        err = U.ortho_error_any(res.y)
+        ref_err = golden_kats["cfg1"][f"fp32_{name}"]["ortho_error"]
+        print(f"cfg1 {name} fp32: rel {r:.2e}  ortho_error {err:.6f} (reference {ref_err:.6f})")
+        assert r <= TOL["fp32"], (name, r)
+        assert err == pytest.approx(ref_err, rel=1e-4)
+
+
+def test_cfg1_bf16_mode(golden_arrays, golden_kats):
+    g = O.gaussian_matrix(512, 128, 0).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    for dtype in (torch.bfloat16, torch.float32):
+        res, y = run(g, spec, dtype, "bf16")
+        r = rel(y, golden_arrays["cfg1_bf16_unso"])
+        print(f"cfg1 unso bf16 mode ({dtype}): rel {r:.2e}")
+        assert r <= TOL["bf16"]
+
+
+# ------------------------------------------------------------------ properties (tests/test_ortho.py)
+def test_orthonormal_rows_are_a_fixed_point():
+    q, _ = np.linalg.qr(O.gaussian_matrix(256, 64, 3))
+    x = torch.from_numpy(np.ascontiguousarray(q.T)).to(DEV)
+    y = U.unso(x, U.default_coefficients())
+    assert torch.allclose(y, x, atol=1e-10)
+    y32 = U.unso(x.float(), U.default_coefficients())
+    assert rel(y32.double().cpu().numpy(), q.T) <= 1e-5
+
+
+def test_diagonal_inputs_stay_diagonal():
+    d = np.diag([0.9, 0.7, 0.5, 0.3, 0.2])
+    for spec in (U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()),
+                 U.MethodSpec(U.MethodKind.MUON_NS, iterations=3)):
+        _, y = run(d, spec, torch.float64, "fp32")
+        assert np.max(np.abs(y - np.diag(np.diag(y)))) < 1e-12
+
+
+def test_zero_matrix_is_degenerate():
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    for dtype, prec in ((torch.float32, "fp32"), (torch.bfloat16, "bf16")):
+        with pytest.raises(U.DegenerateInputError):
+            U.orthogonalize(torch.zeros(64, 256, device=DEV, dtype=dtype), spec, precision=prec)
+    with pytest.raises(U.DegenerateInputError):
+        U.orthogonalize(torch.zeros(64, 256, device=DEV), U.MethodSpec(U.MethodKind.MUON_NS))
+
+
+def test_row_wide_precondition():
+    with pytest.raises(U.ShapeError):
+        U.unso(torch.ones(4, 2, device=DEV, dtype=torch.float64), U.default_coefficients())
+
+
+def test_transpose_equivariance():
+    m = O.gaussian_matrix(96, 200, 4)
+    for spec in (U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()),
+                 U.MethodSpec(U.MethodKind.MUON_NS, iterations=3)):
+        _, a = run(m, spec, torch.float64, "fp32")
+        _, b = run(m.T, spec, torch.float64, "fp32")
+        assert np.max(np.abs(a - b.T)) < 1e-12
+
+
+def test_batch_equals_single_calls():
+    ms = np.stack([O.gaussian_matrix(384, 128, s) for s in range(3)]).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    for dtype, prec in ((torch.float32, "fp32"), (torch.bfloat16, "bf16")):
+        xb = torch.from_numpy(ms).to(DEV, dtype)
+        yb = U.orthogonalize(xb, spec, precision=prec).y
+        for i in range(3):
+            yi = U.orthogonalize(xb[i], spec, precision=prec).y
+            r = rel(yb[i].double().cpu().numpy(), yi.double().cpu().numpy())
+            assert r <= (1e-6 if prec == "fp32" else 1e-2), (prec, i, r)
+
+
+def test_ortho_error_device_matches_oracle():
+    y = O.gaussian_matrix(300, 70, 9) * 0.1
+    got = U.ortho_error_any(torch.from_numpy(y).to(DEV))
+    assert got == pytest.approx(O.ortho_error_any(y), rel=1e-12)
+
+
+def test_preprocess_and_bare_kernels_match_oracle():
+    m = O.gaussian_matrix(160, 48, 12)
+    x, tall = U.preprocess(torch.from_numpy(m).to(DEV), U.Scaling.FROBENIUS_GRAM)
+    xo, to, _ = O.scale_and_orient(m, "gram")
+    assert tall and to
+    assert np.max(np.abs(x.cpu().numpy() - xo)) < 1e-14
+    y = U.unso(x, U.default_coefficients())
+    assert rel(y.cpu().numpy(), O.unso_poly(xo)) <= 1e-10
+    y = U.muon_ns(x, 5)
+    assert rel(y.cpu().numpy(), O.quintic_ns(xo, O.muon_rows(5))) <= 1e-10
+    y = U.original_ns(x, 8)
+    assert rel(y.cpu().numpy(), O.cubic_ns(xo, 8)) <= 1e-10
+
+
+# ------------------------------------------------------------------ larger / BASELINE-shaped cases
+def test_cfg2_full_fp32_mode():
+    """configs[1]: 16 x 2048x512 controlled spectrum s ~ logU[1e-4, 1], fp32 mode <= 1e-5."""
+    rng = np.random.default_rng(2)
+    ms = np.stack([O.controlled_spectrum_matrix(2048, 512, np.exp(rng.uniform(np.log(1e-4), 0, 512)), 100 + i)
+                   for i in range(16)]).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    res = U.orthogonalize(torch.from_numpy(ms).to(DEV), spec, precision="fp32")
+    y = res.y.double().cpu().numpy()
+    worst = 0.0
+    for i in range(16):
+        ref = O.run(ms[i].astype(np.float64), "unso")["y"]
+        worst = max(worst, rel(y[i], ref))
+    print(f"cfg2 fp32 worst rel err {worst:.2e}")
+    assert worst <= TOL["fp32"]
+
+
+@pytest.mark.parametrize("shape,scale,seed", [((4096, 1024), 1.0, 5), ((1024, 1024), 0.02, 6), ((640, 1536), 1.0, 7)])
+def test_bf16_mode_gaussian_shapes(shape, scale, seed):
+    m = (O.gaussian_matrix(*shape, seed) * scale).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    res, y = run(m, spec, torch.bfloat16, "bf16")
+    ref = O.run(bf16_round(m), "unso")["y"]
+    r = rel(y, ref)
+    print(f"bf16 {shape}: rel {r:.2e}")
+    assert r <= TOL["bf16"]
+
+
+def test_pareto_spectrum_both_modes():
+    """configs[4]-like (reduced): heavy-tailed spectrum in [1e-6, 1], fp32 and bf16 modes."""
+    rng = np.random.default_rng(4)
+    s = 1.0 + rng.pareto(1.5, 512)
+    s = 1e-6 + (s - s.min()) / (s.max() - s.min()) * (1.0 - 1e-6)
+    m = O.controlled_spectrum_matrix(1536, 512, s, 44).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    _, y = run(m, spec, torch.float32, "fp32")
+    r32 = rel(y, O.run(m.astype(np.float64), "unso")["y"])
+    _, yb = run(m, spec, torch.float32, "bf16")
+    rb = rel(yb, O.run(bf16_round(m), "unso")["y"])
+    print(f"pareto: fp32 {r32:.2e}  bf16 {rb:.2e}")
+    assert r32 <= TOL["fp32"]
+    assert rb <= TOL["bf16"]
