@@ -67,7 +67,8 @@ typedef struct unso_matrix_desc {
   int64_t batch;         /* number of matrices, >= 1 */
   int64_t batch_stride;  /* elements between consecutive matrices */
   int32_t dtype;         /* unso_dtype of the input and of the output */
-  int32_t reserved;
+  int32_t orientation;   /* 0: auto, long side = rows iff rows > cols (ortho.py:149-150);
+                            1: rows are the long side (a row shard of a tall matrix); 2: cols are */
 } unso_matrix_desc;
 
 typedef struct unso_method_desc {
@@ -128,6 +129,19 @@ int32_t unso_ortho_error(const unso_matrix_desc* y, const void* y_ptr, double* d
 
 /* Number of CUDA kernels launched by the last successful call on this thread. */
 int32_t unso_last_launch_count(void);
+
+/* Stage profiling of unso_orthogonalize (UNSO method) with CUDA events recorded on
+ * the call's stream at stage boundaries, so a caller can attribute a timed region to
+ * kernels without extra syncs.  Stages (UNSO_PROFILE_STAGES):
+ *   0 convert (X -> bf16 copy), 1 gram (K1 SYRK), 2 scale+prep (finalize, norms, C_1, P),
+ *   3 chain (K2, N-1 launches), 4 finalize P, 5 apply (K3).
+ * begin() arms up to max_calls calls (process-wide, not thread-safe); read() synchronises
+ * the recorded events and writes max_calls x UNSO_PROFILE_STAGES milliseconds, returning
+ * the number of calls recorded; end() releases the events. */
+#define UNSO_PROFILE_STAGES 6
+int32_t unso_profile_begin(int32_t max_calls);
+int32_t unso_profile_read(float* out_ms, int32_t max_calls);
+void unso_profile_end(void);
 
 #ifdef __cplusplus
 }

@@ -32,14 +32,15 @@ FLAG_SINGLE_TERM_APPLY = 0x1
 EXPORTED_SYMBOLS = (
     "unso_version", "unso_status_string", "unso_workspace_size", "unso_orthogonalize", "unso_gram",
     "unso_gram_dtype", "unso_orthogonalize_from_gram", "unso_scale_denominator", "unso_ortho_error",
-    "unso_last_launch_count",
+    "unso_last_launch_count", "unso_profile_begin", "unso_profile_read", "unso_profile_end",
 )
+PROFILE_STAGES = ("convert", "gram", "scale_prep", "chain", "finalize_p", "apply")
 
 
 class MatrixDesc(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("ld", ctypes.c_int64),
                 ("batch", ctypes.c_int64), ("batch_stride", ctypes.c_int64), ("dtype", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("orientation", ctypes.c_int32)]
 
 
 class MethodDesc(ctypes.Structure):
@@ -76,6 +77,12 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.unso_ortho_error.argtypes = [XD, P, P, P, ctypes.c_size_t, P]
     lib.unso_last_launch_count.restype = ctypes.c_int32
     lib.unso_last_launch_count.argtypes = []
+    lib.unso_profile_begin.restype = ctypes.c_int32
+    lib.unso_profile_begin.argtypes = [ctypes.c_int32]
+    lib.unso_profile_read.restype = ctypes.c_int32
+    lib.unso_profile_read.argtypes = [P, ctypes.c_int32]
+    lib.unso_profile_end.restype = None
+    lib.unso_profile_end.argtypes = []
 
 
 def lib() -> ctypes.CDLL:
@@ -124,3 +131,30 @@ def version() -> str:
 
 def launch_count() -> int:
     return int(lib().unso_last_launch_count())
+
+
+class StageProfiler:
+    """Context manager around unso_profile_*: per-call stage times (ms) of
+    unso_orthogonalize, recorded with CUDA events on the call's stream."""
+
+    def __init__(self, max_calls: int):
+        self.max_calls = max_calls
+        self.times = None
+
+    def __enter__(self):
+        check(lib().unso_profile_begin(self.max_calls), "unso_profile_begin")
+        return self
+
+    def read(self):
+        import numpy as np
+        buf = (ctypes.c_float * (self.max_calls * len(PROFILE_STAGES)))()
+        n = lib().unso_profile_read(ctypes.cast(buf, ctypes.c_void_p), self.max_calls)
+        arr = np.frombuffer(buf, dtype=np.float32).reshape(self.max_calls, len(PROFILE_STAGES))[:n].copy()
+        self.times = arr
+        return arr
+
+    def __exit__(self, *exc):
+        if self.times is None:
+            self.read()
+        lib().unso_profile_end()
+        return False

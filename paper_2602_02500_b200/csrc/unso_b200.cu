@@ -31,6 +31,19 @@ namespace unso {
 
 static thread_local int g_launches = 0;
 
+// Stage profiler (unso_profile_*): CUDA events recorded on the call's stream.
+struct Profiler {
+  bool on = false;
+  int cap = 0, n = 0;
+  std::vector<cudaEvent_t> ev;
+};
+static Profiler g_prof;
+static thread_local bool g_prof_call = false;
+constexpr int PROF_EV = UNSO_PROFILE_STAGES + 1;
+static void prof_mark(int idx, cudaStream_t st) {
+  if (g_prof_call && g_prof.on && g_prof.n < g_prof.cap) cudaEventRecord(g_prof.ev[g_prof.n * PROF_EV + idx], st);
+}
+
 #define UNSO_CHECK_LAUNCH()                          \
   do {                                               \
     ++g_launches;                                    \
@@ -285,6 +298,9 @@ static int32_t make_problem(const unso_matrix_desc* x, const unso_method_desc* m
   if (x->batch > 1 && x->batch_stride < x->rows * x->ld) return UNSO_ERR_SHAPE;
   p.dt = x->dtype;
   p.tall = x->rows > x->cols;  // ortho.py:149 (square is not transposed)
+  if (x->orientation == 1) p.tall = true;
+  if (x->orientation == 2) p.tall = false;
+  if (x->orientation < 0 || x->orientation > 2) return UNSO_ERR_VALUE;
   p.h = p.tall ? x->cols : x->rows;
   p.w = p.tall ? x->rows : x->cols;
   if (p.h > 65536) return UNSO_ERR_UNSUPPORTED;
@@ -495,6 +511,7 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
                                                   at<double>(ws, pl.C[0]), at<double>(ws, pl.P));
     UNSO_CHECK_LAUNCH();
   }
+  prof_mark(3, st);
   int cur = 0;
   for (int k = 1; k < N; ++k) {  // produces C_{k+1}
     SimtOperand C{at<double>(ws, pl.C[cur]), pl.ldc, pl.hh, DT_F64, 1};
@@ -508,6 +525,7 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
     ++g_launches;
     cur ^= 1;
   }
+  prof_mark(4, st);
   {
     const int nt = (h + 31) / 32;
     dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
@@ -515,6 +533,7 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
                                                at<double>(ws, pl.Pout), nullptr);
     UNSO_CHECK_LAUNCH();
   }
+  prof_mark(5, st);
   // apply: tall Y = X P (A = X K-major over w rows), wide Y = P X (B = X MN-major)
   SimtOperand Xop{x, p.ld, p.bs, p.dt, 1};
   SimtOperand Pop{at<double>(ws, pl.Pout), pl.ldc, pl.hh, DT_F64, 1};
@@ -528,6 +547,7 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
   }
   if (e != cudaSuccess) return UNSO_ERR_CUDA;
   ++g_launches;
+  prof_mark(6, st);
   return UNSO_OK;
 }
 
@@ -591,6 +611,7 @@ static int32_t unso_bf16_from_G(const Problem& p, const Plan& pl, void* ws, cons
                                            at<float>(ws, pl.P));
     UNSO_CHECK_LAUNCH();
   }
+  prof_mark(3, st);
   int cur = 0;
   const UmmaWork wc = umma_make_work(h, h, h, 128, static_cast<int>(p.batch), true, 1);
   for (int k = 1; k < N; ++k) {
@@ -605,6 +626,7 @@ static int32_t unso_bf16_from_G(const Problem& p, const Plan& pl, void* ws, cons
     ++g_launches;
     cur ^= 1;
   }
+  prof_mark(4, st);
   {
     const int nt = (h + 31) / 32;
     dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
@@ -612,6 +634,7 @@ static int32_t unso_bf16_from_G(const Problem& p, const Plan& pl, void* ws, cons
                                                at<__nv_bfloat16>(ws, pl.Phi), at<__nv_bfloat16>(ws, pl.Plo));
     UNSO_CHECK_LAUNCH();
   }
+  prof_mark(5, st);
   const bool single = (p.flags & UNSO_FLAG_SINGLE_TERM_APPLY) != 0;
   CUtensorMap mx, mph, mpl;
   if (!umma_make_kmajor_map(&mph, at<__nv_bfloat16>(ws, pl.Phi), h, h, pl.ldc, p.batch, pl.hh, 128) ||
@@ -634,6 +657,7 @@ static int32_t unso_bf16_from_G(const Problem& p, const Plan& pl, void* ws, cons
   }
   if (e != cudaSuccess) return UNSO_ERR_CUDA;
   ++g_launches;
+  prof_mark(6, st);
   return UNSO_OK;
 }
 
@@ -767,8 +791,18 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
   }
   const Plan pl = make_plan(p, true);
   UNSO_TRY(check_ws(pl, workspace, workspace_bytes));
+  struct ProfGuard {
+    ProfGuard() { g_prof_call = true; }
+    ~ProfGuard() {
+      if (g_prof.on && g_prof.n < g_prof.cap) ++g_prof.n;
+      g_prof_call = false;
+    }
+  } guard;
+  prof_mark(0, st);
   if (p.prec == UNSO_PREC_FP32) {
+    prof_mark(1, st);
     UNSO_TRY(gram_simt(p, x_ptr, p.dt, p.ld, p.bs, pl, workspace, pl.splits, st));
+    prof_mark(2, st);
     double* G = at<double>(workspace, pl.G);
     UNSO_TRY(finalize_gram<double>(p, pl, workspace, pl.splits, G, st));
     return unso_fp32_from_G(p, pl, workspace, x_ptr, G, y_ptr, d_status, st);
@@ -776,10 +810,46 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
   const __nv_bfloat16* xb;
   int64_t ldx, bsx;
   UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
+  prof_mark(1, st);
   UNSO_TRY(gram_bf16(p, pl, workspace, xb, ldx, bsx, st));
+  prof_mark(2, st);
   float* G = at<float>(workspace, pl.G);
   UNSO_TRY(finalize_gram<float>(p, pl, workspace, pl.splits, G, st));
   return unso_bf16_from_G(p, pl, workspace, xb, ldx, bsx, G, y_ptr, d_status, st);
+}
+
+int32_t unso_profile_begin(int32_t max_calls) {
+  unso_profile_end();
+  if (max_calls < 1) return UNSO_ERR_VALUE;
+  g_prof.ev.assign(static_cast<size_t>(max_calls) * PROF_EV, nullptr);
+  for (auto& e : g_prof.ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return UNSO_ERR_CUDA;
+  g_prof.cap = max_calls;
+  g_prof.n = 0;
+  g_prof.on = true;
+  return UNSO_OK;
+}
+
+int32_t unso_profile_read(float* out_ms, int32_t max_calls) {
+  if (!g_prof.on || !out_ms) return 0;
+  const int n = g_prof.n < max_calls ? g_prof.n : max_calls;
+  for (int c = 0; c < n; ++c) {
+    for (int s = 0; s < UNSO_PROFILE_STAGES; ++s) {
+      float ms = 0.f;
+      cudaEvent_t a = g_prof.ev[c * PROF_EV + s], b = g_prof.ev[c * PROF_EV + s + 1];
+      if (cudaEventSynchronize(b) != cudaSuccess || cudaEventElapsedTime(&ms, a, b) != cudaSuccess) ms = -1.f;
+      out_ms[c * UNSO_PROFILE_STAGES + s] = ms;
+    }
+  }
+  return n;
+}
+
+void unso_profile_end(void) {
+  for (auto& e : g_prof.ev)
+    if (e) cudaEventDestroy(e);
+  g_prof.ev.clear();
+  g_prof.on = false;
+  g_prof.cap = g_prof.n = 0;
 }
 
 int32_t unso_gram(const unso_matrix_desc* x, const void* x_ptr, void* g_ptr, const unso_method_desc* method,

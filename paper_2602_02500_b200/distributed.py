@@ -1,0 +1,158 @@
+"""Multi-GPU partitioning of the orthogonalization (one process per GPU).
+
+Two schemes (BASELINE.json north_star):
+
+* Row sharding of one very tall matrix (configs[3]): rank r owns rows
+  [r*w/P, (r+1)*w/P) of the w x h input.  Each rank computes its local Gram
+  X_r^T X_r (``unso_gram``), ONE all-reduce (sum) of the h x h Gram over the
+  process group (NCCL over NVLink on B200), then forms the scale and P(A)
+  redundantly and applies it to its own rows (``unso_orthogonalize_from_gram``).
+  The output stays row-sharded.  This is exact: sum_r X_r^T X_r = X^T X.
+
+* Batch distribution of independent matrices (configs[1,2,4]): longest-
+  processing-time assignment by reference-model FLOPs, no communication.
+
+The stage functions are injectable so the protocol can be exercised on CPU
+(gloo) in tests; the product default is the CUDA library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import heapq
+from dataclasses import dataclass
+from typing import Callable, Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from .errors import DegenerateInputError, ShapeError
+from .ortho import (MethodKind, MethodSpec, _DTYPES, _SCALING, _matrix_desc, _method_desc, _resolve_precision,
+                    kernel_model_flops, workspace_pool)
+
+
+def row_shard_bounds(w: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced split of w rows over `world` ranks."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    base, extra = divmod(w, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def lpt_assignment(costs: Sequence[float], world: int) -> list[list[int]]:
+    """Longest-processing-time-first: items sorted by cost, each to the least-loaded rank.
+    Deterministic (ties broken by rank, then item index)."""
+    heap = [(0.0, r) for r in range(world)]
+    out: list[list[int]] = [[] for _ in range(world)]
+    for i in sorted(range(len(costs)), key=lambda j: (-costs[j], j)):
+        load, r = heapq.heappop(heap)
+        out[r].append(i)
+        heapq.heappush(heap, (load + costs[i], r))
+    return [sorted(v) for v in out]
+
+
+# --------------------------------------------------------------------------- native stages
+
+def native_gram(x_local: torch.Tensor, spec: MethodSpec, precision) -> torch.Tensor:
+    """Un-normalised short-side Gram of a row shard (rows = long side)."""
+    xd = _matrix_desc(x_local)
+    xd.orientation = 1
+    prec = _resolve_precision(spec, x_local, precision)
+    md, co = _method_desc(spec, prec, _SCALING[spec.effective_scaling])
+    lib = N.lib()
+    h = x_local.shape[-1]
+    gdtype = torch.float64 if lib.unso_gram_dtype(ctypes.byref(md)) == N.DTYPE_F64 else torch.float32
+    shape = (h, h) if x_local.dim() == 2 else (x_local.shape[0], h, h)
+    g = torch.empty(shape, dtype=gdtype, device=x_local.device)
+    nbytes = lib.unso_workspace_size(ctypes.byref(xd), ctypes.byref(md))
+    stream = torch.cuda.current_stream(x_local.device)
+    ws = workspace_pool.get(nbytes, x_local.device, stream)
+    code = lib.unso_gram(ctypes.byref(xd), ctypes.c_void_p(x_local.data_ptr()), ctypes.c_void_p(g.data_ptr()),
+                         ctypes.byref(md), ctypes.c_void_p(ws.data_ptr()), ctypes.c_size_t(ws.numel()),
+                         ctypes.c_void_p(stream.cuda_stream))
+    del co
+    N.check(code, "unso_gram")
+    return g
+
+
+def native_finish(x_local: torch.Tensor, g: torch.Tensor, spec: MethodSpec, precision,
+                  out: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Scale, squaring chain and apply on the local rows, given the reduced Gram."""
+    xd = _matrix_desc(x_local)
+    xd.orientation = 1
+    prec = _resolve_precision(spec, x_local, precision)
+    md, co = _method_desc(spec, prec, _SCALING[spec.effective_scaling])
+    lib = N.lib()
+    nbytes = lib.unso_workspace_size(ctypes.byref(xd), ctypes.byref(md))
+    stream = torch.cuda.current_stream(x_local.device)
+    ws = workspace_pool.get(nbytes, x_local.device, stream)
+    y = out if out is not None else torch.empty_like(x_local, memory_format=torch.contiguous_format)
+    status = torch.zeros(xd.batch, dtype=torch.int32, device=x_local.device)
+    code = lib.unso_orthogonalize_from_gram(ctypes.byref(xd), ctypes.c_void_p(x_local.data_ptr()),
+                                            ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                            ctypes.byref(md), ctypes.c_void_p(ws.data_ptr()),
+                                            ctypes.c_size_t(ws.numel()), ctypes.c_void_p(status.data_ptr()),
+                                            ctypes.c_void_p(stream.cuda_stream))
+    del co
+    N.check(code, "unso_orthogonalize_from_gram")
+    return y, status
+
+
+@dataclass
+class ShardStages:
+    gram: Callable
+    finish: Callable
+
+
+NATIVE_STAGES = ShardStages(native_gram, native_finish)
+
+
+def orthogonalize_row_sharded(x_local: torch.Tensor, spec: MethodSpec, *, group=None, precision=None,
+                              out: torch.Tensor | None = None, check: bool = True,
+                              stages: ShardStages = NATIVE_STAGES) -> torch.Tensor:
+    """UNSO on a tall matrix whose rows are sharded over the process group.
+
+    x_local holds this rank's contiguous block of rows (the long side); every
+    rank must pass the same column count h.  Returns this rank's rows of Y."""
+    if spec.kind is not MethodKind.UNSO:
+        raise ShapeError("row sharding is implemented for the UNSO method (one Gram all-reduce)")
+    g = stages.gram(x_local, spec, precision)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)
+    y, status = stages.finish(x_local, g, spec, precision, out)
+    if check and status is not None and bool((status != 0).any()):
+        raise DegenerateInputError("input is identically zero or the scaling denominator is not positive finite")
+    return y
+
+
+def orthogonalize_batch_distributed(mats: Sequence[torch.Tensor], spec: MethodSpec, *, rank: int, world: int,
+                                    orthogonalize_fn=None, precision=None) -> dict[int, torch.Tensor]:
+    """Process this rank's LPT share of independent matrices; no communication.
+    Returns {global index: Y}.  Equal shapes are grouped into one batched call."""
+    from .ortho import orthogonalize
+    fn = orthogonalize_fn or (lambda m: orthogonalize(m, spec, precision=precision, check=False).y)
+    costs = []
+    for m in mats:
+        r, c = m.shape[-2], m.shape[-1]
+        h, w = (c, r) if r > c else (r, c)
+        costs.append(float(kernel_model_flops(h, w, spec)))
+    mine = lpt_assignment(costs, world)[rank]
+    groups: dict = {}
+    for i in mine:
+        groups.setdefault((tuple(mats[i].shape), mats[i].dtype), []).append(i)
+    out = {}
+    for _, idx in sorted(groups.items(), key=lambda kv: str(kv[0])):
+        stacked = torch.stack([mats[i] for i in idx]) if len(idx) > 1 else mats[idx[0]]
+        y = fn(stacked)
+        if len(idx) == 1:
+            out[idx[0]] = y
+        else:
+            for j, i in enumerate(idx):
+                out[i] = y[j]
+    return out
+
+
+__all__ = ["row_shard_bounds", "lpt_assignment", "orthogonalize_row_sharded", "orthogonalize_batch_distributed",
+           "native_gram", "native_finish", "ShardStages", "NATIVE_STAGES", "_DTYPES"]
