@@ -371,6 +371,27 @@ def composed_map(method: str, *, order: int = DEFAULT_ORDER, a=DEFAULT_A, rule: 
     return quintic
 
 
+def unso_rows_of_tall(m: np.ndarray, rows: np.ndarray, order: int = DEFAULT_ORDER, a=DEFAULT_A,
+                      rule: str = DEFAULT_RULE) -> np.ndarray:
+    """Selected rows of orthogonalize(m) for a tall m (w x h, w > h), computed with the
+    reference's operations (ortho.py:140-205) but applying P only to the requested rows:
+    (P X^T)^T restricted to `rows` = X[rows] P (P symmetric).  For full-size parity
+    checks where forming all of Y on the host is unnecessary."""
+    x = np.ascontiguousarray(m.T)                               # preprocess transposes (ortho.py:149-150)
+    g = x @ _T(x)                                               # ortho.py:156
+    denom = float(np.sqrt(float(np.sqrt(np.sum(g * g)))))       # ortho.py:157
+    g = g / (denom * denom)                                     # == (x/denom)(x/denom)^T up to rounding
+    b = final_coefficient(order, a, rule)
+    h = g.shape[0]
+    bk = np.eye(h) - g
+    p = np.eye(h)
+    for k in range(1, order):
+        p = p + float(a[k - 1]) * bk
+        bk = bk @ bk
+    p = p + b * bk
+    return (m[rows] / denom) @ p
+
+
 # ---------------------------------------------------------------------------
 # controlled-spectrum inputs (BASELINE.json configs[1], configs[4]; SURVEY §8d)
 # ---------------------------------------------------------------------------

@@ -1,0 +1,382 @@
+// Fused persistent "scale + squaring chain" kernel (BF16 precision), one CTA per
+// 128x128 upper tile of the h x h state, all tiles co-resident (cooperative launch).
+//
+// Replaces, for the reference's ortho.py:156-167 + 197-204:
+//   split-K finalize -> ||G||_F / trace -> s^2, status -> C_1 = G/s^2, P = alpha I - a_1 C_1
+//   -> N-1 squarings C_{k+1} = 2 C_k - C_k^2 with P -= c_{k+1} C_{k+1} -> P/s split bf16 hi/lo.
+// (C-form of B_{k+1} = B_k^2 with B = I - C; P = I + sum a_k B_k + b B_N = alpha I - sum c_k C_k.)
+//
+// Per CTA (tile (ti, tj), ti <= tj):
+//   TMEM  cols [0,128)   accumulator of C_k^2 for the tile (bf16x3: hi*hi + hi*lo + lo*hi)
+//         cols [128,256) P tile (fp32), resident for the whole chain
+//         cols [256,384) C_k tile (fp32), resident for the whole chain
+//   global: only the CTA's own upper tile of C_{k+1} (bf16 hi/lo, ping-pong buffers) is
+//   written per step.  Operand row-blocks are assembled from upper tiles: block (i, kb)
+//   with kb < i is read through an MN-major (transposed) TMA map of tile (kb, i), and the
+//   tcgen05 instruction descriptor's A/B major bits are switched per k-block.
+//   A grid barrier (gpu-scope release/acquire counter) separates the steps.
+#pragma once
+#include "common.cuh"
+#include "ptx_sm100.cuh"
+#include "umma_gemm.cuh"
+
+namespace unso {
+
+constexpr int CHAIN_MAX_ORDER = 64;
+
+struct ChainMaps {
+  // [buffer][0 = hi, 1 = lo][0 = K-major box {64,128}, 1 = MN-major box {64,64}]
+  CUtensorMap m[2][2][2];
+};
+
+struct ChainParams {
+  const float* part;   // split-K Gram partials: part[(s * batch + b) * mat + r * ld + c]
+  int splits;
+  int h, nt, tiles_per_mat, batch;
+  int64_t ld, mat;     // padded leading dim / per-matrix elements of every h x h buffer
+  __nv_bfloat16* chi[2];
+  __nv_bfloat16* clo[2];
+  __nv_bfloat16* phi;  // out: P/s, full symmetric
+  __nv_bfloat16* plo;
+  double* normbuf;     // [tiles][2]
+  double* scal;        // [batch][SCAL_STRIDE]
+  int32_t* status;     // [batch]
+  unsigned* gbar;      // zeroed before launch
+  int order;
+  int scal_mode;       // SM_GRAM / SM_PLAIN / SM_NONE
+  double alpha;        // 1 + sum a + b
+  float coef[CHAIN_MAX_ORDER];  // coef[k-1] multiplies C_k
+};
+
+constexpr int CH_STAGES = 3;
+constexpr int CH_TILE = 128 * 64 * 2;          // 16 KB operand tile
+constexpr int CH_STAGE_BYTES = 4 * CH_TILE;    // A hi, A lo, B hi, B lo
+constexpr int CH_SMEM = CH_STAGES * CH_STAGE_BYTES + 256 + 1024;
+constexpr uint32_t CH_ACC = 0, CH_P = 128, CH_C = 256;
+
+__device__ __forceinline__ void grid_arrive(unsigned* gbar) {
+  __threadfence();
+  red_release_gpu_add(gbar, 1u);
+}
+__device__ __forceinline__ void grid_wait(const unsigned* gbar, unsigned target) {
+  while (ld_acquire_gpu(gbar) < target) __nanosleep(64);
+}
+
+__device__ __forceinline__ void ch_load_block(const ChainMaps& maps, int buf, int hl, uint64_t* bar, uint8_t* dst,
+                                              int blk, int kt, int b) {
+  const int kb = kt >> 1;  // 128-wide block index of this 64-wide k-slice
+  if (blk <= kb) {
+    tma_load_3d(&maps.m[buf][hl][0], bar, dst, kt * 64, blk * 128, b);      // rows of stored tile (blk, kb)
+  } else {
+    tma_load_3d(&maps.m[buf][hl][1], bar, dst, blk * 128, kt * 64, b);          // tile (kb, blk) read transposed
+    tma_load_3d(&maps.m[buf][hl][1], bar, dst + 8192, blk * 128 + 64, kt * 64, b);
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_constant__ ChainMaps maps,
+                                                                  const __grid_constant__ ChainParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CH_STAGES * CH_STAGE_BYTES);
+  uint64_t* empty = full + CH_STAGES;
+  uint64_t* tfull = empty + CH_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  __shared__ double red[2][4];
+  __shared__ double s_scale[2];  // inv_s2, inv_s
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = gridDim.x;
+  const int b = blockIdx.x / p.tiles_per_mat;
+  const int t = blockIdx.x % p.tiles_per_mat;
+  int ti, tj;
+  simt_tile_coords(t, p.nt, p.nt, 1, ti, tj);
+  const int N = p.order;
+  const int KT = (p.h + 63) / 64;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j)
+        for (int q = 0; q < 2; ++q) tma_prefetch_desc(&maps.m[i][j][q]);
+    for (int s = 0; s < CH_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int k = 1; k < N; ++k) {
+        grid_wait(p.gbar, static_cast<unsigned>(k + 1) * T);  // C_k published (round k)
+        fence_proxy_async_global();
+        const int buf = (k - 1) & 1;
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * CH_STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], CH_STAGE_BYTES);
+          ch_load_block(maps, buf, 0, &full[stage], st, ti, kt, b);
+          ch_load_block(maps, buf, 1, &full[stage], st + CH_TILE, ti, kt, b);
+          ch_load_block(maps, buf, 0, &full[stage], st + 2 * CH_TILE, tj, kt, b);
+          ch_load_block(maps, buf, 1, &full[stage], st + 3 * CH_TILE, tj, kt, b);
+          if (++stage == CH_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int k = 1; k < N; ++k) {
+        mbar_wait(tempty, acc_phase ^ 1);
+        tc_fence_after();
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const int kb = kt >> 1;
+          const bool a_mn = kb < ti, b_mn = kb < tj;
+          const uint32_t idesc = idesc_bf16(128, 128, a_mn ? 1 : 0, b_mn ? 1 : 0);
+          const uint32_t st = smem_u32(smem + stage * CH_STAGE_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t ah = a_mn ? operand_desc<true>(st, ks) : operand_desc<false>(st, ks);
+            const uint64_t al = a_mn ? operand_desc<true>(st + CH_TILE, ks) : operand_desc<false>(st + CH_TILE, ks);
+            const uint64_t bh = b_mn ? operand_desc<true>(st + 2 * CH_TILE, ks)
+                                     : operand_desc<false>(st + 2 * CH_TILE, ks);
+            const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * CH_TILE, ks)
+                                     : operand_desc<false>(st + 3 * CH_TILE, ks);
+            umma_bf16(tmem + CH_ACC, ah, bh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
+            umma_bf16(tmem + CH_ACC, ah, bl, idesc, 1u);
+            umma_bf16(tmem + CH_ACC, al, bh, idesc, 1u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == CH_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(tfull);
+        acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ epilogue warps
+    const int ew = warp - 4;
+    const int r = ew * 32 + lane;
+    const int gr = ti * 128 + r;
+    const bool row_ok = gr < p.h;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(ew * 32) << 16);
+    const int64_t mbase = static_cast<int64_t>(b) * p.mat;
+    const int tid = threadIdx.x - 128;
+
+    // ---- phase A: G tile = sum of split-K partials -> TMEM C region; tile norms
+    double tr = 0.0, fr = 0.0;
+    const double wgt = (ti == tj) ? 1.0 : 2.0;
+    for (int c = 0; c < 4; ++c) {
+      const int gc0 = tj * 128 + c * 32;
+      float g[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) g[j] = 0.f;
+      if (row_ok) {
+        for (int s = 0; s < p.splits; ++s) {
+          const float* src = p.part + (static_cast<int64_t>(s) * p.batch + b) * p.mat + static_cast<int64_t>(gr) * p.ld + gc0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(src + j);
+            g[j] += v.x;
+            g[j + 1] += v.y;
+            g[j + 2] += v.z;
+            g[j + 3] += v.w;
+          }
+        }
+      }
+      uint32_t u[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const bool ok = row_ok && (gc0 + j) < p.h;
+        const float v = ok ? g[j] : 0.f;
+        if (ok && gc0 + j == gr) tr += v;
+        fr += wgt * static_cast<double>(v) * v;
+        u[j] = __float_as_uint(v);
+      }
+      tmem_st32(lane_base + CH_C + c * 32, u);
+    }
+    tmem_wait_st();
+    tr = warp_sum(tr);
+    fr = warp_sum(fr);
+    if (lane == 0) {
+      red[0][ew] = tr;
+      red[1][ew] = fr;
+    }
+    named_bar_sync(1, 128);
+    if (tid == 0) {
+      p.normbuf[blockIdx.x * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+      p.normbuf[blockIdx.x * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+      grid_arrive(p.gbar);  // round 0
+      grid_wait(p.gbar, static_cast<unsigned>(T));
+      double s0 = 0.0, s1 = 0.0;
+      const int first = b * p.tiles_per_mat;
+      for (int q = 0; q < p.tiles_per_mat; ++q) {  // fixed order -> deterministic
+        s0 += __ldcg(&p.normbuf[(first + q) * 2 + 0]);
+        s1 += __ldcg(&p.normbuf[(first + q) * 2 + 1]);
+      }
+      double s2 = p.scal_mode == SM_PLAIN ? s0 : sqrt(s1);
+      if (p.scal_mode == SM_NONE) s2 = 1.0;
+      const double inv_s = 1.0 / sqrt(s2);
+      const bool bad = p.scal_mode != SM_NONE &&
+                       (!(s0 > 0.0) || !isfinite(s0) || !(s2 > 0.0) || !isfinite(s2) || !isfinite(inv_s));
+      s_scale[0] = 1.0 / s2;
+      s_scale[1] = inv_s;
+      if (t == 0) {
+        double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
+        o[S_TRACE] = s0;
+        o[S_FRO2] = s1;
+        o[S_S2] = s2;
+        o[S_INV_S] = inv_s;
+        if (p.status) p.status[b] = bad ? 2 : 0;
+      }
+    }
+    named_bar_sync(1, 128);
+    const float inv_s2 = static_cast<float>(s_scale[0]);
+    const float inv_s = static_cast<float>(s_scale[1]);
+
+    // ---- C_1 = G / s^2 (TMEM + global buffer 0), P = alpha I - coef_1 C_1 (TMEM)
+    for (int c = 0; c < 4; ++c) {
+      const int gc0 = tj * 128 + c * 32;
+      uint32_t u[32], pu[32];
+      tmem_ld32(lane_base + CH_C + c * 32, u);
+      tmem_wait_ld();
+      __align__(16) __nv_bfloat16 hi[32];
+      __align__(16) __nv_bfloat16 lo[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float cv = static_cast<float>(static_cast<double>(__uint_as_float(u[j])) * s_scale[0]);
+        u[j] = __float_as_uint(cv);
+        const float pv = static_cast<float>(((gr == gc0 + j && row_ok) ? p.alpha : 0.0) -
+                                            static_cast<double>(p.coef[0]) * cv);
+        pu[j] = __float_as_uint(pv);
+        split_bf16(cv, hi[j], lo[j]);
+      }
+      tmem_st32(lane_base + CH_C + c * 32, u);
+      tmem_st32(lane_base + CH_P + c * 32, pu);
+      if (row_ok && N > 1) {
+        const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          *reinterpret_cast<uint4*>(p.chi[0] + o + j) = *reinterpret_cast<const uint4*>(hi + j);
+          *reinterpret_cast<uint4*>(p.clo[0] + o + j) = *reinterpret_cast<const uint4*>(lo + j);
+        }
+      }
+    }
+    tmem_wait_st();
+    (void)inv_s2;
+    fence_proxy_async_global();
+    named_bar_sync(1, 128);
+    if (tid == 0) grid_arrive(p.gbar);  // round 1: C_1 published
+
+    // ---- phase B: squaring steps
+    uint32_t acc_phase = 0;
+    for (int k = 1; k < N; ++k) {
+      const bool last = (k == N - 1);
+      const float coef = p.coef[k];  // multiplies C_{k+1}
+      mbar_wait(tfull, acc_phase);
+      acc_phase ^= 1;
+      tc_fence_after();
+      for (int c = 0; c < 4; ++c) {
+        const int gc0 = tj * 128 + c * 32;
+        uint32_t ua[32], uc[32], up[32];
+        tmem_ld32(lane_base + CH_ACC + c * 32, ua);
+        tmem_ld32(lane_base + CH_C + c * 32, uc);
+        tmem_ld32(lane_base + CH_P + c * 32, up);
+        tmem_wait_ld();
+        __align__(16) __nv_bfloat16 hi[32];
+        __align__(16) __nv_bfloat16 lo[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const bool ok = row_ok && gc0 + j < p.h;
+          const float cn = ok ? 2.0f * __uint_as_float(uc[j]) - __uint_as_float(ua[j]) : 0.f;
+          const float pv = __uint_as_float(up[j]) - coef * cn;
+          uc[j] = __float_as_uint(cn);
+          up[j] = __float_as_uint(pv);
+          split_bf16(last ? pv * inv_s : cn, hi[j], lo[j]);
+        }
+        if (!last) {
+          tmem_st32(lane_base + CH_C + c * 32, uc);
+          tmem_st32(lane_base + CH_P + c * 32, up);
+          if (row_ok) {
+            const int nb = k & 1;
+            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              *reinterpret_cast<uint4*>(p.chi[nb] + o + j) = *reinterpret_cast<const uint4*>(hi + j);
+              *reinterpret_cast<uint4*>(p.clo[nb] + o + j) = *reinterpret_cast<const uint4*>(lo + j);
+            }
+          }
+        } else if (row_ok) {
+          // P/s -> full symmetric bf16 hi/lo for the apply; diagonal tiles own c >= r only
+          for (int j = 0; j < 32; ++j) {
+            const int gc = gc0 + j;
+            if (gc >= p.h || (ti == tj && gc < gr)) continue;
+            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
+            const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
+            p.phi[o] = hi[j];
+            p.plo[o] = lo[j];
+            p.phi[om] = hi[j];
+            p.plo[om] = lo[j];
+          }
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(tempty);
+      if (!last) {
+        fence_proxy_async_global();
+        named_bar_sync(1, 128);
+        if (tid == 0) grid_arrive(p.gbar);  // round k+1: C_{k+1} published
+      }
+    }
+    if (N == 1 && row_ok) {  // no squaring: P = (1+b) I - b C_1
+      for (int c = 0; c < 4; ++c) {
+        const int gc0 = tj * 128 + c * 32;
+        uint32_t up[32];
+        tmem_ld32(lane_base + CH_P + c * 32, up);
+        tmem_wait_ld();
+        for (int j = 0; j < 32; ++j) {
+          const int gc = gc0 + j;
+          if (gc >= p.h || (ti == tj && gc < gr)) continue;
+          __nv_bfloat16 hi, lo;
+          split_bf16(__uint_as_float(up[j]) * inv_s, hi, lo);
+          const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
+          const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
+          p.phi[o] = hi;
+          p.plo[o] = lo;
+          p.phi[om] = hi;
+          p.plo[om] = lo;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace unso

@@ -24,6 +24,9 @@
 #include "elementwise.cuh"
 #include "simt_gemm.cuh"
 #include "umma_gemm.cuh"
+#include "chain_persistent.cuh"
+#include "umma2_gemm.cuh"
+#include <cstdlib>
 
 #define UNSO_VERSION_STRING "unso_b200 0.1.0 (sm_100a: tcgen05/TMEM/TMA bf16 path + fp64 DFMA parity path)"
 
@@ -272,6 +275,23 @@ using CfgApplyTall1 = UmmaCfg<128, 1, 1, 1, TERM(0, 0, 0), false, false, 6>;
 // wide apply: (P_hi + P_lo) * X, X read MN-major
 using CfgApplyWide2 = UmmaCfg<128, 2, 1, 2, TERM(0, 0, 0) | TERM(1, 1, 0), false, true, 4>;
 using CfgApplyWide1 = UmmaCfg<128, 1, 1, 1, TERM(0, 0, 0), false, true, 6>;
+// CTA-pair (cta_group::2) 256 x 256 tiles
+using Cfg2GramK = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, false, 6>;
+using Cfg2GramMN = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), true, true, 6>;
+using Cfg2ApplyTall2 = Umma2Cfg<256, 1, 2, 2, TERM(0, 0, 0) | TERM(1, 0, 1), false, false, 4>;
+using Cfg2ApplyTall1 = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, false, 6>;
+using Cfg2ApplyWide2 = Umma2Cfg<256, 2, 1, 2, TERM(0, 0, 0) | TERM(1, 1, 0), false, true, 4>;
+using Cfg2ApplyWide1 = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, true, 6>;
+
+// Engine selection: CTA pairs by default; UNSO_ENGINE=1cta forces the 1-CTA 128x128 engine (A/B tests).
+static bool use_pair_engine() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("UNSO_ENGINE");
+    v = (e && std::strcmp(e, "1cta") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
 
 // ==================================================================== problem + workspace plan
 static inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -343,6 +363,7 @@ struct Plan {
   size_t C[2] = {0, 0}, P = 0, Pout = 0;          // FP32
   size_t Chi[2] = {0, 0}, Clo[2] = {0, 0}, Phi = 0, Plo = 0;  // BF16 (P reused as f32)
   size_t Gk[2] = {0, 0};                          // gelfand powers
+  size_t normbuf = 0, gbar = 0;                   // persistent chain: per-tile norms, grid barrier
   size_t Xs[2] = {0, 0};                          // NS state (f64)
 };
 
@@ -352,16 +373,29 @@ static size_t take(Plan& pl, size_t bytes) {
   return off;
 }
 
+// Split-K factor: the smallest s whose (tiles x s) work items fill >= 90% of the last wave
+// of persistent CTAs (or CTA pairs), keeping >= 4 k-blocks per split.
+static int pick_splits(int64_t tiles, int64_t ktiles, int64_t slots) {
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 32 && s <= ktiles / 4; ++s) {
+    const int64_t items = tiles * s;
+    const double eff = static_cast<double>(items) / (static_cast<double>((items + slots - 1) / slots) * slots);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = s;
+    }
+    if (eff >= 0.9) break;
+  }
+  return best;
+}
+
 static int gram_splits(const Problem& p) {
   if (p.prec == UNSO_PREC_BF16) {
-    const int64_t t = (p.h + 127) / 128;
-    const int64_t tiles = t * (t + 1) / 2 * p.batch;
-    const int64_t kt = (p.w + 63) / 64;
-    int64_t s = (2 * 148 + tiles - 1) / tiles;
-    if (s > kt / 4) s = kt / 4;
-    if (s < 1) s = 1;
-    if (s > 32) s = 32;
-    return static_cast<int>(s);
+    const int64_t tm = use_pair_engine() ? 256 : 128;
+    const int64_t t = (p.h + tm - 1) / tm;
+    const int64_t slots = use_pair_engine() ? 74 : 148;
+    return pick_splits(t * (t + 1) / 2 * p.batch, (p.w + 63) / 64, slots);
   }
   const int64_t t = (p.h + SIMT_BM - 1) / SIMT_BM;
   return simt_pick_splits(static_cast<int>(t * (t + 1) / 2), static_cast<int>(p.batch), static_cast<int>(p.w));
@@ -369,7 +403,7 @@ static int gram_splits(const Problem& p) {
 
 static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) {
   Plan pl;
-  pl.ldc = round_up(p.h, 128);
+  pl.ldc = round_up(p.h, 256);
   pl.hh = p.h * pl.ldc;
   const int64_t B = p.batch;
   const bool bf = !for_error && p.prec == UNSO_PREC_BF16;
@@ -402,6 +436,9 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       pl.P = take(pl, static_cast<size_t>(B * pl.hh) * 4);
       pl.Phi = take(pl, static_cast<size_t>(B * pl.hh) * 2);
       pl.Plo = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+      const int64_t nt = (p.h + 127) / 128;
+      pl.normbuf = take(pl, static_cast<size_t>(nt * (nt + 1) / 2 * B) * 2 * 8);
+      pl.gbar = take(pl, 256);
     } else {
       pl.C[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
       pl.C[1] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
@@ -584,20 +621,66 @@ static int32_t gram_bf16(const Problem& p, const Plan& pl, void* ws, const __nv_
                               static_cast<int>(p.batch), true, pl.splits);
   UEpiPartialF32 epi{at<float>(ws, pl.part), pl.hh, pl.ldc, static_cast<int>(p.batch), static_cast<int>(p.h)};
   cudaError_t e;
+  const bool pair = use_pair_engine();
+  const UmmaWork w2 = umma2_make_work(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 256,
+                                      static_cast<int>(p.batch), true, pl.splits);
   if (p.tall) {
     if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
-    e = launch_umma<CfgGramMN>(mx, mx, mx, mx, w, epi, st);
+    e = pair ? launch_umma2<Cfg2GramMN>(mx, mx, mx, mx, w2, epi, st) : launch_umma<CfgGramMN>(mx, mx, mx, mx, w, epi, st);
   } else {
     if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx, 128)) return UNSO_ERR_CUDA;
-    e = launch_umma<CfgGramK>(mx, mx, mx, mx, w, epi, st);
+    e = pair ? launch_umma2<Cfg2GramK>(mx, mx, mx, mx, w2, epi, st) : launch_umma<CfgGramK>(mx, mx, mx, mx, w, epi, st);
   }
   if (e != cudaSuccess) return UNSO_ERR_CUDA;
   ++g_launches;
   return UNSO_OK;
 }
 
-static int32_t unso_bf16_from_G(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
-                                int64_t bsx, const float* G, void* y, int32_t* status, cudaStream_t st) {
+static int32_t apply_bf16(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
+                          int64_t bsx, void* y, cudaStream_t st) {
+  const int h = static_cast<int>(p.h);
+  const bool single = (p.flags & UNSO_FLAG_SINGLE_TERM_APPLY) != 0;
+  CUtensorMap mx, mph, mpl;
+  if (!umma_make_kmajor_map(&mph, at<__nv_bfloat16>(ws, pl.Phi), h, h, pl.ldc, p.batch, pl.hh, 128) ||
+      !umma_make_kmajor_map(&mpl, at<__nv_bfloat16>(ws, pl.Plo), h, h, pl.ldc, p.batch, pl.hh, 128))
+    return UNSO_ERR_CUDA;
+  const int ydt = p.dt == UNSO_DTYPE_BF16 ? DT_BF16 : DT_F32;
+  cudaError_t e;
+  const bool pair = use_pair_engine();
+  if (p.tall) {
+    if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx, 128)) return UNSO_ERR_CUDA;
+    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, static_cast<int>(p.rows), h};
+    if (pair) {
+      const UmmaWork wa = umma2_make_work(static_cast<int>(p.rows), h, h, 256, static_cast<int>(p.batch), false, 1);
+      e = single ? launch_umma2<Cfg2ApplyTall1>(mx, mx, mph, mph, wa, epi, st)
+                 : launch_umma2<Cfg2ApplyTall2>(mx, mx, mph, mpl, wa, epi, st);
+    } else {
+      const UmmaWork wa = umma_make_work(static_cast<int>(p.rows), h, h, 128, static_cast<int>(p.batch), false, 1);
+      e = single ? launch_umma<CfgApplyTall1>(mx, mx, mph, mph, wa, epi, st)
+                 : launch_umma<CfgApplyTall2>(mx, mx, mph, mpl, wa, epi, st);
+    }
+  } else {
+    if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
+    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, h, static_cast<int>(p.cols)};
+    if (pair) {
+      const UmmaWork wa = umma2_make_work(h, static_cast<int>(p.cols), h, 256, static_cast<int>(p.batch), false, 1);
+      e = single ? launch_umma2<Cfg2ApplyWide1>(mph, mph, mx, mx, wa, epi, st)
+                 : launch_umma2<Cfg2ApplyWide2>(mph, mpl, mx, mx, wa, epi, st);
+    } else {
+      const UmmaWork wa = umma_make_work(h, static_cast<int>(p.cols), h, 128, static_cast<int>(p.batch), false, 1);
+      e = single ? launch_umma<CfgApplyWide1>(mph, mph, mx, mx, wa, epi, st)
+                 : launch_umma<CfgApplyWide2>(mph, mpl, mx, mx, wa, epi, st);
+    }
+  }
+  if (e != cudaSuccess) return UNSO_ERR_CUDA;
+  ++g_launches;
+  prof_mark(6, st);
+  return UNSO_OK;
+}
+
+// Multi-launch scale + chain from a finalized Gram G (large h, or gelfand scaling).
+static int32_t scale_chain_bf16_multi(const Problem& p, const Plan& pl, void* ws, const float* G, int32_t* status,
+                                      cudaStream_t st) {
   UNSO_TRY(norms_and_scalars<float>(p, pl, ws, G, scal_mode(p.scaling), status, st));
   if (p.scaling == UNSO_SCALING_GELFAND) UNSO_TRY(gelfand_scale<float>(p, pl, ws, G, DT_F32, status, st));
   const int h = static_cast<int>(p.h);
@@ -635,30 +718,103 @@ static int32_t unso_bf16_from_G(const Problem& p, const Plan& pl, void* ws, cons
     UNSO_CHECK_LAUNCH();
   }
   prof_mark(5, st);
-  const bool single = (p.flags & UNSO_FLAG_SINGLE_TERM_APPLY) != 0;
-  CUtensorMap mx, mph, mpl;
-  if (!umma_make_kmajor_map(&mph, at<__nv_bfloat16>(ws, pl.Phi), h, h, pl.ldc, p.batch, pl.hh, 128) ||
-      !umma_make_kmajor_map(&mpl, at<__nv_bfloat16>(ws, pl.Plo), h, h, pl.ldc, p.batch, pl.hh, 128))
-    return UNSO_ERR_CUDA;
-  const int ydt = p.dt == UNSO_DTYPE_BF16 ? DT_BF16 : DT_F32;
-  cudaError_t e;
-  if (p.tall) {
-    if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx, 128)) return UNSO_ERR_CUDA;
-    const UmmaWork wa = umma_make_work(static_cast<int>(p.rows), h, h, 128, static_cast<int>(p.batch), false, 1);
-    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, static_cast<int>(p.rows), h};
-    e = single ? launch_umma<CfgApplyTall1>(mx, mx, mph, mph, wa, epi, st)
-               : launch_umma<CfgApplyTall2>(mx, mx, mph, mpl, wa, epi, st);
-  } else {
-    if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
-    const UmmaWork wa = umma_make_work(h, static_cast<int>(p.cols), h, 128, static_cast<int>(p.batch), false, 1);
-    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, h, static_cast<int>(p.cols)};
-    e = single ? launch_umma<CfgApplyWide1>(mph, mph, mx, mx, wa, epi, st)
-               : launch_umma<CfgApplyWide2>(mph, mpl, mx, mx, wa, epi, st);
-  }
-  if (e != cudaSuccess) return UNSO_ERR_CUDA;
-  ++g_launches;
-  prof_mark(6, st);
   return UNSO_OK;
+}
+
+// Can the fused persistent chain run (all tiles co-resident, order and scaling supported)?
+static bool chain_persistent_fits(const Problem& p) {
+  if (p.order < 1 || p.order > CHAIN_MAX_ORDER || p.scaling == UNSO_SCALING_GELFAND) return false;
+  static int max_blocks_per_sm = -1;
+  if (max_blocks_per_sm < 0) {
+    if (cudaFuncSetAttribute(chain_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CH_SMEM) !=
+        cudaSuccess)
+      return false;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, chain_persistent_kernel, 256, CH_SMEM) != cudaSuccess)
+      return false;
+    max_blocks_per_sm = nb;
+  }
+  const int64_t nt = (p.h + 127) / 128;
+  const int64_t T = nt * (nt + 1) / 2 * p.batch;
+  return T <= static_cast<int64_t>(max_blocks_per_sm) * device_sm_count();
+}
+
+static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
+                                           int32_t* status, cudaStream_t st) {
+  const int h = static_cast<int>(p.h);
+  ChainMaps maps;
+  for (int buf = 0; buf < 2; ++buf) {
+    const void* base[2] = {at<__nv_bfloat16>(ws, pl.Chi[buf]), at<__nv_bfloat16>(ws, pl.Clo[buf])};
+    for (int hl = 0; hl < 2; ++hl) {
+      if (!umma_make_kmajor_map(&maps.m[buf][hl][0], base[hl], h, h, pl.ldc, p.batch, pl.hh, 128) ||
+          !umma_make_mnmajor_map(&maps.m[buf][hl][1], base[hl], h, h, pl.ldc, p.batch, pl.hh))
+        return UNSO_ERR_CUDA;
+    }
+  }
+  ChainParams cp;
+  std::memset(&cp, 0, sizeof(cp));
+  cp.part = part;
+  cp.splits = splits;
+  cp.h = h;
+  cp.nt = (h + 127) / 128;
+  cp.tiles_per_mat = cp.nt * (cp.nt + 1) / 2;
+  cp.batch = static_cast<int>(p.batch);
+  cp.ld = pl.ldc;
+  cp.mat = pl.hh;
+  for (int i = 0; i < 2; ++i) {
+    cp.chi[i] = at<__nv_bfloat16>(ws, pl.Chi[i]);
+    cp.clo[i] = at<__nv_bfloat16>(ws, pl.Clo[i]);
+  }
+  cp.phi = at<__nv_bfloat16>(ws, pl.Phi);
+  cp.plo = at<__nv_bfloat16>(ws, pl.Plo);
+  cp.normbuf = at<double>(ws, pl.normbuf);
+  cp.scal = at<double>(ws, pl.scal);
+  cp.status = status;
+  cp.gbar = at<unsigned>(ws, pl.gbar);
+  cp.order = p.order;
+  cp.scal_mode = scal_mode(p.scaling);
+  cp.alpha = 1.0;
+  for (int k = 0; k < p.order; ++k) {
+    cp.alpha += p.co[k];
+    cp.coef[k] = static_cast<float>(p.co[k]);
+  }
+  if (cudaMemsetAsync(cp.gbar, 0, sizeof(unsigned), st) != cudaSuccess) return UNSO_ERR_CUDA;
+  prof_mark(3, st);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(cp.tiles_per_mat * cp.batch));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = CH_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, chain_persistent_kernel, maps, cp) != cudaSuccess) return UNSO_ERR_CUDA;
+  ++g_launches;
+  prof_mark(4, st);
+  prof_mark(5, st);
+  return UNSO_OK;
+}
+
+// Everything after the Gram partials: scale, chain, P, apply.
+static int32_t unso_bf16_after_gram(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
+                                    int64_t bsx, const float* part, int splits, void* y, int32_t* status,
+                                    cudaStream_t st) {
+  if (chain_persistent_fits(p)) {
+    UNSO_TRY(scale_chain_bf16_persistent(p, pl, ws, part, splits, status, st));
+  } else {
+    float* G = at<float>(ws, pl.G);
+    if (part != G || splits != 1) {
+      const int nt = static_cast<int>((p.h + 31) / 32);
+      dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
+      finalize_sum_kernel<float><<<grid, 256, 0, st>>>(part, splits, static_cast<int>(p.batch), static_cast<int>(p.h),
+                                                       pl.ldc, G);
+      UNSO_CHECK_LAUNCH();
+    }
+    UNSO_TRY(scale_chain_bf16_multi(p, pl, ws, G, status, st));
+  }
+  return apply_bf16(p, pl, ws, xb, ldx, bsx, y, st);
 }
 
 // ---------------------------------------------------------------- NS baselines (FP32 precision)
@@ -813,9 +969,8 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
   prof_mark(1, st);
   UNSO_TRY(gram_bf16(p, pl, workspace, xb, ldx, bsx, st));
   prof_mark(2, st);
-  float* G = at<float>(workspace, pl.G);
-  UNSO_TRY(finalize_gram<float>(p, pl, workspace, pl.splits, G, st));
-  return unso_bf16_from_G(p, pl, workspace, xb, ldx, bsx, G, y_ptr, d_status, st);
+  return unso_bf16_after_gram(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.part), pl.splits, y_ptr,
+                              d_status, st);
 }
 
 int32_t unso_profile_begin(int32_t max_calls) {
@@ -911,7 +1066,7 @@ int32_t unso_orthogonalize_from_gram(const unso_matrix_desc* x, const void* x_pt
   const __nv_bfloat16* xb;
   int64_t ldx, bsx;
   UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
-  return unso_bf16_from_G(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.G), y_ptr, d_status, st);
+  return unso_bf16_after_gram(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.G), 1, y_ptr, d_status, st);
 }
 
 int32_t unso_scale_denominator(const unso_matrix_desc* x, const void* x_ptr, const unso_method_desc* method,

@@ -240,3 +240,65 @@ def test_pareto_spectrum_both_modes():
     print(f"pareto: fp32 {r32:.2e}  bf16 {rb:.2e}")
     assert r32 <= TOL["fp32"]
     assert rb <= TOL["bf16"]
+
+
+# ------------------------------------------------------------------ engine coverage (tcgen05 paths)
+@pytest.mark.parametrize("shape", [(65536, 512), (512, 65536), (9000, 640), (640, 9000)])
+def test_bf16_many_tiles_per_cta_pair(shape):
+    """More work items than CTA pairs (multi-tile accumulator ring, phase tracking), tall and
+    wide orientations, ragged h (640 is not a multiple of 256) -- against the oracle."""
+    m = O.gaussian_matrix(*shape, 21).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    _, y = run(m, spec, torch.float32, "bf16")
+    ref = O.run(bf16_round(m), "unso")["y"]
+    r = rel(y, ref)
+    print(f"bf16 {shape}: rel {r:.2e}")
+    assert r <= TOL["bf16"]
+
+
+def test_bf16_batched_persistent_chain():
+    ms = np.stack([O.gaussian_matrix(1024, 256, 30 + i) for i in range(8)]).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    y = U.orthogonalize(torch.from_numpy(ms).to(DEV), spec, precision="bf16").y.double().cpu().numpy()
+    for i in range(8):
+        assert rel(y[i], O.run(bf16_round(ms[i]), "unso")["y"]) <= TOL["bf16"]
+
+
+def test_bf16_multi_launch_chain_large_h():
+    """h = 2304: 171 upper 128-tiles > 148 SMs -> the multi-launch chain path; ragged vs 256."""
+    m = O.gaussian_matrix(4608, 2304, 40).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    _, y = run(m, spec, torch.float32, "bf16")
+    r = rel(y, O.run(bf16_round(m), "unso")["y"])
+    print(f"bf16 multi-launch chain h=2304: rel {r:.2e}")
+    assert r <= TOL["bf16"]
+
+
+def test_single_term_apply_option():
+    m = O.gaussian_matrix(8192, 512, 41).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), single_term_apply=True)
+    _, y = run(m, spec, torch.float32, "bf16")
+    r = rel(y, O.run(bf16_round(m), "unso")["y"])
+    print(f"single-term apply: rel {r:.2e}")
+    assert r <= TOL["bf16"]
+
+
+@pytest.mark.slow
+def test_cfg4_full_size_rows_against_oracle():
+    """configs[3] at full size (262144 x 2048 bf16): 2048 sampled rows of Y against the
+    oracle (fp64 Gram, chain and apply on the host), plus the whole Y against the
+    fp32-mode (fp64-grade) device path on the same input."""
+    g = torch.Generator(device=DEV).manual_seed(1234)
+    x = torch.randn(262144, 2048, generator=g, device=DEV).to(torch.bfloat16)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    yb = U.orthogonalize(x, spec, precision="bf16").y
+    y64 = U.orthogonalize(x.double(), spec, precision="fp32").y
+    r_dev = float((yb.double() - y64).norm() / y64.norm())
+    rows = np.sort(np.random.default_rng(0).choice(262144, 2048, replace=False))
+    ref = O.unso_rows_of_tall(x.double().cpu().numpy(), rows)
+    r_bf = rel(yb[torch.from_numpy(rows).to(DEV)].double().cpu().numpy(), ref)
+    r_64 = rel(y64[torch.from_numpy(rows).to(DEV)].cpu().numpy(), ref)
+    print(f"cfg4: bf16 vs oracle rows {r_bf:.2e}; fp32-mode vs oracle rows {r_64:.2e}; bf16 vs fp32-mode {r_dev:.2e}")
+    assert r_64 <= 1e-9
+    assert r_bf <= TOL["bf16"]
+    assert r_dev <= TOL["bf16"]
