@@ -44,7 +44,8 @@ def parse_args():
     ap.add_argument("--rows", type=int, default=262144)
     ap.add_argument("--cols", type=int, default=2048)
     ap.add_argument("--precision", choices=["bf16", "fp32"], default="bf16")
-    ap.add_argument("--single-term-apply", action="store_true")
+    ap.add_argument("--apply-terms", type=int, choices=[1, 2], default=None,
+                    help="bf16 apply split: default adaptive per matrix (device-side bound)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample-rows", type=int, default=32768)
     ap.add_argument("--ref-sample-rows", type=int, default=8192)
@@ -209,7 +210,7 @@ def main():
                                                                                       if args.precision == "bf16"
                                                                                       else torch.float32)
     spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), precision=args.precision,
-                        single_term_apply=args.single_term_apply)
+                        apply_terms=args.apply_terms)
     y = torch.empty_like(x)
 
     def step():
@@ -219,9 +220,11 @@ def main():
             orthogonalize_row_sharded(x, spec, out=y, check=False)
 
     # ---- correctness gate (untimed): status + orthogonality of the output
+    apply_info = None
     if world == 1:
         res = U.orthogonalize(x, spec, out=y, check=True)
         launches_per_step = res.launches
+        apply_info = res.info[0] if res.info else None
     else:
         orthogonalize_row_sharded(x, spec, out=y, check=True)
         launches_per_step = None
@@ -347,7 +350,8 @@ def main():
             "config": {"workload": f"configs[3]: one {rows}x{cols} {args.precision} matrix, UNSO order-14 "
                                    "shipped coefficients", "global_batch": 1, "shape": [rows, cols],
                        "precision_recipe": ("bf16 Gram, bf16x3 C-form chain, "
-                                            + ("bf16" if args.single_term_apply else "bf16x2") + " apply")
+                                            + {None: "adaptive bf16/bf16x2 (shifted P)", 1: "bf16", 2: "bf16x2"}[
+                                                args.apply_terms] + " apply")
                        if args.precision == "bf16" else "fp64-grade DFMA",
                        "parallelism": f"row-shard x{world} + NCCL all-reduce of G" if world > 1 else "1 GPU",
                        "l2": "input 1 GiB > 126 MB L2 (no flush needed)"},
@@ -362,6 +366,9 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "ortho_error": ortho_err,
+            "apply_decision": None if apply_info is None else {
+                "single_term": bool(apply_info["apply_single"]), "bound": apply_info["apply_bound"],
+                "shift": apply_info["shift"]},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -59,7 +59,11 @@ typedef enum unso_scaling {
 typedef enum unso_method { UNSO_METHOD_UNSO = 0, UNSO_METHOD_ORIGINAL_NS = 1, UNSO_METHOD_QUINTIC = 2 } unso_method;
 
 /* flags */
-#define UNSO_FLAG_SINGLE_TERM_APPLY 0x1 /* BF16: apply with P rounded to one bf16 term (faster, less accurate) */
+#define UNSO_FLAG_SINGLE_TERM_APPLY 0x1 /* BF16: always apply with one bf16 term of P (faster, less accurate) */
+#define UNSO_FLAG_TWO_TERM_APPLY 0x2    /* BF16: always apply with the bf16x2 (hi + lo) split of P.
+                                           Default (neither flag): per matrix, the lo term is dropped on the
+                                           device when ||X dR||_F / ||Y||_F <= 2^-9 ||R||_F / sqrt(tr C_1) <= 5e-3
+                                           (R = P - d I, d = tr(P)/h; d X is added exactly in the epilogue). */
 
 typedef struct unso_matrix_desc {
   int64_t rows, cols;    /* per matrix, as given (orientation is chosen internally, ortho.py:149-150) */
@@ -126,6 +130,14 @@ int32_t unso_scale_denominator(const unso_matrix_desc* x, const void* x_ptr, con
  * writes `batch` doubles to device memory d_err. */
 int32_t unso_ortho_error(const unso_matrix_desc* y, const void* y_ptr, double* d_err, void* workspace,
                          size_t workspace_bytes, void* stream);
+
+/* Copy the per-matrix scalars the last call on this workspace produced into device memory
+ * d_out (batch x UNSO_SCALARS doubles): [0] trace(G), [1] ||G||_F^2, [2] ||G - I||_F^2, [3] s^2,
+ * [4] 1/s, [5] ortho error, [6] d/s identity shift, [7] apply mode (1 = P_lo term skipped),
+ * [8] the adaptive bound.  Same descriptors as the call. */
+#define UNSO_SCALARS 16
+int32_t unso_query_scalars(const unso_matrix_desc* x, const unso_method_desc* method, const void* workspace,
+                           double* d_out, void* stream);
 
 /* Number of CUDA kernels launched by the last successful call on this thread. */
 int32_t unso_last_launch_count(void);

@@ -33,7 +33,11 @@ EXPORTED_SYMBOLS = (
     "unso_version", "unso_status_string", "unso_workspace_size", "unso_orthogonalize", "unso_gram",
     "unso_gram_dtype", "unso_orthogonalize_from_gram", "unso_scale_denominator", "unso_ortho_error",
     "unso_last_launch_count", "unso_profile_begin", "unso_profile_read", "unso_profile_end",
+    "unso_query_scalars",
 )
+SCALARS = 16
+SCALAR_NAMES = ("trace", "fro2", "dev2", "s2", "inv_s", "ortho_error", "shift", "apply_single", "apply_bound")
+FLAG_TWO_TERM_APPLY = 0x2
 PROFILE_STAGES = ("convert", "gram", "scale_prep", "chain", "finalize_p", "apply")
 
 
@@ -81,6 +85,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.unso_profile_begin.argtypes = [ctypes.c_int32]
     lib.unso_profile_read.restype = ctypes.c_int32
     lib.unso_profile_read.argtypes = [P, ctypes.c_int32]
+    lib.unso_query_scalars.restype = ctypes.c_int32
+    lib.unso_query_scalars.argtypes = [XD, MD, P, P, P]
     lib.unso_profile_end.restype = None
     lib.unso_profile_end.argtypes = []
 

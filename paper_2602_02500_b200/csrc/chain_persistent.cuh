@@ -38,7 +38,10 @@ struct ChainParams {
   __nv_bfloat16* clo[2];
   __nv_bfloat16* phi;  // out: P/s, full symmetric
   __nv_bfloat16* plo;
-  double* normbuf;     // [tiles][2]
+  double* normbuf;     // [tiles][2]  phase-A norms
+  double* pstat;       // [tiles][2]  final-P statistics (trace, weighted sum of squares)
+  int adaptive;        // 1: decide per matrix whether the apply may drop the P_lo term
+  double tau;          // bound threshold for that decision
   double* scal;        // [batch][SCAL_STRIDE]
   int32_t* status;     // [batch]
   unsigned* gbar;      // zeroed before launch
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     }
     named_bar_sync(1, 128);
     const float inv_s2 = static_cast<float>(s_scale[0]);
-    const float inv_s = static_cast<float>(s_scale[1]);
+    (void)0;
 
     // ---- C_1 = G / s^2 (TMEM + global buffer 0), P = alpha I - coef_1 C_1 (TMEM)
     for (int c = 0; c < 4; ++c) {
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
           const float pv = __uint_as_float(up[j]) - coef * cn;
           uc[j] = __float_as_uint(cn);
           up[j] = __float_as_uint(pv);
-          split_bf16(last ? pv * inv_s : cn, hi[j], lo[j]);
+          split_bf16(cn, hi[j], lo[j]);
         }
         if (!last) {
           tmem_st32(lane_base + CH_C + c * 32, uc);
@@ -328,18 +331,8 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
               *reinterpret_cast<uint4*>(p.clo[nb] + o + j) = *reinterpret_cast<const uint4*>(lo + j);
             }
           }
-        } else if (row_ok) {
-          // P/s -> full symmetric bf16 hi/lo for the apply; diagonal tiles own c >= r only
-          for (int j = 0; j < 32; ++j) {
-            const int gc = gc0 + j;
-            if (gc >= p.h || (ti == tj && gc < gr)) continue;
-            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
-            const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
-            p.phi[o] = hi[j];
-            p.plo[o] = lo[j];
-            p.phi[om] = hi[j];
-            p.plo[om] = lo[j];
-          }
+        } else {
+          tmem_st32(lane_base + CH_P + c * 32, up);  // final P stays in TMEM for the shifted split
         }
       }
       tmem_wait_st();
@@ -351,23 +344,79 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         if (tid == 0) grid_arrive(p.gbar);  // round k+1: C_{k+1} published
       }
     }
-    if (N == 1 && row_ok) {  // no squaring: P = (1+b) I - b C_1
+    // ---- final P: statistics -> identity shift d and the adaptive apply decision, then
+    //      R/s = (P - d I)/s split into bf16 hi/lo, written symmetric for the apply.
+    {
+      double trp = 0.0, sp2 = 0.0;
       for (int c = 0; c < 4; ++c) {
         const int gc0 = tj * 128 + c * 32;
         uint32_t up[32];
         tmem_ld32(lane_base + CH_P + c * 32, up);
         tmem_wait_ld();
+#pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int gc = gc0 + j;
-          if (gc >= p.h || (ti == tj && gc < gr)) continue;
-          __nv_bfloat16 hi, lo;
-          split_bf16(__uint_as_float(up[j]) * inv_s, hi, lo);
-          const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
-          const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
-          p.phi[o] = hi;
-          p.plo[o] = lo;
-          p.phi[om] = hi;
-          p.plo[om] = lo;
+          const bool ok = row_ok && gc0 + j < p.h;
+          const double v = ok ? static_cast<double>(__uint_as_float(up[j])) : 0.0;
+          if (ok && gc0 + j == gr) trp += v;
+          sp2 += wgt * v * v;
+        }
+      }
+      trp = warp_sum(trp);
+      sp2 = warp_sum(sp2);
+      if (lane == 0) {
+        red[0][ew] = trp;
+        red[1][ew] = sp2;
+      }
+      named_bar_sync(1, 128);
+      if (tid == 0) {
+        p.pstat[blockIdx.x * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+        p.pstat[blockIdx.x * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+        // rounds so far: 0 (norms), 1 (C_1), 2..N-1 (C_{k+1}, k < N-1); this is the next one
+        const unsigned round = N >= 2 ? static_cast<unsigned>(N) : 2u;
+        grid_arrive(p.gbar);
+        grid_wait(p.gbar, (round + 1) * static_cast<unsigned>(T));
+        double tp = 0.0, s2p = 0.0;
+        const int first = b * p.tiles_per_mat;
+        for (int q = 0; q < p.tiles_per_mat; ++q) {
+          tp += __ldcg(&p.pstat[(first + q) * 2 + 0]);
+          s2p += __ldcg(&p.pstat[(first + q) * 2 + 1]);
+        }
+        const double d = tp / p.h;
+        const double r2 = fmax(s2p - tp * tp / p.h, 0.0);
+        // ||X (R_hat - R)||_F <= ||X||_2 2^-9 ||R||_F with ||X||_2 <= 1 (gram/plain scaling), and
+        // ||Y||_F >= min_sigma f(sigma)/sigma * ||X||_F = sqrt(tr C_1) (min f(s)/s = f(1) = 1).
+        const double trc = fmax(s_scale[0] * __ldcg(&p.scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_TRACE]), 0.0);
+        const double bound = ldexp(sqrt(r2), -9) / fmax(sqrt(trc), 1e-300);
+        const bool single = p.adaptive && bound <= p.tau;
+        s_scale[0] = d;
+        if (t == 0) {
+          double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
+          o[S_SHIFT] = d * s_scale[1];
+          o[S_MODE] = single ? 1.0 : 0.0;
+          o[S_BOUND] = bound;
+        }
+      }
+      named_bar_sync(1, 128);
+      const double d = s_scale[0];
+      for (int c = 0; c < 4; ++c) {
+        const int gc0 = tj * 128 + c * 32;
+        uint32_t up[32];
+        tmem_ld32(lane_base + CH_P + c * 32, up);  // warp-collective: every lane, row_ok or not
+        tmem_wait_ld();
+        if (row_ok) {
+          for (int j = 0; j < 32; ++j) {
+            const int gc = gc0 + j;
+            if (gc >= p.h || (ti == tj && gc < gr)) continue;
+            const double rv = static_cast<double>(__uint_as_float(up[j])) - (gc == gr ? d : 0.0);
+            __nv_bfloat16 hi, lo;
+            split_bf16(static_cast<float>(rv * s_scale[1]), hi, lo);
+            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
+            const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
+            p.phi[o] = hi;
+            p.plo[o] = lo;
+            p.phi[om] = hi;
+            p.plo[om] = lo;
+          }
         }
       }
     }

@@ -10,8 +10,12 @@ namespace unso {
 constexpr int NORM_BLOCKS = 64;  // per-matrix partial-reduction blocks (fixed -> deterministic)
 
 // scal[b * SCAL_STRIDE + ...]
-enum ScalSlot : int { S_TRACE = 0, S_FRO2 = 1, S_DEV2 = 2, S_S2 = 3, S_INV_S = 4, S_ERR = 5 };
-constexpr int SCAL_STRIDE = 8;
+// S_SHIFT: d/s, the identity shift removed from P before the bf16 split (added back as d/s * X in the
+// apply epilogue); S_MODE: 1 = the apply may skip the P_lo term (adaptive bound met); S_BOUND: that bound.
+enum ScalSlot : int {
+  S_TRACE = 0, S_FRO2 = 1, S_DEV2 = 2, S_S2 = 3, S_INV_S = 4, S_ERR = 5, S_SHIFT = 6, S_MODE = 7, S_BOUND = 8
+};
+constexpr int SCAL_STRIDE = 16;
 
 // ------------------------------------------------------------------ conversion
 // dst[b](r, c) = src[b](r, c) * (scal ? scal[b].inv_s : 1), any dtype -> any dtype.
@@ -180,6 +184,9 @@ __global__ void scalars_kernel(const double* __restrict__ blk, int nblk, int mod
   o[S_TRACE] = s0;
   o[S_FRO2] = s1;
   o[S_DEV2] = s2v;
+  o[S_SHIFT] = 0.0;
+  o[S_MODE] = 0.0;
+  o[S_BOUND] = -1.0;
   if (mode == SM_NONE) {  // bare kernel on pre-scaled input: no rescale, no degenerate check
     o[S_S2] = 1.0;
     o[S_INV_S] = 1.0;

@@ -13,11 +13,12 @@
 
 namespace unso {
 
-template <int BN_, int NA_, int NB_, int NT_, int TERMS_, bool A_MN_, bool B_MN_, int STAGES_>
+// OPT: 0 = all tiles always used; 1 = B tile 1 optional; 2 = A tile 1 optional (see UmmaWork::opt_skip).
+template <int BN_, int NA_, int NB_, int NT_, int TERMS_, bool A_MN_, bool B_MN_, int STAGES_, int OPT_ = 0>
 struct Umma2Cfg {
   static constexpr int BM = 256, BN = BN_, BK = 64;       // pair tile
   static constexpr int HB = BN / 2;                        // B rows per CTA
-  static constexpr int NA = NA_, NB = NB_, NT = NT_, TERMS = TERMS_, STAGES = STAGES_;
+  static constexpr int NA = NA_, NB = NB_, NT = NT_, TERMS = TERMS_, STAGES = STAGES_, OPT = OPT_;
   static constexpr bool A_MN = A_MN_, B_MN = B_MN_;
   static constexpr int A_TILE = 128 * BK * 2;
   static constexpr int B_TILE = HB * BK * 2;
@@ -92,16 +93,19 @@ __global__ void __launch_bounds__(256, 1)
         umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
         const int arow = tm * Cfg::BM + static_cast<int>(rank) * 128;
         const int brow = tn * Cfg::BN + static_cast<int>(rank) * Cfg::HB;
+        const bool skip = Cfg::OPT != 0 && work.opt_skip && work.opt_skip[static_cast<int64_t>(b) * work.opt_stride] != 0.0;
+        const uint32_t bytes = 2 * (Cfg::STAGE_BYTES - (skip ? (Cfg::OPT == 1 ? Cfg::B_TILE : Cfg::A_TILE) : 0));
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
           const uint32_t lbar = lbar0 + stage * 8;
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
           load_operand_tile_pair<Cfg::A_MN, 128>(&tmA0, lbar, st, kt * 64, arow, b);
-          if (Cfg::NA > 1) load_operand_tile_pair<Cfg::A_MN, 128>(&tmA1, lbar, st + Cfg::A_TILE, kt * 64, arow, b);
+          if (Cfg::NA > 1 && !(skip && Cfg::OPT == 2))
+            load_operand_tile_pair<Cfg::A_MN, 128>(&tmA1, lbar, st + Cfg::A_TILE, kt * 64, arow, b);
           uint8_t* sb = st + Cfg::NA * Cfg::A_TILE;
           load_operand_tile_pair<Cfg::B_MN, Cfg::HB>(&tmB0, lbar, sb, kt * 64, brow, b);
-          if (Cfg::NB > 1)
+          if (Cfg::NB > 1 && !(skip && Cfg::OPT == 1))
             load_operand_tile_pair<Cfg::B_MN, Cfg::HB>(&tmB1, lbar, sb + Cfg::B_TILE, kt * 64, brow, b);
           if (++stage == Cfg::STAGES) {
             stage = 0;
@@ -119,6 +123,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int idx = cluster; idx < work.num_work; idx += nclusters) {
         int b, split, tm, tn, kt0, kt1;
         umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
+        const bool skip = Cfg::OPT != 0 && work.opt_skip && work.opt_skip[static_cast<int64_t>(b) * work.opt_stride] != 0.0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * Cfg::BN);
@@ -133,6 +138,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int t = 0; t < Cfg::NT; ++t) {
               const int ai = (Cfg::TERMS >> (2 * t)) & 1;
               const int bi = (Cfg::TERMS >> (2 * t + 1)) & 1;
+              if (skip && ((Cfg::OPT == 1 && bi == 1) || (Cfg::OPT == 2 && ai == 1))) continue;
               const uint64_t ad = operand_desc<Cfg::A_MN>(st + ai * Cfg::A_TILE, ks);
               const uint64_t bd = operand_desc<Cfg::B_MN>(sb + bi * Cfg::B_TILE, ks);
               umma_bf16_pair(d_tmem, ad, bd, Cfg::IDESC, (kt > kt0 || ks > 0 || t > 0) ? 1u : 0u);

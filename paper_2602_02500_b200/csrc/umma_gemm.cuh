@@ -23,6 +23,10 @@ namespace unso {
 
 struct UmmaWork {
   int tiles_m, tiles_n, syrk, splits, k_tiles, batch, tiles_valid, num_work;
+  // Optional second operand tile (CTA-pair engine, Cfg::OPT != 0): skipped for matrix b when
+  // opt_skip[b * opt_stride] != 0 (device-side decision written by an earlier kernel).
+  const double* opt_skip = nullptr;
+  int opt_stride = 0;
 };
 
 __device__ __forceinline__ void umma_decode(const UmmaWork& w, int idx, int& b, int& split, int& tm, int& tn,

@@ -236,8 +236,32 @@ struct UEpiOut {
   int dt;  // DT_BF16 or DT_F32
   int64_t ld, bs;
   int M, N;
-  __device__ void operator()(int b, int, int row, int col0, const float* v) const {
+  // identity shift: Y += scal[b].shift * X (X = the bf16 operand, same indexing as Y)
+  const __nv_bfloat16* x = nullptr;
+  int64_t xld = 0, xbs = 0;
+  const double* scal = nullptr;
+  __device__ void operator()(int b, int, int row, int col0, const float* vin) const {
     if (row >= M) return;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = vin[j];
+    if (x) {
+      const float sh = static_cast<float>(scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_SHIFT]);
+      if (sh != 0.0f) {
+        const __nv_bfloat16* xr = x + static_cast<int64_t>(b) * xbs + static_cast<int64_t>(row) * xld + col0;
+        if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            __align__(16) __nv_bfloat16 t[8];
+            *reinterpret_cast<uint4*>(t) = *reinterpret_cast<const uint4*>(xr + j);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[j + q] = fmaf(sh, __bfloat162float(t[q]), v[j + q]);
+          }
+        } else {
+          for (int j = 0; j < 32 && col0 + j < N; ++j) v[j] = fmaf(sh, __bfloat162float(xr[j]), v[j]);
+        }
+      }
+    }
     const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + col0;
     if (dt == DT_BF16) {
       __nv_bfloat16* y = static_cast<__nv_bfloat16*>(out) + o;
@@ -278,9 +302,9 @@ using CfgApplyWide1 = UmmaCfg<128, 1, 1, 1, TERM(0, 0, 0), false, true, 6>;
 // CTA-pair (cta_group::2) 256 x 256 tiles
 using Cfg2GramK = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, false, 6>;
 using Cfg2GramMN = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), true, true, 6>;
-using Cfg2ApplyTall2 = Umma2Cfg<256, 1, 2, 2, TERM(0, 0, 0) | TERM(1, 0, 1), false, false, 4>;
+using Cfg2ApplyTall2 = Umma2Cfg<256, 1, 2, 2, TERM(0, 0, 0) | TERM(1, 0, 1), false, false, 4, 1>;
 using Cfg2ApplyTall1 = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, false, 6>;
-using Cfg2ApplyWide2 = Umma2Cfg<256, 2, 1, 2, TERM(0, 0, 0) | TERM(1, 1, 0), false, true, 4>;
+using Cfg2ApplyWide2 = Umma2Cfg<256, 2, 1, 2, TERM(0, 0, 0) | TERM(1, 1, 0), false, true, 4, 2>;
 using Cfg2ApplyWide1 = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, true, 6>;
 
 // Engine selection: CTA pairs by default; UNSO_ENGINE=1cta forces the 1-CTA 128x128 engine (A/B tests).
@@ -363,7 +387,7 @@ struct Plan {
   size_t C[2] = {0, 0}, P = 0, Pout = 0;          // FP32
   size_t Chi[2] = {0, 0}, Clo[2] = {0, 0}, Phi = 0, Plo = 0;  // BF16 (P reused as f32)
   size_t Gk[2] = {0, 0};                          // gelfand powers
-  size_t normbuf = 0, gbar = 0;                   // persistent chain: per-tile norms, grid barrier
+  size_t normbuf = 0, pstat = 0, gbar = 0;        // persistent chain: per-tile norms / P stats, grid barrier
   size_t Xs[2] = {0, 0};                          // NS state (f64)
 };
 
@@ -409,6 +433,7 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
   const bool bf = !for_error && p.prec == UNSO_PREC_BF16;
   const size_t ge = bf ? 4 : 8;  // Gram element size
   pl.splits = with_gram ? gram_splits(p) : 1;
+  pl.scal = take(pl, static_cast<size_t>(B) * SCAL_STRIDE * 8);  // first: same offset for every plan
   pl.ldx = p.ld;
   pl.xcopy = false;
   if (bf) {
@@ -421,7 +446,6 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
   if (with_gram) pl.part = take(pl, static_cast<size_t>(pl.splits) * B * pl.hh * ge);
   pl.G = take(pl, static_cast<size_t>(B * pl.hh) * ge);
   pl.blk = take(pl, static_cast<size_t>(B) * NORM_BLOCKS * 3 * 8);
-  pl.scal = take(pl, static_cast<size_t>(B) * SCAL_STRIDE * 8);
   if (for_error) return pl;
   if (p.scaling == UNSO_SCALING_GELFAND && p.gpow > 1) {
     pl.Gk[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
@@ -438,6 +462,7 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       pl.Plo = take(pl, static_cast<size_t>(B * pl.hh) * 2);
       const int64_t nt = (p.h + 127) / 128;
       pl.normbuf = take(pl, static_cast<size_t>(nt * (nt + 1) / 2 * B) * 2 * 8);
+      pl.pstat = take(pl, static_cast<size_t>(nt * (nt + 1) / 2 * B) * 2 * 8);
       pl.gbar = take(pl, 256);
     } else {
       pl.C[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
@@ -649,9 +674,11 @@ static int32_t apply_bf16(const Problem& p, const Plan& pl, void* ws, const __nv
   const bool pair = use_pair_engine();
   if (p.tall) {
     if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx, 128)) return UNSO_ERR_CUDA;
-    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, static_cast<int>(p.rows), h};
+    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, static_cast<int>(p.rows), h, xb, ldx, bsx, at<double>(ws, pl.scal)};
     if (pair) {
-      const UmmaWork wa = umma2_make_work(static_cast<int>(p.rows), h, h, 256, static_cast<int>(p.batch), false, 1);
+      UmmaWork wa = umma2_make_work(static_cast<int>(p.rows), h, h, 256, static_cast<int>(p.batch), false, 1);
+      wa.opt_skip = at<double>(ws, pl.scal) + S_MODE;
+      wa.opt_stride = SCAL_STRIDE;
       e = single ? launch_umma2<Cfg2ApplyTall1>(mx, mx, mph, mph, wa, epi, st)
                  : launch_umma2<Cfg2ApplyTall2>(mx, mx, mph, mpl, wa, epi, st);
     } else {
@@ -661,9 +688,11 @@ static int32_t apply_bf16(const Problem& p, const Plan& pl, void* ws, const __nv
     }
   } else {
     if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
-    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, h, static_cast<int>(p.cols)};
+    UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, h, static_cast<int>(p.cols), xb, ldx, bsx, at<double>(ws, pl.scal)};
     if (pair) {
-      const UmmaWork wa = umma2_make_work(h, static_cast<int>(p.cols), h, 256, static_cast<int>(p.batch), false, 1);
+      UmmaWork wa = umma2_make_work(h, static_cast<int>(p.cols), h, 256, static_cast<int>(p.batch), false, 1);
+      wa.opt_skip = at<double>(ws, pl.scal) + S_MODE;
+      wa.opt_stride = SCAL_STRIDE;
       e = single ? launch_umma2<Cfg2ApplyWide1>(mph, mph, mx, mx, wa, epi, st)
                  : launch_umma2<Cfg2ApplyWide2>(mph, mpl, mx, mx, wa, epi, st);
     } else {
@@ -768,6 +797,10 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
   cp.phi = at<__nv_bfloat16>(ws, pl.Phi);
   cp.plo = at<__nv_bfloat16>(ws, pl.Plo);
   cp.normbuf = at<double>(ws, pl.normbuf);
+  cp.pstat = at<double>(ws, pl.pstat);
+  // adaptive P_lo skipping needs ||X||_2 <= 1, i.e. a gram/plain-scaled input
+  cp.adaptive = ((p.flags & UNSO_FLAG_TWO_TERM_APPLY) == 0 && p.scaling != UNSO_SCALING_NONE) ? 1 : 0;
+  cp.tau = 5e-3;
   cp.scal = at<double>(ws, pl.scal);
   cp.status = status;
   cp.gbar = at<unsigned>(ws, pl.gbar);
@@ -971,6 +1004,19 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
   prof_mark(2, st);
   return unso_bf16_after_gram(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.part), pl.splits, y_ptr,
                               d_status, st);
+}
+
+int32_t unso_query_scalars(const unso_matrix_desc* x, const unso_method_desc* method, const void* workspace,
+                           double* d_out, void* stream) {
+  Problem p;
+  UNSO_TRY(make_problem(x, method, p));
+  if (!workspace || !d_out) return UNSO_ERR_VALUE;
+  static_assert(SCAL_STRIDE == UNSO_SCALARS, "scalar block layout");
+  const Plan pl = make_plan(p, true);
+  if (cudaMemcpyAsync(d_out, static_cast<const char*>(workspace) + pl.scal, sizeof(double) * SCAL_STRIDE * p.batch,
+                      cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return UNSO_ERR_CUDA;
+  return UNSO_OK;
 }
 
 int32_t unso_profile_begin(int32_t max_calls) {

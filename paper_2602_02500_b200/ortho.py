@@ -74,7 +74,7 @@ class MethodSpec:
     scaling: Scaling | None = None
     gelfand_power: int = 2
     precision: Precision | None = None
-    single_term_apply: bool = False
+    apply_terms: int | None = None   # bf16 mode: None = adaptive per matrix, 1 = P_hi only, 2 = P_hi + P_lo
 
     def __post_init__(self):
         kind = MethodKind(self.kind)
@@ -85,6 +85,8 @@ class MethodSpec:
             object.__setattr__(self, "precision", Precision(self.precision))
         if self.gelfand_power < 1:
             raise ValueError("gelfand_power must be >= 1")
+        if self.apply_terms not in (None, 1, 2):
+            raise ValueError("apply_terms must be None (adaptive), 1 or 2")
         if kind is MethodKind.UNSO:
             if self.coeffs is None:
                 raise ValueError("unso requires a CoefficientSet")
@@ -135,6 +137,7 @@ class OrthoResult:
     executed_matmul_shapes: list[tuple[int, int, int]] = field(default_factory=list)
     precision: str = "fp32"
     launches: int = 0
+    info: dict | None = None         # per-matrix device scalars (scale, apply decision, bound) when check=True
 
 
 class FlopsCounter:
@@ -300,7 +303,7 @@ def _method_desc(spec: MethodSpec, precision: Precision, scaling_code: int):
         co = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1)
         method, order, steps = N.METHOD_QUINTIC, 0, rows.shape[0]
     co = np.ascontiguousarray(co, dtype=np.float64)
-    flags = N.FLAG_SINGLE_TERM_APPLY if spec.single_term_apply else 0
+    flags = {None: 0, 1: N.FLAG_SINGLE_TERM_APPLY, 2: N.FLAG_TWO_TERM_APPLY}[spec.apply_terms]
     md = N.MethodDesc(method, scaling_code, spec.gelfand_power,
                       N.PREC_BF16 if precision is Precision.BF16 else N.PREC_FP32, order, steps,
                       co.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), flags, 0)
@@ -355,10 +358,17 @@ def _run(m: torch.Tensor, spec: MethodSpec, scaling_code: int, precision, out, c
                                       ctypes.byref(md), ctypes.c_void_p(ws.data_ptr()), ctypes.c_size_t(ws.numel()),
                                       ctypes.c_void_p(status.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
         launches = N.launch_count()
+        info = None
+        if code == N.OK and check:
+            sc = torch.empty(xd.batch, N.SCALARS, dtype=torch.float64, device=device)
+            if lib.unso_query_scalars(ctypes.byref(xd), ctypes.byref(md), ctypes.c_void_p(ws.data_ptr()),
+                                      ctypes.c_void_p(sc.data_ptr()), ctypes.c_void_p(stream.cuda_stream)) == N.OK:
+                rows = sc.cpu().numpy()
+                info = [dict(zip(N.SCALAR_NAMES, map(float, r))) for r in rows]
     del co
     N.check(code, "unso_orthogonalize")
     _status_check(status, check)
-    return y, prec, launches
+    return y, prec, launches, info
 
 
 def _hw(m: torch.Tensor) -> tuple[int, int, bool]:
@@ -373,12 +383,12 @@ def orthogonalize(m: torch.Tensor, spec: MethodSpec, *, precision=None, out=None
     """preprocess -> kernel -> restore orientation (ortho.py:267-283), fused on the device."""
     h, w, tall = _hw(m)
     scaling = spec.effective_scaling
-    y, prec, launches = _run(m, spec, _SCALING[scaling], precision, out, check)
+    y, prec, launches, info = _run(m, spec, _SCALING[scaling], precision, out, check)
     return OrthoResult(y=y, flops=kernel_model_flops(h, w, spec), was_transposed=tall,
                        preprocess_flops=preprocess_model_flops(h, w, scaling, spec.gelfand_power),
                        kernel_matmul_shapes=model_matmul_shapes(h, w, spec),
                        executed_matmul_shapes=executed_matmul_shapes(h, w, spec), precision=prec.value,
-                       launches=launches)
+                       launches=launches, info=info)
 
 
 def scale_denominator(m: torch.Tensor, scaling: Scaling, gelfand_power: int = 2, check: bool = True) -> torch.Tensor:
@@ -426,7 +436,7 @@ def _bare(x: torch.Tensor, spec: MethodSpec, counter, precision, check=False) ->
     h, w = x.shape[-2], x.shape[-1]
     if h > w:
         raise ShapeError(f"kernel expects rows <= cols, got {h}x{w}")  # ortho.py:186-187, 211-212, 223-224
-    y, _, _ = _run(x, spec, N.SCALING_NONE, precision, None, check)
+    y, _, _, _ = _run(x, spec, N.SCALING_NONE, precision, None, check)
     if counter is not None:
         for s in model_matmul_shapes(h, w, spec):
             counter.matmul_shapes.append(s)

@@ -276,7 +276,7 @@ def test_bf16_multi_launch_chain_large_h():
 
 def test_single_term_apply_option():
     m = O.gaussian_matrix(8192, 512, 41).astype(np.float32)
-    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), single_term_apply=True)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), apply_terms=1)
     _, y = run(m, spec, torch.float32, "bf16")
     r = rel(y, O.run(bf16_round(m), "unso")["y"])
     print(f"single-term apply: rel {r:.2e}")
@@ -302,3 +302,28 @@ def test_cfg4_full_size_rows_against_oracle():
     assert r_64 <= 1e-9
     assert r_bf <= TOL["bf16"]
     assert r_dev <= TOL["bf16"]
+
+
+def test_adaptive_apply_decision():
+    """Default bf16 apply: P_lo is dropped on the device only when the bound allows it;
+    a well-conditioned Gaussian takes the single-term path, an ill-conditioned one keeps two
+    terms, and both stay within tolerance (and match the forced two-term path closely)."""
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    spec2 = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), apply_terms=2)
+    g = O.gaussian_matrix(32768, 512, 50).astype(np.float32)
+    rng = np.random.default_rng(51)
+    s = np.exp(rng.uniform(np.log(1e-4), 0, 512))
+    ill = O.controlled_spectrum_matrix(2048, 512, s, 52).astype(np.float32)
+    for m, expect_single in ((g, True), (ill, False)):
+        x = torch.from_numpy(m).to(DEV)
+        res = U.orthogonalize(x, spec, precision="bf16")
+        info = res.info[0]
+        y = res.y.double().cpu().numpy()
+        ref = O.run(bf16_round(m), "unso")["y"]
+        r = rel(y, ref)
+        r2 = rel(U.orthogonalize(x, spec2, precision="bf16").y.double().cpu().numpy(), ref)
+        print(f"adaptive apply: single={info['apply_single']} bound={info['apply_bound']:.2e} rel={r:.2e} (two-term {r2:.2e})")
+        assert bool(info["apply_single"]) == expect_single
+        assert r <= TOL["bf16"]
+        if expect_single:
+            assert r <= info["apply_bound"] + 2 * r2
