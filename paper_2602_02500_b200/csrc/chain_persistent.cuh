@@ -62,7 +62,11 @@ __device__ __forceinline__ void grid_arrive(unsigned* gbar) {
   red_release_gpu_add(gbar, 1u);
 }
 __device__ __forceinline__ void grid_wait(const unsigned* gbar, unsigned target) {
-  while (ld_acquire_gpu(gbar) < target) __nanosleep(64);
+  const long long t0 = clock64();
+  while (ld_acquire_gpu(gbar) < target) {
+    __nanosleep(64);
+    if (clock64() - t0 > UNSO_WATCHDOG_CYCLES) __trap();
+  }
 }
 
 __device__ __forceinline__ void ch_load_block(const ChainMaps& maps, int buf, int hl, uint64_t* bar, uint8_t* dst,

@@ -36,9 +36,15 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Watchdog: a wait that exceeds ~2^35 SM cycles (~18 s at 1.9 GHz) traps instead of hanging the
+// GPU forever (a protocol bug then surfaces as a launch error, not a wedged device).
+constexpr long long UNSO_WATCHDOG_CYCLES = 1ll << 35;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > UNSO_WATCHDOG_CYCLES) __trap();
   }
 }
 

@@ -6,6 +6,11 @@
 // ncu (profiles/round1_ncu_summary.md).  Accumulator: rows [128r, 128r+128) of the
 // 256 x BN tile live in CTA r's TMEM (double-buffered, 2 x BN columns).
 //
+// Warp roles: 0 TMA producer (both CTAs), 1 MMA issuer (leader), 2 TMEM allocator,
+// 3 idle, 4.. epilogue (EPI_WARPS warps: warp w reads TMEM lanes 32*(w%4).., the
+// (w-4)/4-th column group of the tile), so the epilogue of one tile overlaps the
+// mainloop of the next even when the tile's K-loop is short.
+//
 // Same term/operand conventions as umma_gemm.cuh; the epilogue functor receives
 // (b, split, row, col0, v[32]) for the CTA's own rows.
 #pragma once
@@ -14,11 +19,14 @@
 namespace unso {
 
 // OPT: 0 = all tiles always used; 1 = B tile 1 optional; 2 = A tile 1 optional (see UmmaWork::opt_skip).
-template <int BN_, int NA_, int NB_, int NT_, int TERMS_, bool A_MN_, bool B_MN_, int STAGES_, int OPT_ = 0>
+template <int BN_, int NA_, int NB_, int NT_, int TERMS_, bool A_MN_, bool B_MN_, int STAGES_, int OPT_ = 0,
+          int EPI_WARPS_ = 8>
 struct Umma2Cfg {
   static constexpr int BM = 256, BN = BN_, BK = 64;       // pair tile
   static constexpr int HB = BN / 2;                        // B rows per CTA
   static constexpr int NA = NA_, NB = NB_, NT = NT_, TERMS = TERMS_, STAGES = STAGES_, OPT = OPT_;
+  static constexpr int EPI_WARPS = EPI_WARPS_;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr bool A_MN = A_MN_, B_MN = B_MN_;
   static constexpr int A_TILE = 128 * BK * 2;
   static constexpr int B_TILE = HB * BK * 2;
@@ -27,6 +35,8 @@ struct Umma2Cfg {
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static constexpr uint32_t IDESC = idesc_bf16(256, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
   static_assert(BN == 128 || BN == 256, "BN");
+  static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps");
+  static_assert((BN / 32) % (EPI_WARPS / 4) == 0, "column groups");
   static_assert(SMEM <= 227 * 1024, "smem budget");
   static_assert(TMEM_COLS <= 512, "tmem budget");
 };
@@ -42,8 +52,12 @@ __device__ __forceinline__ void load_operand_tile_pair(const CUtensorMap* map, u
   }
 }
 
+__device__ __forceinline__ bool opt_skipped(const UmmaWork& w, int b) {
+  return w.opt_skip && w.opt_skip[static_cast<int64_t>(b) * w.opt_stride] != 0.0;
+}
+
 template <class Cfg, class Epi>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
     umma2_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                       const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
                       const UmmaWork work, const Epi epi) {
@@ -71,7 +85,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[a], 2 * Cfg::EPI_WARPS);  // every epilogue warp of both CTAs
     }
     fence_mbar_init();
   }
@@ -93,7 +107,7 @@ __global__ void __launch_bounds__(256, 1)
         umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
         const int arow = tm * Cfg::BM + static_cast<int>(rank) * 128;
         const int brow = tn * Cfg::BN + static_cast<int>(rank) * Cfg::HB;
-        const bool skip = Cfg::OPT != 0 && work.opt_skip && work.opt_skip[static_cast<int64_t>(b) * work.opt_stride] != 0.0;
+        const bool skip = Cfg::OPT != 0 && opt_skipped(work, b);
         const uint32_t bytes = 2 * (Cfg::STAGE_BYTES - (skip ? (Cfg::OPT == 1 ? Cfg::B_TILE : Cfg::A_TILE) : 0));
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -123,7 +137,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int idx = cluster; idx < work.num_work; idx += nclusters) {
         int b, split, tm, tn, kt0, kt1;
         umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
-        const bool skip = Cfg::OPT != 0 && work.opt_skip && work.opt_skip[static_cast<int64_t>(b) * work.opt_stride] != 0.0;
+        const bool skip = Cfg::OPT != 0 && opt_skipped(work, b);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * Cfg::BN);
@@ -161,6 +175,10 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
     const int ew = warp - 4;
+    const int q = warp & 3;                         // TMEM lane quarter this warp may access
+    constexpr int GROUPS = Cfg::EPI_WARPS / 4;      // column groups
+    constexpr int CPG = Cfg::BN / 32 / GROUPS;      // 32-column chunks per group
+    const int c0 = (ew / 4) * CPG;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int idx = cluster; idx < work.num_work; idx += nclusters) {
@@ -168,10 +186,10 @@ __global__ void __launch_bounds__(256, 1)
       umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = tm * Cfg::BM + static_cast<int>(rank) * 128 + ew * 32 + lane;
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * Cfg::BN);
+      const int row = tm * Cfg::BM + static_cast<int>(rank) * 128 + q * 32 + lane;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::BN);
 #pragma unroll 1
-      for (int c = 0; c < Cfg::BN / 32; ++c) {
+      for (int c = c0; c < c0 + CPG; ++c) {
         uint32_t r[32];
         tmem_ld32(taddr + c * 32, r);
         tmem_wait_ld();
@@ -225,7 +243,7 @@ inline cudaError_t launch_umma2(const CUtensorMap& a0, const CUtensorMap& a1, co
   const int nclusters = w.num_work < pairs ? w.num_work : pairs;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * nclusters));
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(Cfg::THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

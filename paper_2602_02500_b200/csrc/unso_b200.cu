@@ -240,49 +240,60 @@ struct UEpiOut {
   const __nv_bfloat16* x = nullptr;
   int64_t xld = 0, xbs = 0;
   const double* scal = nullptr;
-  __device__ void operator()(int b, int, int row, int col0, const float* vin) const {
+  // All indexing below is compile-time (fully unrolled, predicated tails): the 32-value chunk
+  // stays in registers (a dynamic index would spill it to local memory, ~18 GB of L1 traffic
+  // per cfg4 apply in round-1 ncu).
+  __device__ __forceinline__ void operator()(int b, int, int row, int col0, const float (&vin)[32]) const {
     if (row >= M) return;
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = vin[j];
+    const bool full = col0 + 32 <= N;
     if (x) {
       const float sh = static_cast<float>(scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_SHIFT]);
       if (sh != 0.0f) {
         const __nv_bfloat16* xr = x + static_cast<int64_t>(b) * xbs + static_cast<int64_t>(row) * xld + col0;
-        if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
+        if (full && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
-            __align__(16) __nv_bfloat16 t[8];
-            *reinterpret_cast<uint4*>(t) = *reinterpret_cast<const uint4*>(xr + j);
+            const uint4 t = *reinterpret_cast<const uint4*>(xr + j);
+            const uint32_t w[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[j + q] = fmaf(sh, __bfloat162float(t[q]), v[j + q]);
+            for (int q = 0; q < 4; ++q) {
+              v[j + 2 * q] = fmaf(sh, bf16_lo_to_f32(w[q]), v[j + 2 * q]);
+              v[j + 2 * q + 1] = fmaf(sh, bf16_hi_to_f32(w[q]), v[j + 2 * q + 1]);
+            }
           }
         } else {
-          for (int j = 0; j < 32 && col0 + j < N; ++j) v[j] = fmaf(sh, __bfloat162float(xr[j]), v[j]);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < N) v[j] = fmaf(sh, __bfloat162float(xr[j]), v[j]);
         }
       }
     }
     const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + col0;
     if (dt == DT_BF16) {
       __nv_bfloat16* y = static_cast<__nv_bfloat16*>(out) + o;
-      if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+      if (full && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          __align__(16) __nv_bfloat162 p[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) p[q] = __floats2bfloat162_rn(v[j + 2 * q], v[j + 2 * q + 1]);
-          *reinterpret_cast<uint4*>(y + j) = *reinterpret_cast<uint4*>(p);
-        }
+        for (int j = 0; j < 32; j += 8)
+          *reinterpret_cast<uint4*>(y + j) =
+              make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                         pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
       } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) y[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) y[j] = __float2bfloat16_rn(v[j]);
       }
     } else {
       float* y = static_cast<float*>(out) + o;
-      if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+      if (full && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(y + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) y[j] = v[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) y[j] = v[j];
       }
     }
   }
