@@ -55,6 +55,11 @@ __device__ __forceinline__ void load_operand_tile_pair(const CUtensorMap* map, u
 __device__ __forceinline__ bool opt_skipped(const UmmaWork& w, int b) {
   return w.opt_skip && w.opt_skip[static_cast<int64_t>(b) * w.opt_stride] != 0.0;
 }
+// Every role evaluates the same predicate on the same data, so all skip the same work items.
+__device__ __forceinline__ bool filtered_out(const UmmaWork& w, int b) {
+  if (!w.mode_flag || w.mode_want < 0) return false;
+  return (w.mode_flag[static_cast<int64_t>(b) * w.opt_stride] != 0.0) != (w.mode_want == 1);
+}
 
 template <class Cfg, class Epi>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
@@ -73,6 +78,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  if (work.mode_flag && work.mode_want >= 0) {
+    // Both CTAs of the pair see the same items: if none passes the filter, leave before any
+    // barrier / TMEM setup (the companion launch of the adaptive apply then costs ~a launch).
+    bool any = false;
+    for (int idx = cluster; idx < work.num_work && !any; idx += nclusters) {
+      int b, split, tm, tn, kt0, kt1;
+      umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
+      any = !filtered_out(work, b);
+    }
+    if (!any) return;
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA0);
@@ -105,6 +121,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       for (int idx = cluster; idx < work.num_work; idx += nclusters) {
         int b, split, tm, tn, kt0, kt1;
         umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
+        if (filtered_out(work, b)) continue;
         const int arow = tm * Cfg::BM + static_cast<int>(rank) * 128;
         const int brow = tn * Cfg::BN + static_cast<int>(rank) * Cfg::HB;
         const bool skip = Cfg::OPT != 0 && opt_skipped(work, b);
@@ -137,6 +154,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       for (int idx = cluster; idx < work.num_work; idx += nclusters) {
         int b, split, tm, tn, kt0, kt1;
         umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
+        if (filtered_out(work, b)) continue;
         const bool skip = Cfg::OPT != 0 && opt_skipped(work, b);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -184,6 +202,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     for (int idx = cluster; idx < work.num_work; idx += nclusters) {
       int b, split, tm, tn, kt0, kt1;
       umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
+      if (filtered_out(work, b)) continue;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = tm * Cfg::BM + static_cast<int>(rank) * 128 + q * 32 + lane;

@@ -27,6 +27,10 @@ struct UmmaWork {
   // opt_skip[b * opt_stride] != 0 (device-side decision written by an earlier kernel).
   const double* opt_skip = nullptr;
   int opt_stride = 0;
+  // Work filter (CTA-pair engine): when mode_flag is set, only matrices b with
+  // (mode_flag[b * opt_stride] != 0) == (mode_want == 1) are processed by this launch.
+  const double* mode_flag = nullptr;
+  int mode_want = -1;
 };
 
 __device__ __forceinline__ void umma_decode(const UmmaWork& w, int idx, int& b, int& split, int& tm, int& tn,

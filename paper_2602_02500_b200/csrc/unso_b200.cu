@@ -313,9 +313,9 @@ using CfgApplyWide1 = UmmaCfg<128, 1, 1, 1, TERM(0, 0, 0), false, true, 6>;
 // CTA-pair (cta_group::2) 256 x 256 tiles
 using Cfg2GramK = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, false, 6>;
 using Cfg2GramMN = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), true, true, 6>;
-using Cfg2ApplyTall2 = Umma2Cfg<256, 1, 2, 2, TERM(0, 0, 0) | TERM(1, 0, 1), false, false, 4, 1>;
+using Cfg2ApplyTall2 = Umma2Cfg<256, 1, 2, 2, TERM(0, 0, 0) | TERM(1, 0, 1), false, false, 4>;
 using Cfg2ApplyTall1 = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, false, 6>;
-using Cfg2ApplyWide2 = Umma2Cfg<256, 2, 1, 2, TERM(0, 0, 0) | TERM(1, 1, 0), false, true, 4, 2>;
+using Cfg2ApplyWide2 = Umma2Cfg<256, 2, 1, 2, TERM(0, 0, 0) | TERM(1, 1, 0), false, true, 4>;
 using Cfg2ApplyWide1 = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, true, 6>;
 
 // Engine selection: CTA pairs by default; UNSO_ENGINE=1cta forces the 1-CTA 128x128 engine (A/B tests).
@@ -675,40 +675,54 @@ static int32_t gram_bf16(const Problem& p, const Plan& pl, void* ws, const __nv_
 static int32_t apply_bf16(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
                           int64_t bsx, void* y, cudaStream_t st) {
   const int h = static_cast<int>(p.h);
-  const bool single = (p.flags & UNSO_FLAG_SINGLE_TERM_APPLY) != 0;
+  const bool force1 = (p.flags & UNSO_FLAG_SINGLE_TERM_APPLY) != 0;
+  const bool force2 = (p.flags & UNSO_FLAG_TWO_TERM_APPLY) != 0;
   CUtensorMap mx, mph, mpl;
   if (!umma_make_kmajor_map(&mph, at<__nv_bfloat16>(ws, pl.Phi), h, h, pl.ldc, p.batch, pl.hh, 128) ||
       !umma_make_kmajor_map(&mpl, at<__nv_bfloat16>(ws, pl.Plo), h, h, pl.ldc, p.batch, pl.hh, 128))
     return UNSO_ERR_CUDA;
   const int ydt = p.dt == UNSO_DTYPE_BF16 ? DT_BF16 : DT_F32;
-  cudaError_t e;
+  cudaError_t e = cudaSuccess;
   const bool pair = use_pair_engine();
+  const double* mode = at<double>(ws, pl.scal) + S_MODE;
+  // Adaptive (default): two launches, each processing only the matrices whose device-side
+  // decision matches it -- a 6-stage single-term kernel and a 4-stage bf16x2 kernel.
+  auto filt = [&](UmmaWork w, int want) {
+    if (!force1 && !force2) {
+      w.mode_flag = mode;
+      w.opt_stride = SCAL_STRIDE;
+      w.mode_want = want;
+    }
+    return w;
+  };
   if (p.tall) {
     if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx, 128)) return UNSO_ERR_CUDA;
     UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, static_cast<int>(p.rows), h, xb, ldx, bsx, at<double>(ws, pl.scal)};
     if (pair) {
-      UmmaWork wa = umma2_make_work(static_cast<int>(p.rows), h, h, 256, static_cast<int>(p.batch), false, 1);
-      wa.opt_skip = at<double>(ws, pl.scal) + S_MODE;
-      wa.opt_stride = SCAL_STRIDE;
-      e = single ? launch_umma2<Cfg2ApplyTall1>(mx, mx, mph, mph, wa, epi, st)
-                 : launch_umma2<Cfg2ApplyTall2>(mx, mx, mph, mpl, wa, epi, st);
+      const UmmaWork wa = umma2_make_work(static_cast<int>(p.rows), h, h, 256, static_cast<int>(p.batch), false, 1);
+      if (!force2) {
+        e = launch_umma2<Cfg2ApplyTall1>(mx, mx, mph, mph, filt(wa, 1), epi, st);
+        ++g_launches;
+      }
+      if (e == cudaSuccess && !force1) e = launch_umma2<Cfg2ApplyTall2>(mx, mx, mph, mpl, filt(wa, 0), epi, st);
     } else {
       const UmmaWork wa = umma_make_work(static_cast<int>(p.rows), h, h, 128, static_cast<int>(p.batch), false, 1);
-      e = single ? launch_umma<CfgApplyTall1>(mx, mx, mph, mph, wa, epi, st)
+      e = force1 ? launch_umma<CfgApplyTall1>(mx, mx, mph, mph, wa, epi, st)
                  : launch_umma<CfgApplyTall2>(mx, mx, mph, mpl, wa, epi, st);
     }
   } else {
     if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
     UEpiOut epi{y, ydt, p.cols, p.rows * p.cols, h, static_cast<int>(p.cols), xb, ldx, bsx, at<double>(ws, pl.scal)};
     if (pair) {
-      UmmaWork wa = umma2_make_work(h, static_cast<int>(p.cols), h, 256, static_cast<int>(p.batch), false, 1);
-      wa.opt_skip = at<double>(ws, pl.scal) + S_MODE;
-      wa.opt_stride = SCAL_STRIDE;
-      e = single ? launch_umma2<Cfg2ApplyWide1>(mph, mph, mx, mx, wa, epi, st)
-                 : launch_umma2<Cfg2ApplyWide2>(mph, mpl, mx, mx, wa, epi, st);
+      const UmmaWork wa = umma2_make_work(h, static_cast<int>(p.cols), h, 256, static_cast<int>(p.batch), false, 1);
+      if (!force2) {
+        e = launch_umma2<Cfg2ApplyWide1>(mph, mph, mx, mx, filt(wa, 1), epi, st);
+        ++g_launches;
+      }
+      if (e == cudaSuccess && !force1) e = launch_umma2<Cfg2ApplyWide2>(mph, mpl, mx, mx, filt(wa, 0), epi, st);
     } else {
       const UmmaWork wa = umma_make_work(h, static_cast<int>(p.cols), h, 128, static_cast<int>(p.batch), false, 1);
-      e = single ? launch_umma<CfgApplyWide1>(mph, mph, mx, mx, wa, epi, st)
+      e = force1 ? launch_umma<CfgApplyWide1>(mph, mph, mx, mx, wa, epi, st)
                  : launch_umma<CfgApplyWide2>(mph, mpl, mx, mx, wa, epi, st);
     }
   }
