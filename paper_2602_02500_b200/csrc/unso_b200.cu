@@ -26,6 +26,7 @@
 #include "umma_gemm.cuh"
 #include "chain_persistent.cuh"
 #include "umma2_gemm.cuh"
+#include "chain_pair.cuh"
 #include <cstdlib>
 
 #define UNSO_VERSION_STRING "unso_b200 0.1.0 (sm_100a: tcgen05/TMEM/TMA bf16 path + fp64 DFMA parity path)"
@@ -750,8 +751,27 @@ static int32_t scale_chain_bf16_multi(const Problem& p, const Plan& pl, void* ws
   }
   prof_mark(3, st);
   int cur = 0;
+  if (use_pair_engine()) {
+    const UmmaWork wc2 = umma2_make_work(h, h, h, 256, static_cast<int>(p.batch), true, 1);
+    for (int k = 1; k < N; ++k) {
+      SymMaps maps;
+      const void* hi = at<__nv_bfloat16>(ws, pl.Chi[cur]);
+      const void* lo = at<__nv_bfloat16>(ws, pl.Clo[cur]);
+      if (!umma_make_kmajor_map(&maps.hiK, hi, h, h, pl.ldc, p.batch, pl.hh, 128) ||
+          !umma_make_kmajor_map(&maps.loK, lo, h, h, pl.ldc, p.batch, pl.hh, 128) ||
+          !umma_make_mnmajor_map(&maps.hiMN, hi, h, h, pl.ldc, p.batch, pl.hh) ||
+          !umma_make_mnmajor_map(&maps.loMN, lo, h, h, pl.ldc, p.batch, pl.hh))
+        return UNSO_ERR_CUDA;
+      EpiChainSym epi{at<__nv_bfloat16>(ws, pl.Chi[cur]), at<__nv_bfloat16>(ws, pl.Clo[cur]),
+                      at<__nv_bfloat16>(ws, pl.Chi[cur ^ 1]), at<__nv_bfloat16>(ws, pl.Clo[cur ^ 1]),
+                      at<float>(ws, pl.P), pl.ldc, pl.hh, h, static_cast<float>(p.co[k]), k + 1 < N ? 1 : 0};
+      if (launch_chain_pair(maps, wc2, epi, st) != cudaSuccess) return UNSO_ERR_CUDA;
+      ++g_launches;
+      cur ^= 1;
+    }
+  }
   const UmmaWork wc = umma_make_work(h, h, h, 128, static_cast<int>(p.batch), true, 1);
-  for (int k = 1; k < N; ++k) {
+  for (int k = 1; k < N && !use_pair_engine(); ++k) {
     CUtensorMap mh, ml;
     if (!umma_make_kmajor_map(&mh, at<__nv_bfloat16>(ws, pl.Chi[cur]), h, h, pl.ldc, p.batch, pl.hh, 128) ||
         !umma_make_kmajor_map(&ml, at<__nv_bfloat16>(ws, pl.Clo[cur]), h, h, pl.ldc, p.batch, pl.hh, 128))
