@@ -27,6 +27,7 @@
 #include "chain_persistent.cuh"
 #include "umma2_gemm.cuh"
 #include "chain_pair.cuh"
+#include "ns_bf16.cuh"
 #include <cstdlib>
 
 #define UNSO_VERSION_STRING "unso_b200 0.1.0 (sm_100a: tcgen05/TMEM/TMA bf16 path + fp64 DFMA parity path)"
@@ -384,7 +385,6 @@ static int32_t make_problem(const unso_matrix_desc* x, const unso_method_desc* m
   }
   for (double v : p.co)
     if (!std::isfinite(v)) return UNSO_ERR_VALUE;
-  if (p.method != UNSO_METHOD_UNSO && p.prec == UNSO_PREC_BF16) return UNSO_ERR_UNSUPPORTED;
   return UNSO_OK;
 }
 
@@ -400,7 +400,8 @@ struct Plan {
   size_t Chi[2] = {0, 0}, Clo[2] = {0, 0}, Phi = 0, Plo = 0;  // BF16 (P reused as f32)
   size_t Gk[2] = {0, 0};                          // gelfand powers
   size_t normbuf = 0, pstat = 0, gbar = 0;        // persistent chain: per-tile norms / P stats, grid barrier
-  size_t Xs[2] = {0, 0};                          // NS state (f64)
+  size_t Xs[2] = {0, 0};                          // NS state (f64 in FP32 mode, f32 in BF16 mode)
+  size_t xb2 = 0;                                 // NS BF16: second bf16 operand buffer (ping-pong)
 };
 
 static size_t take(Plan& pl, size_t bytes) {
@@ -482,6 +483,22 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       pl.P = take(pl, static_cast<size_t>(B * pl.hh) * 8);
       pl.Pout = take(pl, static_cast<size_t>(B * pl.hh) * 8);
     }
+  } else if (bf) {
+    // NS in BF16: fp32 state ping-pong + bf16 operand copy (always), G hi/lo, operator B (P), B hi/lo
+    if (!pl.xcopy) {
+      pl.xcopy = true;
+      pl.ldx = round_up(p.cols, 8);
+      pl.xb = take(pl, static_cast<size_t>(B * p.rows * pl.ldx) * 2);
+    }
+    pl.xb2 = take(pl, static_cast<size_t>(B * p.rows * pl.ldx) * 2);
+    pl.Xs[0] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 4);
+    pl.Xs[1] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 4);
+    pl.Chi[0] = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+    pl.Clo[0] = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+    pl.P = take(pl, static_cast<size_t>(B * pl.hh) * 4);
+    pl.Phi = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+    pl.Plo = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+    pl.normbuf = take(pl, static_cast<size_t>(B) * SCAL_STRIDE * 8);  // unit scalars for finalize_p
   } else {
     pl.Xs[0] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 8);
     pl.Xs[1] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 8);
@@ -964,6 +981,111 @@ static int32_t ns_fp32(const Problem& p, const Plan& pl, void* ws, const void* x
   return UNSO_OK;
 }
 
+// ---------------------------------------------------------------- NS baselines (BF16 precision, tcgen05)
+using Cfg2NSTall = Umma2Cfg<256, 1, 2, 2, TERM(0, 0, 0) | TERM(1, 0, 1), false, false, 4>;
+using Cfg2NSWide = Umma2Cfg<256, 2, 1, 2, TERM(0, 0, 0) | TERM(1, 1, 0), false, true, 4>;
+
+static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x, void* y, int32_t* status,
+                       cudaStream_t st) {
+  const int64_t B = p.batch;
+  const int h = static_cast<int>(p.h);
+  const int64_t xsz = p.rows * p.cols;
+  __nv_bfloat16* xbs[2] = {at<__nv_bfloat16>(ws, pl.xb), at<__nv_bfloat16>(ws, pl.xb2)};
+  __nv_bfloat16* xb = xbs[0];
+  const int64_t ldx = pl.ldx, bsx = p.rows * pl.ldx;
+  double* scal = at<double>(ws, pl.scal);
+  double* unit = at<double>(ws, pl.normbuf);
+  fill_unit_scal_kernel<<<static_cast<unsigned>((B + 127) / 128), 128, 0, st>>>(unit, static_cast<int>(B));
+  UNSO_CHECK_LAUNCH();
+  // preprocess scale (ortho.py:140-168): plain = ||A||_F, gram = ||A A^T||_F^(1/2), none = 1
+  const double* xscale = scal;
+  if (p.scaling == UNSO_SCALING_NONE) {
+    xscale = nullptr;
+  } else if (p.scaling == UNSO_SCALING_PLAIN) {
+    dim3 grid(NORM_BLOCKS, static_cast<unsigned>(B));
+    sumsq_kernel<<<grid, 256, 0, st>>>(x, p.dt, p.rows, p.cols, p.ld, p.bs, at<double>(ws, pl.blk));
+    UNSO_CHECK_LAUNCH();
+    scalars_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, SM_PLAIN, p.gpow,
+                                                            scal, status);
+    UNSO_CHECK_LAUNCH();
+  } else {  // gram / gelfand: Gram of the unscaled bf16 input on the tensor cores
+    ns_init_state_kernel<<<grid_for(B * xsz), 256, 0, st>>>(x, p.dt, p.ld, p.bs, nullptr, at<float>(ws, pl.Xs[0]), xb,
+                                                           ldx, p.rows, p.cols, static_cast<int>(B));
+    UNSO_CHECK_LAUNCH();
+    UNSO_TRY(gram_bf16(p, pl, ws, xb, ldx, bsx, st));
+    UNSO_TRY(finalize_gram<float>(p, pl, ws, pl.splits, at<float>(ws, pl.G), st));
+    UNSO_TRY(norms_and_scalars<float>(p, pl, ws, at<float>(ws, pl.G), SM_GRAM, status, st));
+    if (p.scaling == UNSO_SCALING_GELFAND)
+      UNSO_TRY(gelfand_scale<float>(p, pl, ws, at<float>(ws, pl.G), DT_F32, status, st));
+  }
+  ns_init_state_kernel<<<grid_for(B * xsz), 256, 0, st>>>(x, p.dt, p.ld, p.bs, xscale, at<float>(ws, pl.Xs[0]), xb,
+                                                         ldx, p.rows, p.cols, static_cast<int>(B));
+  UNSO_CHECK_LAUNCH();
+  const int nt = (h + 31) / 32;
+  const dim3 pgrid(nt * (nt + 1) / 2, static_cast<unsigned>(B));
+  const dim3 egrid(grid_for(static_cast<int64_t>(h) * h, 256, 1024), static_cast<unsigned>(B));
+  int cur = 0;
+  for (int it = 0; it < p.steps; ++it) {
+    xb = xbs[cur];  // read this step's operand, write the next one into the other buffer
+    UNSO_TRY(gram_bf16(p, pl, ws, xb, ldx, bsx, st));
+    UNSO_TRY(finalize_gram<float>(p, pl, ws, pl.splits, at<float>(ws, pl.G), st));
+    const float* G = at<float>(ws, pl.G);
+    float a_c;
+    if (p.method == UNSO_METHOD_ORIGINAL_NS) {  // B = -0.5 G, X' = 1.5 X + X B
+      a_c = 1.5f;
+      split_scaled_kernel<<<egrid, 256, 0, st>>>(G, h, pl.ldc, -0.5f, at<__nv_bfloat16>(ws, pl.Phi),
+                                                 at<__nv_bfloat16>(ws, pl.Plo));
+      UNSO_CHECK_LAUNCH();
+    } else {  // B = b G + c G^2 (bf16x3 SYRK), X' = a X + X B
+      a_c = static_cast<float>(p.co[3 * it + 0]);
+      split_scaled_kernel<<<egrid, 256, 0, st>>>(G, h, pl.ldc, 1.0f, at<__nv_bfloat16>(ws, pl.Chi[0]),
+                                                 at<__nv_bfloat16>(ws, pl.Clo[0]));
+      UNSO_CHECK_LAUNCH();
+      SymMaps maps;
+      const void* hi = at<__nv_bfloat16>(ws, pl.Chi[0]);
+      const void* lo = at<__nv_bfloat16>(ws, pl.Clo[0]);
+      if (!umma_make_kmajor_map(&maps.hiK, hi, h, h, pl.ldc, B, pl.hh, 128) ||
+          !umma_make_kmajor_map(&maps.loK, lo, h, h, pl.ldc, B, pl.hh, 128) ||
+          !umma_make_mnmajor_map(&maps.hiMN, hi, h, h, pl.ldc, B, pl.hh) ||
+          !umma_make_mnmajor_map(&maps.loMN, lo, h, h, pl.ldc, B, pl.hh))
+        return UNSO_ERR_CUDA;
+      const UmmaWork wq = umma2_make_work(h, h, h, 256, static_cast<int>(B), true, 1);
+      EpiQuinticBF16 qe{G, at<float>(ws, pl.P), pl.ldc, pl.hh, h, static_cast<float>(p.co[3 * it + 1]),
+                        static_cast<float>(p.co[3 * it + 2])};
+      if (launch_chain_pair(maps, wq, qe, st) != cudaSuccess) return UNSO_ERR_CUDA;
+      ++g_launches;
+      finalize_p_kernel<1><<<pgrid, 256, 0, st>>>(at<float>(ws, pl.P), h, pl.ldc, unit, at<__nv_bfloat16>(ws, pl.Phi),
+                                                   at<__nv_bfloat16>(ws, pl.Plo));
+      UNSO_CHECK_LAUNCH();
+    }
+    CUtensorMap mx, mph, mpl;
+    if (!umma_make_kmajor_map(&mph, at<__nv_bfloat16>(ws, pl.Phi), h, h, pl.ldc, B, pl.hh, 128) ||
+        !umma_make_kmajor_map(&mpl, at<__nv_bfloat16>(ws, pl.Plo), h, h, pl.ldc, B, pl.hh, 128))
+      return UNSO_ERR_CUDA;
+    const float* xo = at<float>(ws, pl.Xs[cur]);
+    float* xn = at<float>(ws, pl.Xs[cur ^ 1]);
+    cudaError_t e;
+    if (p.tall) {
+      if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, B, bsx, 128)) return UNSO_ERR_CUDA;
+      EpiNSUpdate epi{xo, xn, xbs[cur ^ 1], ldx, p.rows, p.cols, static_cast<int>(p.rows), h, a_c};
+      const UmmaWork wa = umma2_make_work(static_cast<int>(p.rows), h, h, 256, static_cast<int>(B), false, 1);
+      e = launch_umma2<Cfg2NSTall>(mx, mx, mph, mpl, wa, epi, st);
+    } else {
+      if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, B, bsx)) return UNSO_ERR_CUDA;
+      EpiNSUpdate epi{xo, xn, xbs[cur ^ 1], ldx, p.rows, p.cols, h, static_cast<int>(p.cols), a_c};
+      const UmmaWork wa = umma2_make_work(h, static_cast<int>(p.cols), h, 256, static_cast<int>(B), false, 1);
+      e = launch_umma2<Cfg2NSWide>(mph, mpl, mx, mx, wa, epi, st);
+    }
+    if (e != cudaSuccess) return UNSO_ERR_CUDA;
+    ++g_launches;
+    cur ^= 1;
+  }
+  convert_kernel<<<grid_for(B * xsz), 256, 0, st>>>(at<float>(ws, pl.Xs[cur]), DT_F32, p.cols, xsz, y, p.dt, p.cols,
+                                                    xsz, p.rows, p.cols, static_cast<int>(B), nullptr);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
 static int32_t check_ws(const Plan& pl, void* ws, size_t bytes) {
   if (bytes < pl.total) return UNSO_ERR_WORKSPACE;
   if (pl.total > 0 && !ws) return UNSO_ERR_WORKSPACE;
@@ -1021,7 +1143,8 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
   if (p.method != UNSO_METHOD_UNSO) {
     const Plan pl = make_plan(p, true);
     UNSO_TRY(check_ws(pl, workspace, workspace_bytes));
-    return ns_fp32(p, pl, workspace, x_ptr, y_ptr, d_status, st);
+    return p.prec == UNSO_PREC_FP32 ? ns_fp32(p, pl, workspace, x_ptr, y_ptr, d_status, st)
+                                    : ns_bf16(p, pl, workspace, x_ptr, y_ptr, d_status, st);
   }
   const Plan pl = make_plan(p, true);
   UNSO_TRY(check_ws(pl, workspace, workspace_bytes));

@@ -327,3 +327,32 @@ def test_adaptive_apply_decision():
         assert r <= TOL["bf16"]
         if expect_single:
             assert r <= info["apply_bound"] + 2 * r2
+
+
+# ------------------------------------------------------------------ NS / Muon comparison path in bf16 mode
+@pytest.mark.parametrize("name", ["muon5", "muon3", "original4", "cesista", "external"])
+def test_ns_bf16_mode_small_cases(golden_arrays, golden_kats, name):
+    for key in ("in_64x256", "in_130x66", "in_16x40", "in_40x16"):
+        m = golden_arrays[key].astype(np.float32)
+        _, y = run(m, spec_for(name, golden_kats), torch.float32, "bf16")
+        ref = O.run(bf16_round(m), **oracle_kw(name, golden_kats))["y"]
+        r = rel(y, ref)
+        assert r <= TOL["bf16"], (name, key, r)
+
+
+def test_ns_bf16_cfg1_and_large():
+    g = O.gaussian_matrix(512, 128, 0).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.MUON_NS, iterations=5)
+    _, y = run(g, spec, torch.float32, "bf16")
+    r = rel(y, O.run(bf16_round(g), "muon", iterations=5)["y"])
+    print(f"cfg1 muon5 bf16: rel {r:.2e}")
+    assert r <= TOL["bf16"]
+    m = (O.gaussian_matrix(3000, 1024, 61) * 0.02).astype(np.float32)   # cfg3-like, ragged w
+    _, y = run(m, spec, torch.float32, "bf16")
+    r = rel(y, O.run(bf16_round(m), "muon", iterations=5)["y"])
+    print(f"3000x1024 muon5 bf16: rel {r:.2e}")
+    assert r <= TOL["bf16"]
+    ms = np.stack([O.gaussian_matrix(256, 768, 70 + i) for i in range(3)]).astype(np.float32)
+    yb = U.orthogonalize(torch.from_numpy(ms).to(DEV), spec, precision="bf16").y.double().cpu().numpy()
+    for i in range(3):
+        assert rel(yb[i], O.run(bf16_round(ms[i]), "muon", iterations=5)["y"]) <= TOL["bf16"]
