@@ -263,6 +263,7 @@ __global__ void finalize_p_kernel(const void* __restrict__ Pin, int h, int64_t l
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t off = static_cast<int64_t>(b) * h * ld;
   const double inv_s = scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_INV_S];
+  const double shift = scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_SHIFT];  // d/s (0 unless decided)
   for (int r = ty; r < 32; r += 8) {
     const int gr = ti * 32 + r, gc = tj * 32 + tx;
     double v = 0.0;
@@ -270,7 +271,7 @@ __global__ void finalize_p_kernel(const void* __restrict__ Pin, int h, int64_t l
       const int64_t o = off + static_cast<int64_t>(gr) * ld + gc;
       v = OUT == 0 ? static_cast<const double*>(Pin)[o] : static_cast<double>(static_cast<const float*>(Pin)[o]);
     }
-    tile[r][tx] = v * inv_s;
+    tile[r][tx] = v * inv_s - (gr == gc ? shift : 0.0);
   }
   __syncthreads();
   auto put = [&](int gr, int gc, double v) {

@@ -1,0 +1,240 @@
+// Glue-free multi-launch pipeline for large h (tiles > co-resident CTAs):
+//   K1 gram epilogue -> G as bf16 hi/lo (upper pair tiles) + per-warp norm partials
+//   scalars          -> s^2, 1/s, status               (fixed-order reduction, deterministic)
+//   K2 step 1        -> C_1 = G/s^2 folded into the epilogue, P initialised (no P read)
+//   K2 steps 2..N-1  -> C-form squarings, the last one emitting P statistics
+//   decision         -> identity shift d, adaptive apply bound (as in chain_persistent.cuh)
+//   finalize P       -> (P - d I)/s, bf16 hi/lo, symmetric
+// Norm/statistics partials are written per (matrix, pair tile, 32-row group, 32-column chunk)
+// by lane 0 after a warp reduction: no atomics, bitwise reproducible.
+#pragma once
+#include "common.cuh"
+#include "elementwise.cuh"
+
+namespace unso {
+
+__device__ __forceinline__ int upper_tile_index(int tm, int tn, int nt) {
+  return tm * nt - tm * (tm - 1) / 2 + (tn - tm);
+}
+
+// Slot of a (b, pair tile, row group, chunk) partial: row group = (row >> 5) & 7, chunk = (col0 >> 5) & 7.
+__device__ __forceinline__ int64_t partial_slot(int b, int row, int col0, int nt) {
+  const int tm = row >> 8, tn = col0 >> 8;
+  const int T = nt * (nt + 1) / 2;
+  return ((static_cast<int64_t>(b) * T + upper_tile_index(tm, tn, nt)) * 8 + ((row >> 5) & 7)) * 8 + ((col0 >> 5) & 7);
+}
+
+// Gram epilogue (CTA-pair engine, no split-K): G tile -> bf16 hi/lo + norm partials.
+struct UEpiGramSplit {
+  __nv_bfloat16* hi;
+  __nv_bfloat16* lo;
+  double* part;  // [slots][3]: trace, weighted ||.||^2, 0
+  int64_t ld, bs;
+  int h, nt;
+  __device__ __forceinline__ void operator()(int b, int, int row, int col0, const float (&v)[32]) const {
+    const bool rok = row < h;
+    const double w = ((row >> 8) == (col0 >> 8)) ? 1.0 : 2.0;  // off-diagonal pair tiles stand for both triangles
+    double tr = 0.0, fr = 0.0;
+    uint32_t hw[16], lw[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = col0 + 2 * j;
+      const bool ok0 = rok && c < h, ok1 = rok && c + 1 < h;
+      const float x0 = ok0 ? v[2 * j] : 0.f, x1 = ok1 ? v[2 * j + 1] : 0.f;
+      fr += w * (static_cast<double>(x0) * x0 + static_cast<double>(x1) * x1);
+      if (c == row) tr += x0;
+      if (c + 1 == row) tr += x1;
+      const uint32_t hh = pack_bf16x2(x0, x1);
+      hw[j] = hh;
+      lw[j] = pack_bf16x2(x0 - bf16_lo_to_f32(hh), x1 - bf16_hi_to_f32(hh));
+    }
+    tr = warp_sum(tr);
+    fr = warp_sum(fr);
+    if ((threadIdx.x & 31) == 0) {
+      double* o = part + partial_slot(b, row, col0, nt) * 3;
+      o[0] = tr;
+      o[1] = fr;
+      o[2] = 0.0;
+    }
+    if (!rok) return;
+    const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + col0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      *reinterpret_cast<uint4*>(hi + o + 8 * j) = make_uint4(hw[4 * j], hw[4 * j + 1], hw[4 * j + 2], hw[4 * j + 3]);
+      *reinterpret_cast<uint4*>(lo + o + 8 * j) = make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
+    }
+  }
+};
+
+// Split-K finalize for the multi-launch path: sum partials -> bf16 hi/lo (both triangles)
+// + one norm partial per 32x32 upper tile.
+__global__ void finalize_split_kernel(const float* __restrict__ part, int splits, int batch, int h, int64_t ld,
+                                      __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
+                                      double* __restrict__ norms) {
+  __shared__ float tile[32][33];
+  __shared__ double scratch[32];
+  const int nt = (h + 31) / 32;
+  int ti, tj;
+  sym_tile_coords(blockIdx.x, nt, ti, tj);
+  const int b = blockIdx.y;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t mat = static_cast<int64_t>(h) * ld;
+  double tr = 0.0, fr = 0.0;
+  for (int r = ty; r < 32; r += 8) {
+    const int gr = ti * 32 + r, gc = tj * 32 + tx;
+    float s = 0.f;
+    if (gr < h && gc < h) {
+      for (int sp = 0; sp < splits; ++sp)
+        s += part[(static_cast<int64_t>(sp) * batch + b) * mat + static_cast<int64_t>(gr) * ld + gc];
+      if (gr == gc) tr += s;
+      if (gr <= gc) fr += (gr == gc ? 1.0 : 2.0) * static_cast<double>(s) * s;
+    }
+    tile[r][tx] = s;
+  }
+  __syncthreads();
+  const int64_t off = static_cast<int64_t>(b) * mat;
+  for (int r = ty; r < 32; r += 8) {
+    const int gr = ti * 32 + r, gc = tj * 32 + tx;
+    if (gr < h && gc < h) split_bf16((ti == tj && r > tx) ? tile[tx][r] : tile[r][tx], hi[off + static_cast<int64_t>(gr) * ld + gc],
+                                     lo[off + static_cast<int64_t>(gr) * ld + gc]);
+    if (ti != tj) {
+      const int mr = tj * 32 + r, mc = ti * 32 + tx;
+      if (mr < h && mc < h) split_bf16(tile[tx][r], hi[off + static_cast<int64_t>(mr) * ld + mc], lo[off + static_cast<int64_t>(mr) * ld + mc]);
+    }
+  }
+  tr = block_sum(tr, scratch);
+  const double trs = tr;
+  fr = block_sum(fr, scratch);
+  if (threadIdx.x == 0) {
+    double* o = norms + (static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * 3;
+    o[0] = trs;
+    o[1] = fr;
+    o[2] = 0.0;
+  }
+}
+
+// Per matrix: reduce the final-P statistics (trace P, weighted ||P||^2) -> identity shift d,
+// adaptive apply bound and mode (same rule as chain_persistent.cuh).
+__global__ void apply_decision_kernel(const double* __restrict__ pstat, int nslots, double* __restrict__ scal, int h,
+                                      int adaptive, double tau) {
+  __shared__ double scratch[32];
+  const int b = blockIdx.x;
+  double t0 = 0.0, t1 = 0.0;
+  for (int i = threadIdx.x; i < nslots; i += blockDim.x) {
+    t0 += pstat[(static_cast<int64_t>(b) * nslots + i) * 2 + 0];
+    t1 += pstat[(static_cast<int64_t>(b) * nslots + i) * 2 + 1];
+  }
+  t0 = block_sum(t0, scratch);
+  const double tp = t0;
+  t1 = block_sum(t1, scratch);
+  if (threadIdx.x != 0) return;
+  double* o = scal + static_cast<int64_t>(b) * SCAL_STRIDE;
+  const double d = tp / h;
+  const double r2 = fmax(t1 - tp * tp / h, 0.0);
+  const double trc = fmax(o[S_TRACE] / o[S_S2], 0.0);
+  const double bound = ldexp(sqrt(r2), -9) / fmax(sqrt(trc), 1e-300);
+  o[S_SHIFT] = d * o[S_INV_S];
+  o[S_MODE] = (adaptive && bound <= tau) ? 1.0 : 0.0;
+  o[S_BOUND] = bound;
+}
+
+// One squaring step's epilogue on the CTA's rows of an upper pair tile (register resident).
+//   first: the stored C is the unscaled Gram G; C_1 = G/s^2 and P = alpha I - a_1 C_1 - a_2 C_2.
+//   pstat: on the last step, per-warp partials of trace(P) and weighted ||P||^2.
+struct EpiChainStep {
+  const __nv_bfloat16* chi;
+  const __nv_bfloat16* clo;
+  __nv_bfloat16* nhi;
+  __nv_bfloat16* nlo;
+  float* P;
+  int64_t ld, bs;
+  int h, nt;
+  float coef;          // multiplies C_{k+1}
+  int write_next;
+  int first;
+  float coef1;         // first step: multiplies C_1
+  double alpha;        // first step: 1 + sum a + b
+  const double* scal;  // first step: s^2
+  double* pstat;       // last step: statistics partials (nullable)
+  __device__ __forceinline__ void operator()(int b, int, int row, int col0, const float (&v)[32]) const {
+    const bool rok = row < h;
+    const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + col0;
+    float cs = 1.f, as = 1.f;
+    if (first) {
+      const double is2 = 1.0 / scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_S2];
+      cs = static_cast<float>(is2);
+      as = static_cast<float>(is2 * is2);
+    }
+    uint32_t hw[16], lw[16];
+    float pv[32];
+    if (rok) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint4 a = *reinterpret_cast<const uint4*>(chi + o + 8 * j);
+        const uint4 c = *reinterpret_cast<const uint4*>(clo + o + 8 * j);
+        hw[4 * j] = a.x; hw[4 * j + 1] = a.y; hw[4 * j + 2] = a.z; hw[4 * j + 3] = a.w;
+        lw[4 * j] = c.x; lw[4 * j + 1] = c.y; lw[4 * j + 2] = c.z; lw[4 * j + 3] = c.w;
+      }
+      if (!first) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 t = *reinterpret_cast<const float4*>(P + o + 4 * j);
+          pv[4 * j] = t.x; pv[4 * j + 1] = t.y; pv[4 * j + 2] = t.z; pv[4 * j + 3] = t.w;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) hw[j] = lw[j] = 0u;
+    }
+    uint32_t nh[16], nl[16];
+    double tr = 0.0, fr = 0.0;
+    const double w = ((row >> 8) == (col0 >> 8)) ? 1.0 : 2.0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float c0v = (bf16_lo_to_f32(hw[j]) + bf16_lo_to_f32(lw[j])) * cs;
+      const float c1v = (bf16_hi_to_f32(hw[j]) + bf16_hi_to_f32(lw[j])) * cs;
+      const float n0 = 2.0f * c0v - v[2 * j] * as;
+      const float n1 = 2.0f * c1v - v[2 * j + 1] * as;
+      if (first) {
+        const int c = col0 + 2 * j;
+        pv[2 * j] = static_cast<float>((c == row ? alpha : 0.0) - static_cast<double>(coef1) * c0v);
+        pv[2 * j + 1] = static_cast<float>((c + 1 == row ? alpha : 0.0) - static_cast<double>(coef1) * c1v);
+      }
+      pv[2 * j] -= coef * n0;
+      pv[2 * j + 1] -= coef * n1;
+      const uint32_t hh = pack_bf16x2(n0, n1);
+      nh[j] = hh;
+      nl[j] = pack_bf16x2(n0 - bf16_lo_to_f32(hh), n1 - bf16_hi_to_f32(hh));
+      if (pstat) {
+        const int c = col0 + 2 * j;
+        const bool ok0 = rok && c < h, ok1 = rok && c + 1 < h;
+        if (ok0) fr += w * static_cast<double>(pv[2 * j]) * pv[2 * j];
+        if (ok1) fr += w * static_cast<double>(pv[2 * j + 1]) * pv[2 * j + 1];
+        if (ok0 && c == row) tr += pv[2 * j];
+        if (ok1 && c + 1 == row) tr += pv[2 * j + 1];
+      }
+    }
+    if (pstat) {
+      tr = warp_sum(tr);
+      fr = warp_sum(fr);
+      if ((threadIdx.x & 31) == 0) {
+        double* s = pstat + partial_slot(b, row, col0, nt) * 2;
+        s[0] = tr;
+        s[1] = fr;
+      }
+    }
+    if (!rok) return;
+    if (write_next) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        *reinterpret_cast<uint4*>(nhi + o + 8 * j) = make_uint4(nh[4 * j], nh[4 * j + 1], nh[4 * j + 2], nh[4 * j + 3]);
+        *reinterpret_cast<uint4*>(nlo + o + 8 * j) = make_uint4(nl[4 * j], nl[4 * j + 1], nl[4 * j + 2], nl[4 * j + 3]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(P + o + 4 * j) = make_float4(pv[4 * j], pv[4 * j + 1], pv[4 * j + 2], pv[4 * j + 3]);
+  }
+};
+
+}  // namespace unso

@@ -28,6 +28,7 @@
 #include "umma2_gemm.cuh"
 #include "chain_pair.cuh"
 #include "ns_bf16.cuh"
+#include "multi_chain.cuh"
 #include <cstdlib>
 
 #define UNSO_VERSION_STRING "unso_b200 0.1.0 (sm_100a: tcgen05/TMEM/TMA bf16 path + fp64 DFMA parity path)"
@@ -402,6 +403,7 @@ struct Plan {
   size_t normbuf = 0, pstat = 0, gbar = 0;        // persistent chain: per-tile norms / P stats, grid barrier
   size_t Xs[2] = {0, 0};                          // NS state (f64 in FP32 mode, f32 in BF16 mode)
   size_t xb2 = 0;                                 // NS BF16: second bf16 operand buffer (ping-pong)
+  size_t mnorm = 0, mpstat = 0;                   // multi-launch pipeline: norm / final-P partials
 };
 
 static size_t take(Plan& pl, size_t bytes) {
@@ -413,6 +415,7 @@ static size_t take(Plan& pl, size_t bytes) {
 // Split-K factor: the smallest s whose (tiles x s) work items fill >= 90% of the last wave
 // of persistent CTAs (or CTA pairs), keeping >= 4 k-blocks per split.
 static int pick_splits(int64_t tiles, int64_t ktiles, int64_t slots) {
+  if (tiles >= 2 * slots) return 1;  // >= 2 waves: the tail is small, and no split-K reduction is needed
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= 32 && s <= ktiles / 4; ++s) {
@@ -476,6 +479,12 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       const int64_t nt = (p.h + 127) / 128;
       pl.normbuf = take(pl, static_cast<size_t>(nt * (nt + 1) / 2 * B) * 2 * 8);
       pl.pstat = take(pl, static_cast<size_t>(nt * (nt + 1) / 2 * B) * 2 * 8);
+      // multi-launch pipeline partials: per (pair tile, 32-row group, 32-col chunk), or per 32x32 tile
+      const int64_t nt2 = (p.h + 255) / 256, nt32 = (p.h + 31) / 32;
+      const int64_t slots = nt2 * (nt2 + 1) / 2 * 64;
+      const int64_t nrm = slots > nt32 * (nt32 + 1) / 2 ? slots : nt32 * (nt32 + 1) / 2;
+      pl.mnorm = take(pl, static_cast<size_t>(B * nrm) * 3 * 8);
+      pl.mpstat = take(pl, static_cast<size_t>(B * slots) * 2 * 8);
       pl.gbar = take(pl, 256);
     } else {
       pl.C[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
@@ -690,6 +699,82 @@ static int32_t gram_bf16(const Problem& p, const Plan& pl, void* ws, const __nv_
   return UNSO_OK;
 }
 
+// K1 writing G straight into the chain's bf16 hi/lo state + norm partials (CTA pairs, no split-K).
+static int32_t gram_bf16_split(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
+                               int64_t bsx, cudaStream_t st) {
+  CUtensorMap mx;
+  const int nt2 = static_cast<int>((p.h + 255) / 256);
+  UEpiGramSplit epi{at<__nv_bfloat16>(ws, pl.Chi[0]), at<__nv_bfloat16>(ws, pl.Clo[0]), at<double>(ws, pl.mnorm),
+                    pl.ldc, pl.hh, static_cast<int>(p.h), nt2};
+  const UmmaWork w2 = umma2_make_work(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 256,
+                                      static_cast<int>(p.batch), true, 1);
+  cudaError_t e;
+  if (p.tall) {
+    if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
+    e = launch_umma2<Cfg2GramMN>(mx, mx, mx, mx, w2, epi, st);
+  } else {
+    if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx, 128)) return UNSO_ERR_CUDA;
+    e = launch_umma2<Cfg2GramK>(mx, mx, mx, mx, w2, epi, st);
+  }
+  if (e != cudaSuccess) return UNSO_ERR_CUDA;
+  ++g_launches;
+  return UNSO_OK;
+}
+
+// Multi-launch pipeline for large h (multi_chain.cuh): scalars from the norm partials, N-1 CTA-pair
+// squaring steps (the first folds C_1 = G/s^2 and initialises P, the last emits P statistics),
+// the adaptive-apply decision and the shifted symmetric P.  Requires C hi/lo[0] = split(G) and
+// the partials in pl.mnorm (nnorm per matrix).
+static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void* ws, int nnorm, int32_t* status,
+                                          cudaStream_t st) {
+  const int h = static_cast<int>(p.h);
+  const int N = p.order;
+  const int nt2 = (h + 255) / 256;
+  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(ws, pl.mnorm), nnorm,
+                                                                  scal_mode(p.scaling), p.gpow,
+                                                                  at<double>(ws, pl.scal), status);
+  UNSO_CHECK_LAUNCH();
+  prof_mark(3, st);
+  double alpha = 1.0;
+  for (double v : p.co) alpha += v;
+  const UmmaWork wc2 = umma2_make_work(h, h, h, 256, static_cast<int>(p.batch), true, 1);
+  int cur = 0;
+  for (int k = 1; k < N; ++k) {
+    SymMaps maps;
+    const void* hi = at<__nv_bfloat16>(ws, pl.Chi[cur]);
+    const void* lo = at<__nv_bfloat16>(ws, pl.Clo[cur]);
+    if (!umma_make_kmajor_map(&maps.hiK, hi, h, h, pl.ldc, p.batch, pl.hh, 128) ||
+        !umma_make_kmajor_map(&maps.loK, lo, h, h, pl.ldc, p.batch, pl.hh, 128) ||
+        !umma_make_mnmajor_map(&maps.hiMN, hi, h, h, pl.ldc, p.batch, pl.hh) ||
+        !umma_make_mnmajor_map(&maps.loMN, lo, h, h, pl.ldc, p.batch, pl.hh))
+      return UNSO_ERR_CUDA;
+    const bool last = k + 1 == N;
+    EpiChainStep epi{at<__nv_bfloat16>(ws, pl.Chi[cur]), at<__nv_bfloat16>(ws, pl.Clo[cur]),
+                     at<__nv_bfloat16>(ws, pl.Chi[cur ^ 1]), at<__nv_bfloat16>(ws, pl.Clo[cur ^ 1]),
+                     at<float>(ws, pl.P), pl.ldc, pl.hh, h, nt2, static_cast<float>(p.co[k]), last ? 0 : 1,
+                     k == 1 ? 1 : 0, static_cast<float>(p.co[0]), alpha, at<double>(ws, pl.scal),
+                     last ? at<double>(ws, pl.mpstat) : nullptr};
+    if (launch_chain_pair(maps, wc2, epi, st) != cudaSuccess) return UNSO_ERR_CUDA;
+    ++g_launches;
+    cur ^= 1;
+  }
+  prof_mark(4, st);
+  const int adaptive = ((p.flags & UNSO_FLAG_TWO_TERM_APPLY) == 0 && p.scaling != UNSO_SCALING_NONE) ? 1 : 0;
+  apply_decision_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(ws, pl.mpstat),
+                                                                         nt2 * (nt2 + 1) / 2 * 64,
+                                                                         at<double>(ws, pl.scal), h, adaptive, 5e-3);
+  UNSO_CHECK_LAUNCH();
+  {
+    const int nt = (h + 31) / 32;
+    dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
+    finalize_p_kernel<1><<<grid, 256, 0, st>>>(at<float>(ws, pl.P), h, pl.ldc, at<double>(ws, pl.scal),
+                                               at<__nv_bfloat16>(ws, pl.Phi), at<__nv_bfloat16>(ws, pl.Plo));
+    UNSO_CHECK_LAUNCH();
+  }
+  prof_mark(5, st);
+  return UNSO_OK;
+}
+
 static int32_t apply_bf16(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
                           int64_t bsx, void* y, cudaStream_t st) {
   const int h = static_cast<int>(p.h);
@@ -892,12 +977,38 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
   return UNSO_OK;
 }
 
-// Everything after the Gram partials: scale, chain, P, apply.
+// Which scale+chain implementation a BF16 UNSO problem takes.
+enum Bf16Route { ROUTE_PERSISTENT, ROUTE_GLUE_FREE, ROUTE_LEGACY };
+static Bf16Route bf16_route(const Problem& p) {
+  if (chain_persistent_fits(p)) return ROUTE_PERSISTENT;
+  if (use_pair_engine() && p.order >= 2 && p.scaling != UNSO_SCALING_GELFAND) return ROUTE_GLUE_FREE;
+  return ROUTE_LEGACY;
+}
+
+// Everything after the Gram: scale, chain, P, apply.  `split_done`: K1 already wrote G as
+// bf16 hi/lo + norm partials (glue-free route with one split); otherwise `part` holds split-K
+// fp32 partials (or the reduced Gram with splits == 1).
 static int32_t unso_bf16_after_gram(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
-                                    int64_t bsx, const float* part, int splits, void* y, int32_t* status,
-                                    cudaStream_t st) {
-  if (chain_persistent_fits(p)) {
+                                    int64_t bsx, const float* part, int splits, bool split_done, void* y,
+                                    int32_t* status, cudaStream_t st) {
+  const Bf16Route route = bf16_route(p);
+  if (route == ROUTE_PERSISTENT) {
     UNSO_TRY(scale_chain_bf16_persistent(p, pl, ws, part, splits, status, st));
+  } else if (route == ROUTE_GLUE_FREE) {
+    int nnorm;
+    if (split_done) {
+      const int64_t nt2 = (p.h + 255) / 256;
+      nnorm = static_cast<int>(nt2 * (nt2 + 1) / 2 * 64);
+    } else {
+      const int nt = static_cast<int>((p.h + 31) / 32);
+      nnorm = nt * (nt + 1) / 2;
+      dim3 grid(nnorm, static_cast<unsigned>(p.batch));
+      finalize_split_kernel<<<grid, 256, 0, st>>>(part, splits, static_cast<int>(p.batch), static_cast<int>(p.h), pl.ldc,
+                                                  at<__nv_bfloat16>(ws, pl.Chi[0]), at<__nv_bfloat16>(ws, pl.Clo[0]),
+                                                  at<double>(ws, pl.mnorm));
+      UNSO_CHECK_LAUNCH();
+    }
+    UNSO_TRY(scale_chain_bf16_glue_free(p, pl, ws, nnorm, status, st));
   } else {
     float* G = at<float>(ws, pl.G);
     if (part != G || splits != 1) {
@@ -1168,10 +1279,14 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
   int64_t ldx, bsx;
   UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
   prof_mark(1, st);
-  UNSO_TRY(gram_bf16(p, pl, workspace, xb, ldx, bsx, st));
+  const bool split_out = bf16_route(p) == ROUTE_GLUE_FREE && pl.splits == 1;
+  if (split_out)
+    UNSO_TRY(gram_bf16_split(p, pl, workspace, xb, ldx, bsx, st));
+  else
+    UNSO_TRY(gram_bf16(p, pl, workspace, xb, ldx, bsx, st));
   prof_mark(2, st);
-  return unso_bf16_after_gram(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.part), pl.splits, y_ptr,
-                              d_status, st);
+  return unso_bf16_after_gram(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.part), pl.splits, split_out,
+                              y_ptr, d_status, st);
 }
 
 int32_t unso_query_scalars(const unso_matrix_desc* x, const unso_method_desc* method, const void* workspace,
@@ -1280,7 +1395,8 @@ int32_t unso_orthogonalize_from_gram(const unso_matrix_desc* x, const void* x_pt
   const __nv_bfloat16* xb;
   int64_t ldx, bsx;
   UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
-  return unso_bf16_after_gram(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.G), 1, y_ptr, d_status, st);
+  return unso_bf16_after_gram(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.G), 1, false, y_ptr, d_status,
+                              st);
 }
 
 int32_t unso_scale_denominator(const unso_matrix_desc* x, const void* x_ptr, const unso_method_desc* method,

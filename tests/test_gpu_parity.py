@@ -356,3 +356,16 @@ def test_ns_bf16_cfg1_and_large():
     yb = U.orthogonalize(torch.from_numpy(ms).to(DEV), spec, precision="bf16").y.double().cpu().numpy()
     for i in range(3):
         assert rel(yb[i], O.run(bf16_round(ms[i]), "muon", iterations=5)["y"]) <= TOL["bf16"]
+
+
+def test_bf16_glue_free_route_ragged_batch():
+    """Batch whose tiles exceed co-residency and fill >= 2 waves: K1 writes G as bf16 hi/lo +
+    norm partials directly (no split-K), the first squaring folds C_1 = G/s^2, the last emits
+    P statistics; ragged h (640) and w (900)."""
+    ms = np.stack([O.gaussian_matrix(900, 640, 80 + i) for i in range(48)]).astype(np.float32)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    res = U.orthogonalize(torch.from_numpy(ms).to(DEV), spec, precision="bf16")
+    y = res.y.double().cpu().numpy()
+    worst = max(rel(y[i], O.run(bf16_round(ms[i]), "unso")["y"]) for i in range(0, 48, 6))
+    print(f"glue-free ragged batch: worst rel {worst:.2e}; apply_single={res.info[0]['apply_single']}")
+    assert worst <= TOL["bf16"]
