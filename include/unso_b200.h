@@ -60,6 +60,8 @@ typedef enum unso_method { UNSO_METHOD_UNSO = 0, UNSO_METHOD_ORIGINAL_NS = 1, UN
 
 /* flags */
 #define UNSO_FLAG_SINGLE_TERM_APPLY 0x1 /* BF16: always apply with one bf16 term of P (faster, less accurate) */
+#define UNSO_FLAG_CHAIN_BF16X3 0x4       /* BF16, large h: keep all squarings in bf16x3 (hi*hi + hi*lo + lo*hi)
+                                           instead of the default hi*hi (bf16) + e4m3 cross terms */
 #define UNSO_FLAG_TWO_TERM_APPLY 0x2    /* BF16: always apply with the bf16x2 (hi + lo) split of P.
                                            Default (neither flag): per matrix, the lo term is dropped on the
                                            device when ||X dR||_F / ||Y||_F <= 2^-9 ||R||_F / sqrt(tr C_1) <= 5e-3

@@ -156,6 +156,12 @@ struct EpiChainStep {
   double alpha;        // first step: 1 + sum a + b
   const double* scal;  // first step: s^2
   double* pstat;       // last step: statistics partials (nullable)
+  uint8_t* n8hi = nullptr;  // optional e4m3 operand copies of C_{k+1}: 2^8 hi, 2^16 (C - hi)
+  uint8_t* n8lo = nullptr;
+  float in_hi_scale = 1.f;   // stored hi of C_k is (2^12 hi) when produced for the fp8 kernel
+  float out_hi_scale = 1.f;  // scale of the stored hi of C_{k+1} (2^12 when n8hi is set)
+  uint8_t* n8i = nullptr;    // interleaved [hi8 | lo8] per 64-column block (row stride ld8i bytes)
+  int64_t ld8i = 0;
   __device__ __forceinline__ void operator()(int b, int, int row, int col0, const float (&v)[32]) const {
     const bool rok = row < h;
     const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + col0;
@@ -186,13 +192,13 @@ struct EpiChainStep {
 #pragma unroll
       for (int j = 0; j < 16; ++j) hw[j] = lw[j] = 0u;
     }
-    uint32_t nh[16], nl[16];
+    uint32_t nh[16], nl[16], q8h[16], q8l[16];
     double tr = 0.0, fr = 0.0;
     const double w = ((row >> 8) == (col0 >> 8)) ? 1.0 : 2.0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float c0v = (bf16_lo_to_f32(hw[j]) + bf16_lo_to_f32(lw[j])) * cs;
-      const float c1v = (bf16_hi_to_f32(hw[j]) + bf16_hi_to_f32(lw[j])) * cs;
+      const float c0v = fmaf(bf16_lo_to_f32(hw[j]), in_hi_scale, bf16_lo_to_f32(lw[j])) * cs;
+      const float c1v = fmaf(bf16_hi_to_f32(hw[j]), in_hi_scale, bf16_hi_to_f32(lw[j])) * cs;
       const float n0 = 2.0f * c0v - v[2 * j] * as;
       const float n1 = 2.0f * c1v - v[2 * j + 1] * as;
       if (first) {
@@ -203,8 +209,13 @@ struct EpiChainStep {
       pv[2 * j] -= coef * n0;
       pv[2 * j + 1] -= coef * n1;
       const uint32_t hh = pack_bf16x2(n0, n1);
-      nh[j] = hh;
-      nl[j] = pack_bf16x2(n0 - bf16_lo_to_f32(hh), n1 - bf16_hi_to_f32(hh));
+      const float h0 = bf16_lo_to_f32(hh), h1 = bf16_hi_to_f32(hh);
+      nh[j] = out_hi_scale == 1.f ? hh : pack_bf16x2(h0 * out_hi_scale, h1 * out_hi_scale);  // exact rescale
+      nl[j] = pack_bf16x2(n0 - h0, n1 - h1);
+      if (n8hi) {
+        q8h[j] = pack_e4m3x2(h0 * 256.0f, h1 * 256.0f);
+        q8l[j] = pack_e4m3x2((n0 - h0) * 65536.0f, (n1 - h1) * 65536.0f);
+      }
       if (pstat) {
         const int c = col0 + 2 * j;
         const bool ok0 = rok && c < h, ok1 = rok && c + 1 < h;
@@ -229,6 +240,29 @@ struct EpiChainStep {
       for (int j = 0; j < 4; ++j) {
         *reinterpret_cast<uint4*>(nhi + o + 8 * j) = make_uint4(nh[4 * j], nh[4 * j + 1], nh[4 * j + 2], nh[4 * j + 3]);
         *reinterpret_cast<uint4*>(nlo + o + 8 * j) = make_uint4(nl[4 * j], nl[4 * j + 1], nl[4 * j + 2], nl[4 * j + 3]);
+      }
+      if (n8hi) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          *reinterpret_cast<uint4*>(n8hi + o + 16 * j) =
+              make_uint4(q8h[8 * j] | (q8h[8 * j + 1] << 16), q8h[8 * j + 2] | (q8h[8 * j + 3] << 16),
+                         q8h[8 * j + 4] | (q8h[8 * j + 5] << 16), q8h[8 * j + 6] | (q8h[8 * j + 7] << 16));
+          *reinterpret_cast<uint4*>(n8lo + o + 16 * j) =
+              make_uint4(q8l[8 * j] | (q8l[8 * j + 1] << 16), q8l[8 * j + 2] | (q8l[8 * j + 3] << 16),
+                         q8l[8 * j + 4] | (q8l[8 * j + 5] << 16), q8l[8 * j + 6] | (q8l[8 * j + 7] << 16));
+        }
+        // interleaved copy: row r, 64-column block k: [hi8 (64 B) | lo8 (64 B)]
+        uint8_t* ri = n8i + static_cast<int64_t>(b) * (bs / ld) * ld8i + static_cast<int64_t>(row) * ld8i +
+                      (col0 >> 6) * 128 + (col0 & 63);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          *reinterpret_cast<uint4*>(ri + 16 * j) =
+              make_uint4(q8h[8 * j] | (q8h[8 * j + 1] << 16), q8h[8 * j + 2] | (q8h[8 * j + 3] << 16),
+                         q8h[8 * j + 4] | (q8h[8 * j + 5] << 16), q8h[8 * j + 6] | (q8h[8 * j + 7] << 16));
+          *reinterpret_cast<uint4*>(ri + 64 + 16 * j) =
+              make_uint4(q8l[8 * j] | (q8l[8 * j + 1] << 16), q8l[8 * j + 2] | (q8l[8 * j + 3] << 16),
+                         q8l[8 * j + 4] | (q8l[8 * j + 5] << 16), q8l[8 * j + 6] | (q8l[8 * j + 7] << 16));
+        }
       }
     }
 #pragma unroll

@@ -93,6 +93,20 @@ static bool make_map(CUtensorMap* m, const void* base, cuuint64_t d0, cuuint64_t
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// e4m3 operand maps (byte elements, SWIZZLE_128B, 128-byte TMA rows).
+static bool make_map_u8(CUtensorMap* m, const void* base, int64_t d0, int64_t d1, int64_t d2, int64_t ld, int64_t bs,
+                        cuuint32_t b0, cuuint32_t b1) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d0), static_cast<cuuint64_t>(d1), static_cast<cuuint64_t>(d2)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(d2 <= 1 ? d1 * ld : bs)};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool umma_make_kmajor_map(CUtensorMap* m, const void* base, int64_t rows, int64_t k, int64_t ld, int64_t batch,
                           int64_t bstride, int box_rows) {
   if (batch <= 1) bstride = rows * ld;
@@ -404,6 +418,8 @@ struct Plan {
   size_t Xs[2] = {0, 0};                          // NS state (f64 in FP32 mode, f32 in BF16 mode)
   size_t xb2 = 0;                                 // NS BF16: second bf16 operand buffer (ping-pong)
   size_t mnorm = 0, mpstat = 0;                   // multi-launch pipeline: norm / final-P partials
+  size_t C8h[2] = {0, 0}, C8l[2] = {0, 0};        // e4m3 operand planes of C_k (2^8 hi, 2^16 lo)
+  size_t C8i[2] = {0, 0};                         // e4m3 interleaved [hi8 | lo8] per 64-column block
 };
 
 static size_t take(Plan& pl, size_t bytes) {
@@ -485,6 +501,11 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       const int64_t nrm = slots > nt32 * (nt32 + 1) / 2 ? slots : nt32 * (nt32 + 1) / 2;
       pl.mnorm = take(pl, static_cast<size_t>(B * nrm) * 3 * 8);
       pl.mpstat = take(pl, static_cast<size_t>(B * slots) * 2 * 8);
+      for (int i = 0; i < 2; ++i) {
+        pl.C8h[i] = take(pl, static_cast<size_t>(B * pl.hh));
+        pl.C8l[i] = take(pl, static_cast<size_t>(B * pl.hh));
+        pl.C8i[i] = take(pl, static_cast<size_t>(B * pl.hh) * 2);
+      }
       pl.gbar = take(pl, 256);
     } else {
       pl.C[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
@@ -738,6 +759,7 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
   double alpha = 1.0;
   for (double v : p.co) alpha += v;
   const UmmaWork wc2 = umma2_make_work(h, h, h, 256, static_cast<int>(p.batch), true, 1);
+  const bool f8 = (p.flags & UNSO_FLAG_CHAIN_BF16X3) == 0;
   int cur = 0;
   for (int k = 1; k < N; ++k) {
     SymMaps maps;
@@ -754,7 +776,31 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
                      at<float>(ws, pl.P), pl.ldc, pl.hh, h, nt2, static_cast<float>(p.co[k]), last ? 0 : 1,
                      k == 1 ? 1 : 0, static_cast<float>(p.co[0]), alpha, at<double>(ws, pl.scal),
                      last ? at<double>(ws, pl.mpstat) : nullptr};
-    if (launch_chain_pair(maps, wc2, epi, st) != cudaSuccess) return UNSO_ERR_CUDA;
+    if (f8 && !last) {  // produce the e4m3 operand copies (and the 2^12-scaled bf16 hi) of C_{k+1}
+      epi.n8hi = at<uint8_t>(ws, pl.C8h[cur ^ 1]);
+      epi.n8lo = at<uint8_t>(ws, pl.C8l[cur ^ 1]);
+      epi.out_hi_scale = 4096.f;
+      epi.n8i = at<uint8_t>(ws, pl.C8i[cur ^ 1]);
+      epi.ld8i = 2 * pl.ldc;
+    }
+    if (f8 && k > 1) epi.in_hi_scale = 1.f / 4096.f;
+    cudaError_t le;
+    if (f8 && k > 1) {  // C_k is scaled (|C| <= 1): hi*hi in bf16 + e4m3 cross terms
+      SymMapsF8 m8;
+      m8.hiK = maps.hiK;
+      m8.hiMN = maps.hiMN;
+      const void* h8 = at<uint8_t>(ws, pl.C8h[cur]);
+      const void* l8 = at<uint8_t>(ws, pl.C8l[cur]);
+      const void* i8 = at<uint8_t>(ws, pl.C8i[cur]);
+      if (!make_map_u8(&m8.f8K, i8, 2 * pl.ldc, h, p.batch, 2 * pl.ldc, 2 * pl.hh, 128, 128) ||
+          !make_map_u8(&m8.h8MN, h8, h, h, p.batch, pl.ldc, pl.hh, 128, 64) ||
+          !make_map_u8(&m8.l8MN, l8, h, h, p.batch, pl.ldc, pl.hh, 128, 64))
+        return UNSO_ERR_CUDA;
+      le = launch_chain_pair_f8(m8, wc2, epi, st);
+    } else {
+      le = launch_chain_pair(maps, wc2, epi, st);
+    }
+    if (le != cudaSuccess) return UNSO_ERR_CUDA;
     ++g_launches;
     cur ^= 1;
   }

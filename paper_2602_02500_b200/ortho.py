@@ -75,6 +75,7 @@ class MethodSpec:
     gelfand_power: int = 2
     precision: Precision | None = None
     apply_terms: int | None = None   # bf16 mode: None = adaptive per matrix, 1 = P_hi only, 2 = P_hi + P_lo
+    chain: str | None = None         # bf16 mode, large h: None = bf16 hi*hi + e4m3 cross terms, "bf16x3"
 
     def __post_init__(self):
         kind = MethodKind(self.kind)
@@ -87,6 +88,8 @@ class MethodSpec:
             raise ValueError("gelfand_power must be >= 1")
         if self.apply_terms not in (None, 1, 2):
             raise ValueError("apply_terms must be None (adaptive), 1 or 2")
+        if self.chain not in (None, "bf16x3"):
+            raise ValueError("chain must be None (bf16 + e4m3 cross terms) or 'bf16x3'")
         if kind is MethodKind.UNSO:
             if self.coeffs is None:
                 raise ValueError("unso requires a CoefficientSet")
@@ -304,6 +307,8 @@ def _method_desc(spec: MethodSpec, precision: Precision, scaling_code: int):
         method, order, steps = N.METHOD_QUINTIC, 0, rows.shape[0]
     co = np.ascontiguousarray(co, dtype=np.float64)
     flags = {None: 0, 1: N.FLAG_SINGLE_TERM_APPLY, 2: N.FLAG_TWO_TERM_APPLY}[spec.apply_terms]
+    if spec.chain == "bf16x3":
+        flags |= N.FLAG_CHAIN_BF16X3
     md = N.MethodDesc(method, scaling_code, spec.gelfand_power,
                       N.PREC_BF16 if precision is Precision.BF16 else N.PREC_FP32, order, steps,
                       co.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), flags, 0)

@@ -369,3 +369,29 @@ def test_bf16_glue_free_route_ragged_batch():
     worst = max(rel(y[i], O.run(bf16_round(ms[i]), "unso")["y"]) for i in range(0, 48, 6))
     print(f"glue-free ragged batch: worst rel {worst:.2e}; apply_single={res.info[0]['apply_single']}")
     assert worst <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("kind", ["cfg3-square", "cfg3-tall", "cfg2-spectrum", "cfg5-pareto"])
+def test_chain_fp8_cross_terms_vs_bf16x3(kind):
+    """Large-h chain recipes (glue-free route, h = 2304 > co-residency): default hi*hi (bf16) +
+    e4m3 cross terms vs the bf16x3 chain, both against the oracle on the same rounded input."""
+    rng = np.random.default_rng(90)
+    if kind == "cfg3-square":
+        m = O.gaussian_matrix(2304, 2304, 91) * 0.02
+    elif kind == "cfg3-tall":
+        m = O.gaussian_matrix(8064, 2304, 92) * 0.02
+    elif kind == "cfg2-spectrum":
+        m = O.controlled_spectrum_matrix(4608, 2304, np.exp(rng.uniform(np.log(1e-4), 0, 2304)), 93)
+    else:
+        s = 1 + rng.pareto(1.5, 2304)
+        m = O.controlled_spectrum_matrix(4608, 2304, 1e-6 + (s - s.min()) / (s.max() - s.min()) * (1 - 1e-6), 94)
+    m = m.astype(np.float32)
+    ref = O.run(bf16_round(m), "unso")["y"]
+    out = {}
+    for chain in (None, "bf16x3"):
+        spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), chain=chain)
+        _, y = run(m, spec, torch.float32, "bf16")
+        out[chain or "bf16+e4m3"] = rel(y, ref)
+    print(f"chain recipes {kind}: {out}")
+    assert all(v <= TOL["bf16"] for v in out.values())
+    assert out["bf16+e4m3"] <= 1e-2
