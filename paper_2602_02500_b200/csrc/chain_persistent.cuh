@@ -32,7 +32,8 @@ struct ChainMaps {
 struct ChainParams {
   const float* part;   // split-K Gram partials: part[(s * batch + b) * mat + r * ld + c]
   int splits;
-  int h, nt, tiles_per_mat, batch;
+  int h, nt, tiles_per_mat, batch;  // batch = TOTAL batch (split-K partial layout)
+  int b0;                            // first matrix of this launch's chunk
   int64_t ld, mat;     // padded leading dim / per-matrix elements of every h x h buffer
   __nv_bfloat16* chi[2];
   __nv_bfloat16* clo[2];
@@ -94,7 +95,8 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = gridDim.x;
-  const int b = blockIdx.x / p.tiles_per_mat;
+  const int lb = blockIdx.x / p.tiles_per_mat;  // matrix within this chunk
+  const int b = p.b0 + lb;
   const int t = blockIdx.x % p.tiles_per_mat;
   int ti, tj;
   simt_tile_coords(t, p.nt, p.nt, 1, ti, tj);
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       grid_arrive(p.gbar);  // round 0
       grid_wait(p.gbar, static_cast<unsigned>(T));
       double s0 = 0.0, s1 = 0.0;
-      const int first = b * p.tiles_per_mat;
+      const int first = lb * p.tiles_per_mat;
       for (int q = 0; q < p.tiles_per_mat; ++q) {  // fixed order -> deterministic
         s0 += __ldcg(&p.normbuf[(first + q) * 2 + 0]);
         s1 += __ldcg(&p.normbuf[(first + q) * 2 + 1]);
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         grid_arrive(p.gbar);
         grid_wait(p.gbar, (round + 1) * static_cast<unsigned>(T));
         double tp = 0.0, s2p = 0.0;
-        const int first = b * p.tiles_per_mat;
+        const int first = lb * p.tiles_per_mat;
         for (int q = 0; q < p.tiles_per_mat; ++q) {
           tp += __ldcg(&p.pstat[(first + q) * 2 + 0]);
           s2p += __ldcg(&p.pstat[(first + q) * 2 + 1]);

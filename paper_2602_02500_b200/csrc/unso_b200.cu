@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/unso_b200.h"
@@ -957,8 +958,13 @@ static bool chain_persistent_fits(const Problem& p) {
     max_blocks_per_sm = nb;
   }
   const int64_t nt = (p.h + 127) / 128;
-  const int64_t T = nt * (nt + 1) / 2 * p.batch;
-  return T <= static_cast<int64_t>(max_blocks_per_sm) * device_sm_count();
+  const int64_t tpm = nt * (nt + 1) / 2;
+  const int64_t cap = static_cast<int64_t>(max_blocks_per_sm) * device_sm_count();
+  if (tpm > cap) return false;
+  // batches run in co-resident chunks; more than ~4 chunks is better served by the
+  // multi-launch pipeline (each launch then covers the whole batch)
+  const int64_t per = cap / tpm;
+  return (p.batch + per - 1) / per <= 4;
 }
 
 static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
@@ -1004,20 +1010,29 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
     cp.alpha += p.co[k];
     cp.coef[k] = static_cast<float>(p.co[k]);
   }
-  if (cudaMemsetAsync(cp.gbar, 0, sizeof(unsigned), st) != cudaSuccess) return UNSO_ERR_CUDA;
   prof_mark(3, st);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(cp.tiles_per_mat * cp.batch));
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = CH_SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, chain_persistent_kernel, maps, cp) != cudaSuccess) return UNSO_ERR_CUDA;
-  ++g_launches;
+  // co-resident chunks of the batch, one cooperative launch each (same stream: the barrier word
+  // and per-tile buffers are reused after the previous chunk completes)
+  int nb_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb_sm, chain_persistent_kernel, 256, CH_SMEM);
+  const int per = std::max(1, nb_sm * device_sm_count() / cp.tiles_per_mat);
+  for (int b0 = 0; b0 < static_cast<int>(p.batch); b0 += per) {
+    const int nb = std::min(per, static_cast<int>(p.batch) - b0);
+    cp.b0 = b0;
+    if (cudaMemsetAsync(cp.gbar, 0, sizeof(unsigned), st) != cudaSuccess) return UNSO_ERR_CUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(cp.tiles_per_mat * nb));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = CH_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, chain_persistent_kernel, maps, cp) != cudaSuccess) return UNSO_ERR_CUDA;
+    ++g_launches;
+  }
   prof_mark(4, st);
   prof_mark(5, st);
   return UNSO_OK;
