@@ -1,15 +1,18 @@
-// fp64-accumulating SIMT (DFMA) GEMM/SYRK engine: the "fp32 mode" of the
-// orthogonalizer (parity <= 1e-5 needs fp64-grade Gram and squaring chain on
-// ill-conditioned inputs), the Gelfand scaling products and
-// the device-side orthogonality-error Gram.
+// fp64-accumulating GEMM/SYRK engine on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64):
+// the "fp32 mode" of the orthogonalizer (parity <= 1e-5 needs fp64-grade Gram and squaring
+// chain on ill-conditioned inputs), the Gelfand scaling products and the
+// device-side orthogonality-error Gram.
 //
-//   D[b](m, n) = sum_k A[b](m, k) * B[b](n, k)        (fp64 accumulate)
+//   D[b](m, n) = sum_k A[b](m, k) * B[b](n, k)        (fp64 products and accumulation)
 //
-// Each operand is a strided batch of row-major matrices read either K-major
-// (element (i,k) at p[i*ld + k]) or MN-major (element (i,k) at p[k*ld + i]),
-// stored as f32 / bf16 / f64.  `syrk` restricts the tile grid to tiles whose
-// columns reach the diagonal (n >= m); the epilogue is only invoked on n >= m
-// there.  `splits` partitions K; every (tile, split) is one CTA.
+// Each operand is a strided batch of row-major matrices read either K-major (element (i,k)
+// at p[i*ld + k]) or MN-major (element (i,k) at p[k*ld + i]), stored as f32 / bf16 / f64 and
+// widened to f64 exactly on the way into shared memory.  `syrk` restricts the tile grid to
+// tiles whose columns reach the diagonal; the epilogue is only invoked on n >= m there.
+// `splits` partitions K; every (tile, split) is one CTA.
+// CTA tile 64 x 64, 4 warps of 32 x 32 (4 x 4 DMMA 8x8x4 fragments), k-tile 16, smem double
+// buffered with register prefetch; shared layouts [k][m] padded by 8 doubles so the 32 lanes of
+// a fragment load hit all banks in the minimum two wavefronts.
 #pragma once
 #include "common.cuh"
 
@@ -23,7 +26,7 @@ struct SimtOperand {
   int kmajor;
 };
 
-constexpr int SIMT_BM = 64, SIMT_BN = 64, SIMT_BK = 16;
+constexpr int SIMT_BM = 64, SIMT_BN = 64, SIMT_BK = 16, SIMT_PAD = 8;
 
 __device__ __forceinline__ void simt_tile_coords(int t, int tiles_m, int tiles_n, int syrk, int& tm, int& tn) {
   if (!syrk) {
@@ -41,13 +44,58 @@ __device__ __forceinline__ void simt_tile_coords(int t, int tiles_m, int tiles_n
   tn = row + t;
 }
 
+__device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// 64 rows x 16 k of one operand -> 8 values per thread (coalesced along the contiguous axis).
+template <int DT>
+__device__ __forceinline__ void simt_fetch(const char* base, const SimtOperand& op, int r0, int k0, int R, int K,
+                                           double (&v)[8]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int e = threadIdx.x + 128 * q;
+    int i, k;
+    if (op.kmajor) { k = e & 15; i = e >> 4; } else { i = e & 63; k = e >> 6; }
+    double x = 0.0;
+    if (r0 + i < R && k0 + k < K) {
+      const int64_t off = op.kmajor ? static_cast<int64_t>(r0 + i) * op.ld + (k0 + k)
+                                    : static_cast<int64_t>(k0 + k) * op.ld + (r0 + i);
+      if (DT == DT_F32) x = static_cast<double>(reinterpret_cast<const float*>(base)[off]);
+      else if (DT == DT_BF16) x = static_cast<double>(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[off]));
+      else x = reinterpret_cast<const double*>(base)[off];
+    }
+    v[q] = x;
+  }
+}
+
+__device__ __forceinline__ void simt_fetch_any(const char* base, const SimtOperand& op, int r0, int k0, int R, int K,
+                                               double (&v)[8]) {
+  if (op.dtype == DT_F64) simt_fetch<DT_F64>(base, op, r0, k0, R, K, v);
+  else if (op.dtype == DT_F32) simt_fetch<DT_F32>(base, op, r0, k0, R, K, v);
+  else simt_fetch<DT_BF16>(base, op, r0, k0, R, K, v);
+}
+
+__device__ __forceinline__ void simt_stash(double (*S)[SIMT_BM + SIMT_PAD], const SimtOperand& op,
+                                           const double (&v)[8]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int e = threadIdx.x + 128 * q;
+    int i, k;
+    if (op.kmajor) { k = e & 15; i = e >> 4; } else { i = e & 63; k = e >> 6; }
+    S[k][i] = v[q];
+  }
+}
+
 template <class Epi>
-__global__ void __launch_bounds__(256) simt_gemm_kernel(SimtOperand A, SimtOperand B, int M, int N, int K, int syrk,
+__global__ void __launch_bounds__(128) simt_gemm_kernel(SimtOperand A, SimtOperand B, int M, int N, int K, int syrk,
                                                         int tiles_m, int tiles_n, int splits, Epi epi) {
-  __shared__ double As[SIMT_BK][SIMT_BM + 1];
-  __shared__ double Bs[SIMT_BK][SIMT_BN + 1];
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  __shared__ __align__(16) double As[2][SIMT_BK][SIMT_BM + SIMT_PAD];
+  __shared__ __align__(16) double Bs[2][SIMT_BK][SIMT_BN + SIMT_PAD];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp >> 1, wn = warp & 1, gid = lane >> 2, tig = lane & 3;
   const int split = blockIdx.y, b = blockIdx.z;
   int tm, tn;
   simt_tile_coords(blockIdx.x, tiles_m, tiles_n, syrk, tm, tn);
@@ -58,61 +106,59 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(SimtOperand A, SimtOpera
   const char* pa = static_cast<const char*>(A.p) + static_cast<int64_t>(b) * A.bstride * dtype_size(A.dtype);
   const char* pb = static_cast<const char*>(B.p) + static_cast<int64_t>(b) * B.bstride * dtype_size(B.dtype);
 
-  double acc[4][4];
+  double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  double va[8], vb[8];
+  if (kt0 < kt1) {
+    simt_fetch_any(pa, A, m0, kt0 * SIMT_BK, M, K, va);
+    simt_fetch_any(pb, B, n0, kt0 * SIMT_BK, N, K, vb);
+    simt_stash(As[0], A, va);
+    simt_stash(Bs[0], B, vb);
+  }
+  __syncthreads();
+  int buf = 0;
   for (int kt = kt0; kt < kt1; ++kt) {
-    const int k0 = kt * SIMT_BK;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int e = tid + 256 * r;
-      int i, k;
-      // A tile: 64 rows x 16 k
-      if (A.kmajor) { k = e & 15; i = e >> 4; } else { i = e & 63; k = e >> 6; }
-      double va = 0.0;
-      if (m0 + i < M && k0 + k < K) {
-        const int64_t off = A.kmajor ? static_cast<int64_t>(m0 + i) * A.ld + (k0 + k)
-                                     : static_cast<int64_t>(k0 + k) * A.ld + (m0 + i);
-        va = load_as_f64(pa, off, A.dtype);
-      }
-      As[k][i] = va;
-      if (B.kmajor) { k = e & 15; i = e >> 4; } else { i = e & 63; k = e >> 6; }
-      double vb = 0.0;
-      if (n0 + i < N && k0 + k < K) {
-        const int64_t off = B.kmajor ? static_cast<int64_t>(n0 + i) * B.ld + (k0 + k)
-                                     : static_cast<int64_t>(k0 + k) * B.ld + (n0 + i);
-        vb = load_as_f64(pb, off, B.dtype);
-      }
-      Bs[k][i] = vb;
+    const bool more = kt + 1 < kt1;
+    if (more) {
+      simt_fetch_any(pa, A, m0, (kt + 1) * SIMT_BK, M, K, va);
+      simt_fetch_any(pb, B, n0, (kt + 1) * SIMT_BK, N, K, vb);
     }
-    __syncthreads();
 #pragma unroll
-    for (int k = 0; k < SIMT_BK; ++k) {
+    for (int kk = 0; kk < SIMT_BK / 4; ++kk) {
       double a[4], bv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[k][ty + 16 * i];
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk * 4 + tig][wm * 32 + i * 8 + gid];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[k][tx + 16 * j];
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][kk * 4 + tig][wn * 32 + j * 8 + gid];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) dmma_884(acc[i][j], a[i], bv[j]);
+    }
+    if (more) {
+      simt_stash(As[buf ^ 1], A, va);
+      simt_stash(Bs[buf ^ 1], B, vb);
     }
     __syncthreads();
+    buf ^= 1;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int m = m0 + ty + 16 * i;
+    const int m = m0 + wm * 32 + i * 8 + gid;
     if (m >= M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int n = n0 + tx + 16 * j;
-      if (n >= N) continue;
-      if (syrk && n < m) continue;
-      epi(b, split, m, n, acc[i][j]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = n0 + wn * 32 + j * 8 + 2 * tig + e;
+        if (n >= N) continue;
+        if (syrk && n < m) continue;
+        epi(b, split, m, n, acc[i][j][e]);
+      }
     }
   }
 }
@@ -124,16 +170,15 @@ inline cudaError_t launch_simt_gemm(const SimtOperand& A, const SimtOperand& B, 
   const int tiles = syrk ? tm * (tm + 1) / 2 : tm * tn;
   if (syrk && tm != tn) return cudaErrorInvalidValue;
   dim3 grid(tiles, splits, batch);
-  simt_gemm_kernel<Epi><<<grid, 256, 0, stream>>>(A, B, M, N, K, syrk ? 1 : 0, tm, tn, splits, epi);
+  simt_gemm_kernel<Epi><<<grid, 128, 0, stream>>>(A, B, M, N, K, syrk ? 1 : 0, tm, tn, splits, epi);
   return cudaGetLastError();
 }
 
-// Heuristic: split K until the (tiles x splits x batch) grid covers ~2 waves of 148 SMs,
-// keeping >= 8 k-tiles per split.
+// Split K until the (tiles x splits x batch) grid covers ~4 CTAs per SM, keeping >= 8 k-tiles per split.
 inline int simt_pick_splits(int tiles, int batch, int K) {
   const int ktiles = (K + SIMT_BK - 1) / SIMT_BK;
   int s = 1;
-  while (static_cast<int64_t>(tiles) * batch * s < 296 && ktiles / (2 * s) >= 8 && s < 64) s *= 2;
+  while (static_cast<int64_t>(tiles) * batch * s < 4 * 148 && ktiles / (2 * s) >= 8 && s < 64) s *= 2;
   return s;
 }
 

@@ -1,0 +1,102 @@
+"""Muon-style optimizer step around the batched orthogonalizer (BASELINE configs[2],
+SURVEY §8f item 2).
+
+For every 2-D parameter: momentum buffer M <- mu M + G (Nesterov: update = G + mu M), the update
+is orthogonalized, rescaled by sqrt(max(1, rows/cols)) and applied with learning rate lr and
+decoupled weight decay.  Parameters of equal shape and dtype are stacked and orthogonalized in ONE
+grouped call (one launch per kernel stage for the whole group), which is what makes a 32-layer
+transformer step (224 matrices of 4096 x {4096, 14336}) tensor-core bound instead of launch bound.
+
+The orthogonalizer is any MethodSpec of this package: the learned UNSO polynomial (default) or the
+NS/Muon quintic iteration.  Non-2-D parameters are updated with plain momentum SGD.
+"""
+
+from __future__ import annotations
+
+import math
+from collections import defaultdict
+from typing import Callable, Iterable
+
+import torch
+
+from .ortho import MethodKind, MethodSpec, orthogonalize
+from .scalarpoly import default_coefficients
+
+
+def default_spec(kind: str = "unso") -> MethodSpec:
+    if kind == "unso":
+        return MethodSpec(MethodKind.UNSO, coeffs=default_coefficients())
+    if kind == "muon":
+        return MethodSpec(MethodKind.MUON_NS, iterations=5)
+    raise ValueError(f"unknown orthogonalizer {kind!r}")
+
+
+class Muon(torch.optim.Optimizer):
+    """Momentum + orthogonalized update, grouped by shape.
+
+    Args:
+        params: iterable of parameters or parameter groups.
+        lr: learning rate.
+        momentum: momentum coefficient mu.
+        nesterov: use the Nesterov form G + mu M.
+        weight_decay: decoupled weight decay.
+        spec: MethodSpec of the orthogonalizer (default: UNSO with the shipped coefficients).
+        precision: "bf16" (tensor cores) or "fp32" (fp64-grade parity path).
+        orthogonalize_fn: override (stacked 3-D tensor -> stacked result); for testing.
+    """
+
+    def __init__(self, params: Iterable, lr: float = 0.02, momentum: float = 0.95, nesterov: bool = True,
+                 weight_decay: float = 0.0, spec: MethodSpec | None = None, precision: str = "bf16",
+                 orthogonalize_fn: Callable | None = None):
+        if lr <= 0.0:
+            raise ValueError("lr must be positive")
+        if not 0.0 <= momentum < 1.0:
+            raise ValueError("momentum must be in [0, 1)")
+        defaults = dict(lr=lr, momentum=momentum, nesterov=nesterov, weight_decay=weight_decay)
+        super().__init__(params, defaults)
+        self.spec = spec or default_spec()
+        self.precision = precision
+        self._ortho = orthogonalize_fn or (
+            lambda u: orthogonalize(u, self.spec, precision=self.precision, check=False).y)
+
+    @torch.no_grad()
+    def step(self, closure=None):
+        loss = None
+        if closure is not None:
+            with torch.enable_grad():
+                loss = closure()
+        for group in self.param_groups:
+            lr, mu, nesterov, wd = group["lr"], group["momentum"], group["nesterov"], group["weight_decay"]
+            buckets: dict = defaultdict(list)
+            for p in group["params"]:
+                if p.grad is None:
+                    continue
+                g = p.grad
+                state = self.state[p]
+                buf = state.get("momentum_buffer")
+                if buf is None:
+                    buf = state["momentum_buffer"] = torch.zeros_like(g)
+                buf.mul_(mu).add_(g)
+                upd = g.add(buf, alpha=mu) if nesterov else buf.clone()
+                if p.dim() == 2:
+                    buckets[(tuple(p.shape), upd.dtype, upd.device)].append((p, upd))
+                else:
+                    if wd:
+                        p.mul_(1.0 - lr * wd)
+                    p.add_(upd, alpha=-lr)
+            for (shape, _, _), items in buckets.items():
+                rows, cols = shape
+                stacked = torch.stack([u for _, u in items]).contiguous()
+                ortho = self._ortho(stacked)
+                zero = stacked.flatten(1).abs().amax(1) == 0     # zero update -> zero step (not degenerate)
+                if bool(zero.any()):
+                    ortho = torch.where(zero[:, None, None], torch.zeros_like(ortho), ortho)
+                scale = math.sqrt(max(1.0, rows / cols))
+                for (p, _), o in zip(items, ortho):
+                    if wd:
+                        p.mul_(1.0 - lr * wd)
+                    p.add_(o.to(p.dtype), alpha=-lr * scale)
+        return loss
+
+
+__all__ = ["Muon", "default_spec"]

@@ -395,3 +395,23 @@ def test_chain_fp8_cross_terms_vs_bf16x3(kind):
     print(f"chain recipes {kind}: {out}")
     assert all(v <= TOL["bf16"] for v in out.values())
     assert out["bf16+e4m3"] <= 1e-2
+
+
+def test_graphed_orthogonalize_matches_eager():
+    from paper_2602_02500_b200.graphs import GraphedOrthogonalize
+    g0 = O.gaussian_matrix(512, 128, 0).astype(np.float32)
+    g1 = O.gaussian_matrix(512, 128, 1).astype(np.float32)
+    for prec, spec in (("fp32", U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())),
+                       ("bf16", U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())),
+                       ("fp32", U.MethodSpec(U.MethodKind.MUON_NS, iterations=5))):
+        x0 = torch.from_numpy(g0).to(DEV)
+        x1 = torch.from_numpy(g1).to(DEV)
+        gr = GraphedOrthogonalize(x0, spec, precision=prec)
+        for x in (x1, x0):
+            y = gr(x).clone()
+            e = U.orthogonalize(x, spec, precision=prec).y
+            assert torch.equal(y, e), prec
+    ms = np.stack([O.gaussian_matrix(2048, 512, 200 + i) for i in range(16)]).astype(np.float32)
+    xb = torch.from_numpy(ms).to(DEV)
+    gr = GraphedOrthogonalize(xb, U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()), precision="bf16")
+    assert torch.equal(gr(xb).clone(), U.orthogonalize(xb, gr.spec, precision="bf16").y)

@@ -1,0 +1,64 @@
+"""Muon-style optimizer around the batched orthogonalizer: grouping and update rule (CPU, with an
+oracle stand-in for the device orthogonalizer) and one real device step (GPU)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2602_02500_b200.muon import Muon
+from oracle import unso_oracle as O
+
+
+def oracle_ortho(calls):
+    def fn(stacked):
+        calls.append(tuple(stacked.shape))
+        return torch.from_numpy(np.stack([O.run(m.double().numpy(), "unso")["y"] for m in stacked])).to(stacked.dtype)
+    return fn
+
+
+def test_grouping_and_update_rule_cpu():
+    torch.manual_seed(0)
+    shapes = [(24, 16), (24, 16), (16, 40), (24, 16), (7,)]
+    params = [torch.nn.Parameter(torch.randn(*s, dtype=torch.float64)) for s in shapes]
+    for p in params:
+        p.grad = torch.randn_like(p)
+    before = [p.detach().clone() for p in params]
+    calls = []
+    opt = Muon(params, lr=0.1, momentum=0.9, nesterov=True, weight_decay=0.01, orthogonalize_fn=oracle_ortho(calls))
+    opt.step()
+    assert sorted(calls) == sorted([(3, 24, 16), (1, 16, 40)])     # one grouped call per shape
+    for p, p0 in zip(params, before):
+        g = p.grad
+        upd = g + 0.9 * g                                          # buffer = g after one step; Nesterov
+        if p.dim() == 2:
+            o = torch.from_numpy(O.run(upd.numpy(), "unso")["y"])
+            exp = p0 * (1 - 0.1 * 0.01) - 0.1 * math.sqrt(max(1.0, p.shape[0] / p.shape[1])) * o
+        else:
+            exp = p0 * (1 - 0.1 * 0.01) - 0.1 * upd
+        assert torch.allclose(p.detach(), exp, atol=1e-12)
+
+
+def test_zero_gradient_gives_zero_step():
+    p = torch.nn.Parameter(torch.randn(8, 4, dtype=torch.float64))
+    p.grad = torch.zeros_like(p)
+    p0 = p.detach().clone()
+    Muon([p], lr=0.1, orthogonalize_fn=lambda s: torch.full_like(s, float("nan"))).step()
+    assert torch.equal(p.detach(), p0)
+
+
+@pytest.mark.gpu
+def test_muon_step_on_device():
+    torch.manual_seed(1)
+    dev = torch.device("cuda:0")
+    params = [torch.nn.Parameter(torch.randn(512, 256, device=dev) * 0.02) for _ in range(3)]
+    params.append(torch.nn.Parameter(torch.randn(256, 1024, device=dev) * 0.02))
+    for p in params:
+        p.grad = torch.randn_like(p) * 0.02
+    before = [p.detach().clone() for p in params]
+    Muon(params, lr=0.05, momentum=0.0, nesterov=False, precision="bf16").step()
+    for p, p0 in zip(params, before):
+        step = (p0 - p.detach()).double().cpu().numpy() / 0.05 / math.sqrt(max(1.0, p.shape[0] / p.shape[1]))
+        ref = O.run(p.grad.to(torch.bfloat16).double().cpu().numpy(), "unso")["y"]
+        assert np.linalg.norm(step - ref) / np.linalg.norm(ref) <= 2e-2

@@ -69,6 +69,17 @@ def run(name, x, spec, precision, nmat, h, w, reps=3, check_against=None):
     return out
 
 
+def run_graphed(name, x, spec, precision, nmat, h, w, reps=50):
+    from paper_2602_02500_b200.graphs import GraphedOrthogonalize
+    g = GraphedOrthogonalize(x, spec, precision=precision)
+    ms = timed(lambda: g(), warm=3, reps=reps)
+    f = U.kernel_model_flops(h, w, spec) * nmat
+    out = {"config": name + " (CUDA graph replay)", "precision": precision, "ms": ms,
+           "matrices_per_s": nmat / (ms / 1e3), "model_tflops": f / (ms / 1e3) / 1e12}
+    print(json.dumps(out), flush=True)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg4,cfg5")
@@ -87,6 +98,9 @@ def main():
         results.append(run("cfg1 512x128 unso", x, unso, "fp32", 1, 128, 512, reps=20, check_against=ref))
         results.append(run("cfg1 512x128 unso", x, unso, "bf16", 1, 128, 512, reps=20, check_against=refb))
         results.append(run("cfg1 512x128 muon5", x, muon, "fp32", 1, 128, 512, reps=20))
+        for prec in ("fp32", "bf16"):
+            results.append(run_graphed("cfg1 512x128 unso", x, unso, prec, 1, 128, 512))
+        results.append(run_graphed("cfg1 512x128 muon5", x, muon, "fp32", 1, 128, 512))
     if "cfg2" in only:
         s = torch.exp(torch.empty(16, 512, device=DEV, dtype=torch.float64).uniform_(np.log(1e-4), 0.0, generator=g))
         x = torch.stack([controlled(2048, 512, s[i], g) for i in range(16)]).float()
@@ -94,6 +108,8 @@ def main():
         refb = U.orthogonalize(x.to(torch.bfloat16).double(), unso, precision="fp32").y  # same rounded input
         results.append(run("cfg2 16x2048x512 unso", x, unso, "fp32", 16, 512, 2048, check_against=ref))
         results.append(run("cfg2 16x2048x512 unso", x, unso, "bf16", 16, 512, 2048, check_against=refb))
+        for prec in ("fp32", "bf16"):
+            results.append(run_graphed("cfg2 16x2048x512 unso", x, unso, prec, 16, 512, 2048, reps=20))
     if "cfg3" in only:
         # one layer group: 4 layers x {4 x 4096^2} and 4 layers x {3 x 14336x4096}, N(0, 0.02^2), bf16
         xs = (torch.randn(16, 4096, 4096, generator=g, device=DEV) * 0.02).to(torch.bfloat16)
