@@ -14,7 +14,7 @@ import threading
 from .errors import DegenerateInputError, NativeError, ShapeError, UnsupportedError
 
 LIB_NAME = "libunso_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("UNSO_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 # unso_status
 OK, ERR_SHAPE, ERR_DEGENERATE, ERR_VALUE, ERR_CUDA, ERR_UNSUPPORTED, ERR_WORKSPACE = range(7)

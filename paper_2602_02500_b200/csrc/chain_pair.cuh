@@ -9,6 +9,8 @@
 // full (both triangles) because direct reads of a diagonal block touch both.
 // Batch: one launch per step for every matrix of the batch (work = batch x upper tiles).
 #pragma once
+#include <type_traits>
+
 #include "umma2_gemm.cuh"
 
 namespace unso {
@@ -22,7 +24,30 @@ constexpr int SC_TILE = 128 * 64 * 2;
 constexpr int SC_STAGE_BYTES = 4 * SC_TILE;  // A hi, A lo, B hi, B lo (per CTA)
 constexpr int SC_EPI_WARPS = 8;
 constexpr int SC_THREADS = 128 + 32 * SC_EPI_WARPS;
-constexpr int SC_SMEM = SC_STAGES * SC_STAGE_BYTES + 256 + 1024;
+constexpr int SC_STAGING = SC_EPI_WARPS * 32 * 32 * 4;  // one 4 KB 32 x 32 fp32 block per epilogue warp
+constexpr int SC_SMEM = SC_STAGES * SC_STAGE_BYTES + 256 + SC_STAGING + 1024;
+
+// Epilogues with a rows4(b, split, row0, col0, stage) member take the accumulator through shared memory.
+template <class E, class = void>
+struct epi_has_rows4 : std::false_type {};
+template <class E>
+struct epi_has_rows4<E, std::void_t<decltype(&E::rows4)>> : std::true_type {};
+
+// lane = row: the lane's 32 accumulator columns go to the warp's 4 KB block, 16-byte chunk j at slot
+// j ^ (row & 7) (conflict-free for these row-wise writes and for rows4's 4-rows-per-instruction
+// reads), then the epilogue re-reads the block with lanes spread along the columns.
+template <class Epi>
+__device__ __forceinline__ void stage_block32(const Epi& epi, float* stage, int b, int split, int row0, int col0,
+                                              const float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(stage + lane * 32 + ((j ^ (lane & 7)) << 2)) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  __syncwarp();
+  epi.rows4(b, split, row0, col0, stage);
+  __syncwarp();
+}
 
 __device__ __forceinline__ void sc_load(const CUtensorMap* kmap, const CUtensorMap* mnmap, uint32_t lbar,
                                         uint8_t* dst, int blk256, int row0, int kt, int b) {
@@ -144,6 +169,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const int q = warp & 3;
+    float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256) + ew * 1024;
     constexpr int CPG = 8 / (SC_EPI_WARPS / 4);
     const int c0 = (ew / 4) * CPG;
     int acc = 0;
@@ -163,7 +189,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        epi(b, split, row, tn * 256 + c * 32, v);
+        if constexpr (epi_has_rows4<Epi>::value)
+          stage_block32(epi, stg, b, split, row - lane, tn * 256 + c * 32, v);
+        else
+          epi(b, split, row, tn * 256 + c * 32, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -256,8 +285,13 @@ struct SymMapsF8 {
 constexpr int F8_TILE = 128 * 128;                           // 16 KB: both e4m3 operands of a k-block
 constexpr int F8_STAGE_BYTES = 2 * (SC_TILE + F8_TILE);     // A: hi, f8; B: hi, f8
 constexpr int F8_STAGES = 3;
-constexpr int F8_SMEM = F8_STAGES * F8_STAGE_BYTES + 256 + 1024;
+constexpr int F8_SMEM = F8_STAGES * F8_STAGE_BYTES + 256 + SC_STAGING + 1024;
 constexpr float F8_CROSS_SCALE = 5.9604644775390625e-08f;  // 2^-24
+#ifdef UNSO_EXP_KMAJOR  // timing experiment only: every operand read K-major (wrong results)
+#define F8_BLK(x) 0
+#else
+#define F8_BLK(x) (x)
+#endif
 
 __device__ __forceinline__ void f8_load(const SymMapsF8& m, uint32_t lbar, uint8_t* dst, int blk256, int row0, int kt,
                                         int b) {
@@ -330,10 +364,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
           uint8_t* st = smem + stage * F8_STAGE_BYTES;
           const uint32_t lbar = lbar0 + stage * 8;
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * F8_STAGE_BYTES);
-          sc_load(&maps.hiK, &maps.hiMN, lbar, st, tm, arow, kt, b);
-          sc_load(&maps.hiK, &maps.hiMN, lbar, st + OFF_BH, tn, brow, kt, b);
-          f8_load(maps, lbar, st + OFF_A8, tm, arow, kt, b);
-          f8_load(maps, lbar, st + OFF_B8, tn, brow, kt, b);
+          sc_load(&maps.hiK, &maps.hiMN, lbar, st, F8_BLK(tm), arow, kt, b);
+          sc_load(&maps.hiK, &maps.hiMN, lbar, st + OFF_BH, F8_BLK(tn), brow, kt, b);
+          f8_load(maps, lbar, st + OFF_A8, F8_BLK(tm), arow, kt, b);
+          f8_load(maps, lbar, st + OFF_B8, F8_BLK(tn), brow, kt, b);
           if (++stage == F8_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -355,7 +389,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const bool a_mn = (kt >> 2) < tm, b_mn = (kt >> 2) < tn;
+          const bool a_mn = (kt >> 2) < F8_BLK(tm), b_mn = (kt >> 2) < F8_BLK(tn);
           const uint32_t id16 = idesc_bf16(256, 256, a_mn ? 1 : 0, b_mn ? 1 : 0);
           const uint32_t id8 = idesc_e4m3(256, 256, a_mn ? 1 : 0, b_mn ? 1 : 0);
           const uint32_t st = smem_u32(smem + stage * F8_STAGE_BYTES);
@@ -387,6 +421,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const int q = warp & 3;
+    float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256) + ew * 1024;
     constexpr int CPG = 8 / (SC_EPI_WARPS / 4);
     const int c0 = (ew / 4) * CPG;
     int acc = 0;
@@ -406,7 +441,13 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r0[j]) * F8_CROSS_SCALE;
-        epi(b, split, row, tn * 256 + c * 32, v);
+#ifdef UNSO_EXP_NOEPI  // timing experiment only: skip the epilogue's global traffic
+        if (v[0] == 12345.f && v[31] == 54321.f)
+#endif
+        if constexpr (epi_has_rows4<Epi>::value)
+          stage_block32(epi, stg, b, split, row - lane, tn * 256 + c * 32, v);
+        else
+          epi(b, split, row, tn * 256 + c * 32, v);
       }
       tc_fence_before();
       __syncwarp();

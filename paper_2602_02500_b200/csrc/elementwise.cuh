@@ -52,6 +52,20 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ src, int64_t sld, i
   }
 }
 
+// contiguous f32 -> bf16: 8 elements per thread per iteration, no index arithmetic beyond the stride
+__global__ void f32_to_bf16_flat_kernel(const float4* __restrict__ src, uint4* __restrict__ dst, int64_t n8) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 a = __ldcs(src + 2 * i), b = __ldcs(src + 2 * i + 1);
+    uint4 o;
+    o.x = pack_bf16x2(a.x, a.y);
+    o.y = pack_bf16x2(a.z, a.w);
+    o.z = pack_bf16x2(b.x, b.y);
+    o.w = pack_bf16x2(b.z, b.w);
+    dst[i] = o;
+  }
+}
+
 // ------------------------------------------------------------------ symmetric tiles
 // 32x32 upper tiles (ti <= tj) of a batch of h x h matrices; the load functor
 // produces tile values, the store functor writes (r, c) in both triangles.
@@ -291,6 +305,59 @@ __global__ void finalize_p_kernel(const void* __restrict__ Pin, int h, int64_t l
     if (ti != tj) {
       const int mr = tj * 32 + r, mc = ti * 32 + tx;
       if (mr < h && mc < h) put(mr, mc, tile[tx][r]);
+    }
+  }
+}
+
+// finalize_p_kernel<1> for the tensor-core path, vectorised: 64 x 64 upper tiles of the f32 P, 16-byte
+// loads and 8-byte bf16 hi/lo stores of both the tile and its mirror.  Same values as the scalar form
+// (split of float(p / s - shift)).  Requires ld % 4 == 0 and ld >= round_up(h, 64) (the workspace ldc):
+// columns in [h, round_up(h, 64)) of the padded rows are written as zeros.
+__global__ void __launch_bounds__(256) finalize_p_bf16_kernel(const float* __restrict__ Pin, int h, int64_t ld,
+                                                              const double* __restrict__ scal,
+                                                              __nv_bfloat16* __restrict__ hi,
+                                                              __nv_bfloat16* __restrict__ lo) {
+  __shared__ float tile[64][65];
+  const int nt = (h + 63) / 64;
+  int ti, tj;
+  sym_tile_coords(blockIdx.x, nt, ti, tj);
+  const int b = blockIdx.y;
+  const int64_t off = static_cast<int64_t>(b) * h * ld;
+  const double inv_s = scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_INV_S];
+  const double shift = scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_SHIFT];
+  const int cq = (threadIdx.x & 15) * 4, r0 = threadIdx.x >> 4;
+  for (int r = r0; r < 64; r += 16) {
+    const int gr = ti * 64 + r, gc = tj * 64 + cq;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (gr < h) v = *reinterpret_cast<const float4*>(Pin + off + static_cast<int64_t>(gr) * ld + gc);
+    const float in[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = gc + q;
+      tile[r][cq + q] =
+          (gr < h && c < h) ? static_cast<float>(static_cast<double>(in[q]) * inv_s - (gr == c ? shift : 0.0)) : 0.f;
+    }
+  }
+  __syncthreads();
+  auto put4 = [&](int gr, int gc, const float (&v)[4]) {
+    __nv_bfloat16 h4[4], l4[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) split_bf16(v[q], h4[q], l4[q]);
+    const int64_t o = off + static_cast<int64_t>(gr) * ld + gc;
+    *reinterpret_cast<uint2*>(hi + o) = *reinterpret_cast<const uint2*>(h4);
+    *reinterpret_cast<uint2*>(lo + o) = *reinterpret_cast<const uint2*>(l4);
+  };
+  for (int r = r0; r < 64; r += 16) {
+    float v[4];
+    if (ti * 64 + r < h) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = (ti == tj && r > cq + q) ? tile[cq + q][r] : tile[r][cq + q];
+      put4(ti * 64 + r, tj * 64 + cq, v);
+    }
+    if (ti != tj && tj * 64 + r < h) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = tile[cq + q][r];
+      put4(tj * 64 + r, ti * 64 + cq, v);
     }
   }
 }

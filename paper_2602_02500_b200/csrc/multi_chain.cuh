@@ -269,6 +269,98 @@ struct EpiChainStep {
     for (int j = 0; j < 8; ++j)
       *reinterpret_cast<float4*>(P + o + 4 * j) = make_float4(pv[4 * j], pv[4 * j + 1], pv[4 * j + 2], pv[4 * j + 3]);
   }
+
+  // Row-coalesced form of the same step for a 32 x 32 block staged in shared memory (chain_pair.cuh
+  // stage_block32): lane = (row sub-index, 4-column group), 4 rows per warp instruction, so every
+  // global access is a run of whole 32-byte sectors instead of 32 scattered 16-byte pieces.
+  // Extra knobs of this form: coefk (pending coefficient of C_k, added here when the previous step
+  // skipped its P update) and write_p (0: leave P untouched, the coefficient stays pending).
+  float coefk = 0.f;
+  int write_p = 1;
+  __device__ __forceinline__ void rows4(int b, int, int row0, int col0, const float* stage) const {
+    const int lane = threadIdx.x & 31, cg = lane & 7, rs = lane >> 3;
+    float cs = 1.f, as = 1.f;
+    if (first) {
+      const double is2 = 1.0 / scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_S2];
+      cs = static_cast<float>(is2);
+      as = static_cast<float>(is2 * is2);
+    }
+    const int c = col0 + 4 * cg;
+    const double w = ((row0 >> 8) == (col0 >> 8)) ? 1.0 : 2.0;
+    double tr = 0.0, fr = 0.0;
+#pragma unroll 2
+    for (int it = 0; it < 8; ++it) {
+      const int r = it * 4 + rs, row = row0 + r;
+      const float4 acc = *reinterpret_cast<const float4*>(stage + r * 32 + ((cg ^ (r & 7)) << 2));
+      if (row >= h) continue;
+      const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + c;
+      const uint2 hw = *reinterpret_cast<const uint2*>(chi + o);
+      const uint2 lw = *reinterpret_cast<const uint2*>(clo + o);
+      float pv[4] = {0.f, 0.f, 0.f, 0.f};
+      if (!first && write_p) {
+        const float4 t = *reinterpret_cast<const float4*>(P + o);
+        pv[0] = t.x; pv[1] = t.y; pv[2] = t.z; pv[3] = t.w;
+      }
+      const float cv[4] = {fmaf(bf16_lo_to_f32(hw.x), in_hi_scale, bf16_lo_to_f32(lw.x)) * cs,
+                           fmaf(bf16_hi_to_f32(hw.x), in_hi_scale, bf16_hi_to_f32(lw.x)) * cs,
+                           fmaf(bf16_lo_to_f32(hw.y), in_hi_scale, bf16_lo_to_f32(lw.y)) * cs,
+                           fmaf(bf16_hi_to_f32(hw.y), in_hi_scale, bf16_hi_to_f32(lw.y)) * cs};
+      const float av[4] = {acc.x, acc.y, acc.z, acc.w};
+      float nv[4], hv[4];
+      uint32_t nh[2], nl[2], q8h = 0u, q8l = 0u;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        nv[e] = 2.0f * cv[e] - av[e] * as;
+        if (first) pv[e] = static_cast<float>((c + e == row ? alpha : 0.0) - static_cast<double>(coef1) * cv[e]);
+        else pv[e] -= coefk * cv[e];
+        pv[e] -= coef * nv[e];
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint32_t hh = pack_bf16x2(nv[2 * e], nv[2 * e + 1]);
+        hv[2 * e] = bf16_lo_to_f32(hh);
+        hv[2 * e + 1] = bf16_hi_to_f32(hh);
+        nh[e] = out_hi_scale == 1.f ? hh : pack_bf16x2(hv[2 * e] * out_hi_scale, hv[2 * e + 1] * out_hi_scale);
+        nl[e] = pack_bf16x2(nv[2 * e] - hv[2 * e], nv[2 * e + 1] - hv[2 * e + 1]);
+      }
+      if (n8hi) {
+        q8h = pack_e4m3x2(hv[0] * 256.0f, hv[1] * 256.0f) | (pack_e4m3x2(hv[2] * 256.0f, hv[3] * 256.0f) << 16);
+        q8l = pack_e4m3x2((nv[0] - hv[0]) * 65536.0f, (nv[1] - hv[1]) * 65536.0f) |
+              (pack_e4m3x2((nv[2] - hv[2]) * 65536.0f, (nv[3] - hv[3]) * 65536.0f) << 16);
+      }
+      if (pstat) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (c + e < h) {
+            fr += w * static_cast<double>(pv[e]) * pv[e];
+            if (c + e == row) tr += pv[e];
+          }
+        }
+      }
+      if (write_next) {
+        *reinterpret_cast<uint2*>(nhi + o) = make_uint2(nh[0], nh[1]);
+        *reinterpret_cast<uint2*>(nlo + o) = make_uint2(nl[0], nl[1]);
+        if (n8hi) {
+          *reinterpret_cast<uint32_t*>(n8hi + o) = q8h;
+          *reinterpret_cast<uint32_t*>(n8lo + o) = q8l;
+          uint8_t* ri = n8i + static_cast<int64_t>(b) * (bs / ld) * ld8i + static_cast<int64_t>(row) * ld8i +
+                        (c >> 6) * 128 + (c & 63);
+          *reinterpret_cast<uint32_t*>(ri) = q8h;
+          *reinterpret_cast<uint32_t*>(ri + 64) = q8l;
+        }
+      }
+      if (first || write_p) *reinterpret_cast<float4*>(P + o) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+    }
+    if (pstat) {
+      tr = warp_sum(tr);
+      fr = warp_sum(fr);
+      if ((threadIdx.x & 31) == 0) {
+        double* s = pstat + partial_slot(b, row0, col0, nt) * 2;
+        s[0] = tr;
+        s[1] = fr;
+      }
+    }
+  }
 };
 
 }  // namespace unso

@@ -674,6 +674,17 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
 }
 
 // ---------------------------------------------------------------- UNSO, BF16 precision (tcgen05)
+// Upper-triangle f32 P -> symmetric bf16 hi/lo (scaled by 1/s, shifted by d) for the apply.
+static int32_t finalize_p_bf16(const Problem& p, const Plan& pl, void* ws, const double* scal, cudaStream_t st) {
+  const int h = static_cast<int>(p.h);
+  const int nt = (h + 63) / 64;
+  dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
+  finalize_p_bf16_kernel<<<grid, 256, 0, st>>>(at<float>(ws, pl.P), h, pl.ldc, scal, at<__nv_bfloat16>(ws, pl.Phi),
+                                               at<__nv_bfloat16>(ws, pl.Plo));
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
 static int32_t ensure_bf16_x(const Problem& p, const Plan& pl, void* ws, const void* x, const __nv_bfloat16*& xb,
                              int64_t& ldx, int64_t& bsx, cudaStream_t st) {
   if (!pl.xcopy) {
@@ -686,8 +697,12 @@ static int32_t ensure_bf16_x(const Problem& p, const Plan& pl, void* ws, const v
   ldx = pl.ldx;
   bsx = p.rows * pl.ldx;
   const int64_t n = p.batch * p.rows * p.cols;
-  if (p.dt == UNSO_DTYPE_F32 && p.cols % 4 == 0 && p.ld % 4 == 0 && p.bs % 4 == 0 &&
-      (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+  if (p.dt == UNSO_DTYPE_F32 && p.ld == p.cols && ldx == p.cols && p.bs == p.rows * p.cols && n % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    f32_to_bf16_flat_kernel<<<grid_for(n / 8, 256, 148 * 16), 256, 0, st>>>(static_cast<const float4*>(x),
+                                                                             reinterpret_cast<uint4*>(dst), n / 8);
+  } else if (p.dt == UNSO_DTYPE_F32 && p.cols % 4 == 0 && p.ld % 4 == 0 && p.bs % 4 == 0 &&
+             (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
     f32_to_bf16_kernel<<<grid_for(n / 4), 256, 0, st>>>(static_cast<const float*>(x), p.ld, p.bs, dst, ldx, bsx,
                                                           p.rows, p.cols, static_cast<int>(p.batch));
   } else {
@@ -762,6 +777,7 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
   const UmmaWork wc2 = umma2_make_work(h, h, h, 256, static_cast<int>(p.batch), true, 1);
   const bool f8 = (p.flags & UNSO_FLAG_CHAIN_BF16X3) == 0;
   int cur = 0;
+  bool p_pending = false;
   for (int k = 1; k < N; ++k) {
     SymMaps maps;
     const void* hi = at<__nv_bfloat16>(ws, pl.Chi[cur]);
@@ -785,6 +801,10 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
       epi.ld8i = 2 * pl.ldc;
     }
     if (f8 && k > 1) epi.in_hi_scale = 1.f / 4096.f;
+    // P is updated every other step (a_k C_k + a_{k+1} C_{k+1} in one read-modify-write)
+    epi.write_p = (k == 1 || (k & 1) || last) ? 1 : 0;
+    epi.coefk = p_pending ? static_cast<float>(p.co[k - 1]) : 0.f;
+    p_pending = epi.write_p == 0;
     cudaError_t le;
     if (f8 && k > 1) {  // C_k is scaled (|C| <= 1): hi*hi in bf16 + e4m3 cross terms
       SymMapsF8 m8;
@@ -811,13 +831,7 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
                                                                          nt2 * (nt2 + 1) / 2 * 64,
                                                                          at<double>(ws, pl.scal), h, adaptive, 5e-3);
   UNSO_CHECK_LAUNCH();
-  {
-    const int nt = (h + 31) / 32;
-    dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
-    finalize_p_kernel<1><<<grid, 256, 0, st>>>(at<float>(ws, pl.P), h, pl.ldc, at<double>(ws, pl.scal),
-                                               at<__nv_bfloat16>(ws, pl.Phi), at<__nv_bfloat16>(ws, pl.Plo));
-    UNSO_CHECK_LAUNCH();
-  }
+  UNSO_TRY(finalize_p_bf16(p, pl, ws, at<double>(ws, pl.scal), st));
   prof_mark(5, st);
   return UNSO_OK;
 }
@@ -933,13 +947,7 @@ static int32_t scale_chain_bf16_multi(const Problem& p, const Plan& pl, void* ws
     cur ^= 1;
   }
   prof_mark(4, st);
-  {
-    const int nt = (h + 31) / 32;
-    dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
-    finalize_p_kernel<1><<<grid, 256, 0, st>>>(at<float>(ws, pl.P), h, pl.ldc, at<double>(ws, pl.scal),
-                                               at<__nv_bfloat16>(ws, pl.Phi), at<__nv_bfloat16>(ws, pl.Plo));
-    UNSO_CHECK_LAUNCH();
-  }
+  UNSO_TRY(finalize_p_bf16(p, pl, ws, at<double>(ws, pl.scal), st));
   prof_mark(5, st);
   return UNSO_OK;
 }
@@ -1193,8 +1201,6 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
   ns_init_state_kernel<<<grid_for(B * xsz), 256, 0, st>>>(x, p.dt, p.ld, p.bs, xscale, at<float>(ws, pl.Xs[0]), xb,
                                                          ldx, p.rows, p.cols, static_cast<int>(B));
   UNSO_CHECK_LAUNCH();
-  const int nt = (h + 31) / 32;
-  const dim3 pgrid(nt * (nt + 1) / 2, static_cast<unsigned>(B));
   const dim3 egrid(grid_for(static_cast<int64_t>(h) * h, 256, 1024), static_cast<unsigned>(B));
   int cur = 0;
   for (int it = 0; it < p.steps; ++it) {
@@ -1226,9 +1232,7 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
                         static_cast<float>(p.co[3 * it + 2])};
       if (launch_chain_pair(maps, wq, qe, st) != cudaSuccess) return UNSO_ERR_CUDA;
       ++g_launches;
-      finalize_p_kernel<1><<<pgrid, 256, 0, st>>>(at<float>(ws, pl.P), h, pl.ldc, unit, at<__nv_bfloat16>(ws, pl.Phi),
-                                                   at<__nv_bfloat16>(ws, pl.Plo));
-      UNSO_CHECK_LAUNCH();
+      UNSO_TRY(finalize_p_bf16(p, pl, ws, unit, st));
     }
     CUtensorMap mx, mph, mpl;
     if (!umma_make_kmajor_map(&mph, at<__nv_bfloat16>(ws, pl.Phi), h, h, pl.ldc, B, pl.hh, 128) ||
