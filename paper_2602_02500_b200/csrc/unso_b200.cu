@@ -251,7 +251,7 @@ struct UEpiChainBF16 {
 
 struct UEpiOut {
   void* out;
-  int dt;  // DT_BF16 or DT_F32
+  int dt;  // DT_BF16, DT_F32 or DT_F64
   int64_t ld, bs;
   int M, N;
   // identity shift: Y += scal[b].shift * X (X = the bf16 operand, same indexing as Y)
@@ -303,7 +303,7 @@ struct UEpiOut {
         for (int j = 0; j < 32; ++j)
           if (col0 + j < N) y[j] = __float2bfloat16_rn(v[j]);
       }
-    } else {
+    } else if (dt == DT_F32) {
       float* y = static_cast<float*>(out) + o;
       if (full && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
 #pragma unroll
@@ -313,6 +313,11 @@ struct UEpiOut {
         for (int j = 0; j < 32; ++j)
           if (col0 + j < N) y[j] = v[j];
       }
+    } else {  // f64 I/O on the tensor-core path (the result carries bf16-mode accuracy)
+      double* y = static_cast<double*>(out) + o;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < N) y[j] = static_cast<double>(v[j]);
     }
   }
 };
@@ -845,7 +850,7 @@ static int32_t apply_bf16(const Problem& p, const Plan& pl, void* ws, const __nv
   if (!umma_make_kmajor_map(&mph, at<__nv_bfloat16>(ws, pl.Phi), h, h, pl.ldc, p.batch, pl.hh, 128) ||
       !umma_make_kmajor_map(&mpl, at<__nv_bfloat16>(ws, pl.Plo), h, h, pl.ldc, p.batch, pl.hh, 128))
     return UNSO_ERR_CUDA;
-  const int ydt = p.dt == UNSO_DTYPE_BF16 ? DT_BF16 : DT_F32;
+  const int ydt = p.dt;  // unso_dtype and Dtype share their values
   cudaError_t e = cudaSuccess;
   const bool pair = use_pair_engine();
   const double* mode = at<double>(ws, pl.scal) + S_MODE;

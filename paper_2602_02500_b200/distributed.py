@@ -29,7 +29,7 @@ import torch.distributed as dist
 from . import _native as N
 from .errors import DegenerateInputError, ShapeError
 from .ortho import (MethodKind, MethodSpec, _DTYPES, _SCALING, _matrix_desc, _method_desc, _resolve_precision,
-                    kernel_model_flops, workspace_pool)
+                    _row_major, kernel_model_flops, workspace_pool)
 
 
 def row_shard_bounds(w: int, world: int, rank: int) -> tuple[int, int]:
@@ -57,6 +57,7 @@ def lpt_assignment(costs: Sequence[float], world: int) -> list[list[int]]:
 
 def native_gram(x_local: torch.Tensor, spec: MethodSpec, precision) -> torch.Tensor:
     """Un-normalised short-side Gram of a row shard (rows = long side)."""
+    x_local = _row_major(x_local)
     xd = _matrix_desc(x_local)
     xd.orientation = 1
     prec = _resolve_precision(spec, x_local, precision)
@@ -80,6 +81,7 @@ def native_gram(x_local: torch.Tensor, spec: MethodSpec, precision) -> torch.Ten
 def native_finish(x_local: torch.Tensor, g: torch.Tensor, spec: MethodSpec, precision,
                   out: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
     """Scale, squaring chain and apply on the local rows, given the reduced Gram."""
+    x_local = _row_major(x_local)
     xd = _matrix_desc(x_local)
     xd.orientation = 1
     prec = _resolve_precision(spec, x_local, precision)

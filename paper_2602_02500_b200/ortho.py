@@ -264,6 +264,16 @@ _SCALING = {Scaling.FROBENIUS_GRAM: N.SCALING_GRAM, Scaling.FROBENIUS_PLAIN: N.S
             Scaling.GELFAND: N.SCALING_GELFAND}
 
 
+def _row_major(t: torch.Tensor) -> torch.Tensor:
+    """The kernels read row-major matrices with any row stride (ld) and batch stride; other layouts
+    (transposed or column-strided views) are copied, like the reference's np.ascontiguousarray."""
+    if isinstance(t, torch.Tensor) and t.dim() in (2, 3) and t.numel() > 0:
+        rows, cols = t.shape[-2], t.shape[-1]
+        if t.stride(-1) != 1 or (rows > 1 and t.stride(-2) < cols):
+            return t.contiguous()
+    return t
+
+
 def _matrix_desc(t: torch.Tensor) -> N.MatrixDesc:
     if not isinstance(t, torch.Tensor):
         raise TypeError("expected a torch.Tensor on a CUDA device")
@@ -344,6 +354,7 @@ def _status_check(status: torch.Tensor, check: bool) -> None:
 
 
 def _run(m: torch.Tensor, spec: MethodSpec, scaling_code: int, precision, out, check: bool):
+    m = _row_major(m)
     xd = _matrix_desc(m)
     prec = _resolve_precision(spec, m, precision)
     md, co = _method_desc(spec, prec, scaling_code)
@@ -398,6 +409,7 @@ def orthogonalize(m: torch.Tensor, spec: MethodSpec, *, precision=None, out=None
 
 def scale_denominator(m: torch.Tensor, scaling: Scaling, gelfand_power: int = 2, check: bool = True) -> torch.Tensor:
     """Per-matrix preprocess denominator on the device (ortho.py:153-165), float64 tensor."""
+    m = _row_major(m)
     xd = _matrix_desc(m)
     scaling = Scaling(scaling)
     md = N.MethodDesc(N.METHOD_UNSO, _SCALING[scaling], gelfand_power, N.PREC_FP32, 1, 0, None, 0, 0)
@@ -480,6 +492,7 @@ def cesista_ns(x: torch.Tensor, step_params: CesistaStepParams, counter: FlopsCo
 
 def ortho_error_device(y: torch.Tensor) -> torch.Tensor:
     """||Y Y^T - I||_F on the short side, per matrix, as a float64 CUDA tensor (bench.py:71-82)."""
+    y = _row_major(y)
     yd = _matrix_desc(y)
     lib = N.lib()
     md = N.MethodDesc(N.METHOD_UNSO, N.SCALING_GRAM, 1, N.PREC_FP32, 1, 0, (ctypes.c_double * 1)(0.0), 0, 0)

@@ -1,0 +1,146 @@
+"""GPU edge cases of the drop-in boundary, each checked against the CPU oracle on the same values
+(tolerances as in test_gpu_parity.py: fp32 mode 1e-5, bf16 mode 2e-2 on the bf16-rounded input).
+
+Covers what the reference's own tests exercise around the kernels (tests/test_ortho.py shapes,
+degenerate inputs, orientation) plus the layouts a torch caller hands over: strided rows whose
+leading dimension breaks TMA's 16-byte rule, transposed views, strided batches, tiny and odd shapes,
+h just past a tile edge, square inputs, fp64 I/O, out=, and a zero matrix inside a batch."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_02500_b200 as U
+from oracle import unso_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0")
+TOL = {"fp32": 1e-5, "bf16": 2e-2}
+UNSO = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+MUON = U.MethodSpec(U.MethodKind.MUON_NS, iterations=5)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def oracle_of(x: torch.Tensor, method: str, precision: str) -> np.ndarray:
+    """Oracle output for the values the kernel actually sees (bf16-rounded in bf16 mode)."""
+    v = x.detach().to(torch.bfloat16 if precision == "bf16" else x.dtype).double().cpu().numpy()
+    kw = {"iterations": 5} if method == "muon" else {}
+    if v.ndim == 2:
+        return O.run(v, method, **kw)["y"]
+    return np.stack([O.run(m, method, **kw)["y"] for m in v])
+
+
+def check(x, spec, method, precision, **kw):
+    res = U.orthogonalize(x, spec, precision=precision, **kw)
+    torch.cuda.synchronize()
+    assert res.y.shape == x.shape and res.y.dtype == x.dtype
+    r = rel(res.y.double().cpu().numpy(), oracle_of(x, method, precision))
+    # a bf16 OUTPUT carries its own rounding: round-to-nearest bounds it by 2^-9 relative (Frobenius)
+    tol = TOL[precision] + (2.0 ** -9 if x.dtype == torch.bfloat16 else 0.0)
+    assert r <= tol, (tuple(x.shape), precision, method, r)
+    return res
+
+
+def gaussian(shape, seed, dtype=torch.float32):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randn(*shape, generator=g, dtype=torch.float64).to(dtype).to(DEV)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (7, 1), (2, 3), (3, 2), (5, 5), (8, 8), (9, 17)])
+def test_tiny_shapes(shape, precision):
+    x = gaussian(shape, 11 + shape[0] * 31 + shape[1])
+    check(x, UNSO, "unso", precision)
+    if precision == "fp32":
+        check(x, MUON, "muon", precision)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("shape", [(300, 37), (37, 1000), (129, 700), (700, 129), (257, 1200), (1300, 255),
+                                   (384, 384), (1000, 1000)])
+def test_odd_and_tile_edge_shapes(shape, precision):
+    """h not a multiple of 8, h one past a 128 / 256 tile, square inputs (not transposed)."""
+    x = gaussian(shape, 100 + shape[0] + shape[1])
+    res = check(x, UNSO, "unso", precision)
+    assert res.was_transposed == (shape[0] > shape[1])
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_strided_rows_unaligned_ld(precision, dtype):
+    """Row stride (ld) = cols + 5: not a multiple of 8 elements, so TMA cannot read it in place."""
+    for rows, cols in ((600, 200), (200, 600)):
+        big = gaussian((rows, cols + 5), rows + cols, dtype)
+        x = big[:, :cols]
+        assert x.stride(0) == cols + 5
+        res = check(x, UNSO, "unso", precision)
+        ref = U.orthogonalize(x.contiguous(), UNSO, precision=precision).y
+        assert torch.equal(res.y, ref)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_transposed_view_and_strided_batch(precision):
+    base = gaussian((6, 300, 120), 5)
+    xt = base[0].t()                      # (120, 300) view with stride(-1) != 1
+    check(xt, UNSO, "unso", precision)
+    xb = base[::2]                        # batch stride 2 x 300 x 120
+    res = check(xb, UNSO, "unso", precision)
+    single = torch.stack([U.orthogonalize(m.contiguous(), UNSO, precision=precision).y for m in xb])
+    assert rel(res.y.double().cpu().numpy(), single.double().cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_batches_of_wide_and_tall(precision):
+    check(gaussian((3, 96, 400), 21), UNSO, "unso", precision)
+    check(gaussian((3, 400, 96), 22), UNSO, "unso", precision)
+
+
+def test_many_tiny_matrices():
+    x = gaussian((512, 16, 8), 33)
+    for precision in ("fp32", "bf16"):
+        check(x, UNSO, "unso", precision)
+    check(x, MUON, "muon", "fp32")
+
+
+def test_fp64_io_both_precisions():
+    x = gaussian((500, 140), 44, torch.float64)
+    res = U.orthogonalize(x, UNSO, precision="fp32")
+    assert res.y.dtype == torch.float64
+    assert rel(res.y.cpu().numpy(), O.run(x.cpu().numpy(), "unso")["y"]) <= 1e-10
+    check(x, UNSO, "unso", "bf16")
+
+
+def test_out_parameter_and_input_untouched():
+    x = gaussian((4, 256, 64), 55)
+    keep = x.clone()
+    out = torch.empty_like(x)
+    res = U.orthogonalize(x, UNSO, precision="bf16", out=out)
+    assert res.y.data_ptr() == out.data_ptr()
+    assert torch.equal(x, keep)
+    with pytest.raises(U.ShapeError):
+        U.orthogonalize(x, UNSO, out=torch.empty(4, 64, 256, device=DEV))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_zero_matrix_inside_batch_is_degenerate(precision):
+    x = gaussian((3, 200, 50), 66)
+    x[1].zero_()
+    with pytest.raises(U.DegenerateInputError):
+        U.orthogonalize(x, UNSO, precision=precision)
+    # the other matrices are still computed (status is per matrix)
+    res = U.orthogonalize(x, UNSO, precision=precision, check=False)
+    torch.cuda.synchronize()
+    for i in (0, 2):
+        assert rel(res.y[i].double().cpu().numpy(), oracle_of(x[i], "unso", precision)) <= TOL[precision]
+
+
+def test_scale_invariance():
+    """Both scalings are scale-invariant (ortho.py:153-165): Y(c X) == Y(X) up to rounding."""
+    x = gaussian((400, 100), 77, torch.float64)
+    a = U.orthogonalize(x, UNSO, precision="fp32").y
+    b = U.orthogonalize(x * 1e3, UNSO, precision="fp32").y
+    assert rel(b.cpu().numpy(), a.cpu().numpy()) <= 1e-12
