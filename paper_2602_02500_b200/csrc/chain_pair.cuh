@@ -9,8 +9,6 @@
 // full (both triangles) because direct reads of a diagonal block touch both.
 // Batch: one launch per step for every matrix of the batch (work = batch x upper tiles).
 #pragma once
-#include <type_traits>
-
 #include "umma2_gemm.cuh"
 
 namespace unso {
@@ -27,27 +25,6 @@ constexpr int SC_THREADS = 128 + 32 * SC_EPI_WARPS;
 constexpr int SC_STAGING = SC_EPI_WARPS * 32 * 32 * 4;  // one 4 KB 32 x 32 fp32 block per epilogue warp
 constexpr int SC_SMEM = SC_STAGES * SC_STAGE_BYTES + 256 + SC_STAGING + 1024;
 
-// Epilogues with a rows4(b, split, row0, col0, stage) member take the accumulator through shared memory.
-template <class E, class = void>
-struct epi_has_rows4 : std::false_type {};
-template <class E>
-struct epi_has_rows4<E, std::void_t<decltype(&E::rows4)>> : std::true_type {};
-
-// lane = row: the lane's 32 accumulator columns go to the warp's 4 KB block, 16-byte chunk j at slot
-// j ^ (row & 7) (conflict-free for these row-wise writes and for rows4's 4-rows-per-instruction
-// reads), then the epilogue re-reads the block with lanes spread along the columns.
-template <class Epi>
-__device__ __forceinline__ void stage_block32(const Epi& epi, float* stage, int b, int split, int row0, int col0,
-                                              const float (&v)[32]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    *reinterpret_cast<float4*>(stage + lane * 32 + ((j ^ (lane & 7)) << 2)) =
-        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-  __syncwarp();
-  epi.rows4(b, split, row0, col0, stage);
-  __syncwarp();
-}
 
 __device__ __forceinline__ void sc_load(const CUtensorMap* kmap, const CUtensorMap* mnmap, uint32_t lbar,
                                         uint8_t* dst, int blk256, int row0, int kt, int b) {

@@ -24,6 +24,20 @@ namespace unso {
 
 constexpr int CHAIN_MAX_ORDER = 64;
 
+#ifdef UNSO_EXP_TIMING  // timing experiment only: per-step event timestamps of three CTAs
+__device__ unsigned long long g_chain_trace[3][CHAIN_MAX_ORDER][5];
+__device__ __forceinline__ void chain_trace(int k, int ev) {
+  const int c = blockIdx.x == 0 ? 0 : (blockIdx.x == gridDim.x / 2 ? 1 : (blockIdx.x == gridDim.x - 1 ? 2 : -1));
+  if (c < 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_chain_trace[c][k][ev] = t;
+}
+#define CHAIN_TRACE(k, ev) chain_trace(k, ev)
+#else
+#define CHAIN_TRACE(k, ev)
+#endif
+
 struct ChainMaps {
   // [buffer][0 = hi, 1 = lo][0 = K-major box {64,128}, 1 = MN-major box {64,64}]
   CUtensorMap m[2][2][2];
@@ -128,6 +142,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       uint32_t phase = 0;
       for (int k = 1; k < N; ++k) {
         grid_wait(p.gbar, static_cast<unsigned>(k + 1) * T);  // C_k published (round k)
+        CHAIN_TRACE(k, 0);
         fence_proxy_async_global();
         const int buf = (k - 1) & 1;
         for (int kt = 0; kt < KT; ++kt) {
@@ -156,6 +171,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         tc_fence_after();
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&full[stage], phase);
+          if (kt == 0) CHAIN_TRACE(k, 1);
           tc_fence_after();
           const int kb = kt >> 1;
           const bool a_mn = kb < ti, b_mn = kb < tj;
@@ -170,8 +186,10 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
             const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * CH_TILE, ks)
                                      : operand_desc<false>(st + 3 * CH_TILE, ks);
             umma_bf16(tmem + CH_ACC, ah, bh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
+#ifndef UNSO_EXP_ONETERM  // timing experiment only: hi*hi alone, loads unchanged
             umma_bf16(tmem + CH_ACC, ah, bl, idesc, 1u);
             umma_bf16(tmem + CH_ACC, al, bh, idesc, 1u);
+#endif
           }
           umma_commit(&empty[stage]);
           if (++stage == CH_STAGES) {
@@ -180,6 +198,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
           }
         }
         umma_commit(tfull);
+        CHAIN_TRACE(k, 2);
         acc_phase ^= 1;
       }
     }
@@ -305,6 +324,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       const bool last = (k == N - 1);
       const float coef = p.coef[k];  // multiplies C_{k+1}
       mbar_wait(tfull, acc_phase);
+      if (tid == 0) CHAIN_TRACE(k, 3);
       acc_phase ^= 1;
       tc_fence_after();
       for (int c = 0; c < 4; ++c) {
@@ -347,6 +367,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       if (!last) {
         fence_proxy_async_global();
         named_bar_sync(1, 128);
+        if (tid == 0) CHAIN_TRACE(k, 4);
         if (tid == 0) grid_arrive(p.gbar);  // round k+1: C_{k+1} published
       }
     }

@@ -288,19 +288,28 @@ struct EpiChainStep {
     const int c = col0 + 4 * cg;
     const double w = ((row0 >> 8) == (col0 >> 8)) ? 1.0 : 2.0;
     double tr = 0.0, fr = 0.0;
-#pragma unroll 2
+    // all eight rows' loads first, so their latencies overlap
+    uint2 hwv[8], lwv[8];
+    float4 pvv[8];
+    const bool load_p = !first && write_p;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int row = row0 + it * 4 + rs;
+      const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + c;
+      const bool ok = row < h;
+      hwv[it] = ok ? *reinterpret_cast<const uint2*>(chi + o) : make_uint2(0u, 0u);
+      lwv[it] = ok ? *reinterpret_cast<const uint2*>(clo + o) : make_uint2(0u, 0u);
+      pvv[it] = (ok && load_p) ? *reinterpret_cast<const float4*>(P + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
     for (int it = 0; it < 8; ++it) {
       const int r = it * 4 + rs, row = row0 + r;
       const float4 acc = *reinterpret_cast<const float4*>(stage + r * 32 + ((cg ^ (r & 7)) << 2));
       if (row >= h) continue;
       const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + c;
-      const uint2 hw = *reinterpret_cast<const uint2*>(chi + o);
-      const uint2 lw = *reinterpret_cast<const uint2*>(clo + o);
-      float pv[4] = {0.f, 0.f, 0.f, 0.f};
-      if (!first && write_p) {
-        const float4 t = *reinterpret_cast<const float4*>(P + o);
-        pv[0] = t.x; pv[1] = t.y; pv[2] = t.z; pv[3] = t.w;
-      }
+      const uint2 hw = hwv[it];
+      const uint2 lw = lwv[it];
+      float pv[4] = {pvv[it].x, pvv[it].y, pvv[it].z, pvv[it].w};
       const float cv[4] = {fmaf(bf16_lo_to_f32(hw.x), in_hi_scale, bf16_lo_to_f32(lw.x)) * cs,
                            fmaf(bf16_hi_to_f32(hw.x), in_hi_scale, bf16_hi_to_f32(lw.x)) * cs,
                            fmaf(bf16_lo_to_f32(hw.y), in_hi_scale, bf16_lo_to_f32(lw.y)) * cs,

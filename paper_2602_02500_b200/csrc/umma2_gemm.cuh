@@ -14,6 +14,8 @@
 // Same term/operand conventions as umma_gemm.cuh; the epilogue functor receives
 // (b, split, row, col0, v[32]) for the CTA's own rows.
 #pragma once
+#include <type_traits>
+
 #include "umma_gemm.cuh"
 
 namespace unso {
@@ -59,6 +61,28 @@ __device__ __forceinline__ bool opt_skipped(const UmmaWork& w, int b) {
 __device__ __forceinline__ bool filtered_out(const UmmaWork& w, int b) {
   if (!w.mode_flag || w.mode_want < 0) return false;
   return (w.mode_flag[static_cast<int64_t>(b) * w.opt_stride] != 0.0) != (w.mode_want == 1);
+}
+
+// Epilogues with a rows4(b, split, row0, col0, stage) member take the accumulator through shared memory.
+template <class E, class = void>
+struct epi_has_rows4 : std::false_type {};
+template <class E>
+struct epi_has_rows4<E, std::void_t<decltype(&E::rows4)>> : std::true_type {};
+
+// lane = row: the lane's 32 accumulator columns go to the warp's 4 KB block, 16-byte chunk j at slot
+// j ^ (row & 7) (conflict-free for these row-wise writes and for rows4's 4-rows-per-instruction
+// reads), then the epilogue re-reads the block with lanes spread along the columns.
+template <class Epi>
+__device__ __forceinline__ void stage_block32(const Epi& epi, float* stage, int b, int split, int row0, int col0,
+                                              const float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(stage + lane * 32 + ((j ^ (lane & 7)) << 2)) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  __syncwarp();
+  epi.rows4(b, split, row0, col0, stage);
+  __syncwarp();
 }
 
 template <class Cfg, class Epi>
@@ -197,6 +221,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     constexpr int GROUPS = Cfg::EPI_WARPS / 4;      // column groups
     constexpr int CPG = Cfg::BN / 32 / GROUPS;      // 32-column chunks per group
     const int c0 = (ew / 4) * CPG;
+    float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256) + ew * 1024;
+    (void)stg;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int idx = cluster; idx < work.num_work; idx += nclusters) {
@@ -215,7 +241,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        epi(b, split, row, tn * Cfg::BN + c * 32, v);
+        if constexpr (epi_has_rows4<Epi>::value)
+          stage_block32(epi, stg, b, split, row - lane, tn * Cfg::BN + c * 32, v);
+        else
+          epi(b, split, row, tn * Cfg::BN + c * 32, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -250,10 +279,12 @@ inline UmmaWork umma2_make_work(int M, int N, int K, int BN, int batch, bool syr
 template <class Cfg, class Epi>
 inline cudaError_t launch_umma2(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
                                 const CUtensorMap& b1, const UmmaWork& w, const Epi& epi, cudaStream_t stream) {
+  constexpr int smem = Cfg::SMEM + (epi_has_rows4<Epi>::value ? Cfg::EPI_WARPS * 4096 : 0);
+  static_assert(smem <= 227 * 1024, "smem budget with the epilogue staging blocks");
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(umma2_gemm_kernel<Cfg, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM);
+                                         smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -263,7 +294,7 @@ inline cudaError_t launch_umma2(const CUtensorMap& a0, const CUtensorMap& a1, co
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * nclusters));
   cfg.blockDim = dim3(Cfg::THREADS);
-  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

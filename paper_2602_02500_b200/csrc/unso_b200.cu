@@ -1359,6 +1359,12 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
                               y_ptr, d_status, st);
 }
 
+#ifdef UNSO_EXP_TIMING
+extern "C" int32_t unso_debug_chain_trace(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_chain_trace, sizeof(g_chain_trace)) == cudaSuccess ? UNSO_OK : UNSO_ERR_CUDA;
+}
+#endif
+
 int32_t unso_query_scalars(const unso_matrix_desc* x, const unso_method_desc* method, const void* workspace,
                            double* d_out, void* stream) {
   Problem p;
