@@ -279,12 +279,6 @@ __device__ __forceinline__ void f8_load(const SymMapsF8& m, uint32_t lbar, uint8
     tma_load_3d_pair(&m.l8MN, lbar, dst + 8192, row0, kt * 64, b);  // ... lo8
   }
 }
-// Descriptor of the hi8 (lo = 0) or lo8 (lo = 1) operand, MMA k-step ks (32 e4m3 each).
-__device__ __forceinline__ uint64_t f8_desc(uint32_t tile, bool mn, int lo, int ks) {
-  return mn ? sdesc_sw128(tile + lo * 8192 + ks * 4096, 8192, 1024)   // 32 K-rows of 128 B
-            : sdesc_sw128(tile + lo * 64 + ks * 32, 16, 1024);        // 32 B inside the 128 B row
-}
-
 template <class Epi>
 __global__ void __launch_bounds__(SC_THREADS, 1)
     chain_pair_f8_kernel(const __grid_constant__ SymMapsF8 maps, const UmmaWork work, const Epi epi) {

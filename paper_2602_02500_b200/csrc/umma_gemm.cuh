@@ -82,6 +82,14 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t tile_addr, int ks) {
   return MN ? sdesc_sw128(tile_addr + ks * 2048, 8192, 1024) : sdesc_sw128(tile_addr + ks * 32, 16, 1024);
 }
 
+// e4m3 operand tile of a 128-row block (chain kernels): K-major = one SWIZZLE_128B box of
+// 128 rows x [hi8 k0..63 | lo8 k0..63]; MN-major = hi8 plane (64 K-rows x 128 B) then lo8 plane.
+// Descriptor of the hi8 (lo = 0) or lo8 (lo = 1) operand, MMA k-step ks (32 e4m3 each).
+__device__ __forceinline__ uint64_t f8_desc(uint32_t tile, bool mn, int lo, int ks) {
+  return mn ? sdesc_sw128(tile + lo * 8192 + ks * 4096, 8192, 1024)   // 32 K-rows of 128 B
+            : sdesc_sw128(tile + lo * 64 + ks * 32, 16, 1024);        // 32 B inside the 128 B row
+}
+
 template <class Cfg, class Epi>
 __global__ void __launch_bounds__(256, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,

@@ -30,7 +30,8 @@ def main():
         b = int(sys.argv[3])
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn(b, w, h, generator=g, device="cuda").to(dt)
-    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    chain = os.environ.get("UNSO_CHAIN")  # e.g. "bf16x3"
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), chain=chain)
     U.orthogonalize(x, spec, precision=prec, check=False)
     torch.cuda.synchronize()
     with StageProfiler(reps) as prof:
