@@ -67,6 +67,12 @@ typedef enum unso_method { UNSO_METHOD_UNSO = 0, UNSO_METHOD_ORIGINAL_NS = 1, UN
                                            device when ||X dR||_F / ||Y||_F <= 2^-9 ||R||_F / sqrt(tr C_1) <= 5e-3
                                            (R = P - d I, d = tr(P)/h; d X is added exactly in the epilogue). */
 
+#define UNSO_FLAG_NO_TRUNCATION 0x8     /* UNSO, BF16: run all N-1 squarings.  Default: the persistent chain
+                                           (h <= ~1900 per co-resident batch) stops before step k once every
+                                           matrix has sum_{j>k}|c_j| * ||I - C_k||_F^2 <= 2^-12 and subtracts
+                                           sum_{j>k} c_j * I (the remaining C_j are I to that bound; with
+                                           ||X||_2 <= 1 the relative change of Y is at most that bound). */
+
 typedef struct unso_matrix_desc {
   int64_t rows, cols;    /* per matrix, as given (orientation is chosen internally, ortho.py:149-150) */
   int64_t ld;            /* leading dimension in elements, >= cols */

@@ -36,8 +36,10 @@ EXPORTED_SYMBOLS = (
     "unso_query_scalars",
 )
 SCALARS = 16
-SCALAR_NAMES = ("trace", "fro2", "dev2", "s2", "inv_s", "ortho_error", "shift", "apply_single", "apply_bound")
+SCALAR_NAMES = ("trace", "fro2", "dev2", "s2", "inv_s", "ortho_error", "shift", "apply_single", "apply_bound",
+                "chain_steps")
 FLAG_TWO_TERM_APPLY = 0x2
+FLAG_NO_TRUNCATION = 0x8
 FLAG_CHAIN_BF16X3 = 0x4
 PROFILE_STAGES = ("convert", "gram", "scale_prep", "chain", "finalize_p", "apply")
 

@@ -15,6 +15,12 @@
 //   with kb < i is read through an MN-major (transposed) TMA map of tile (kb, i), and the
 //   tcgen05 instruction descriptor's A/B major bits are switched per k-block.
 //   A grid barrier (gpu-scope release/acquire counter) separates the steps.
+//
+// Data-dependent truncation: each step also reduces ||I - C_{k+1}||_F^2 per tile.
+// Before step k every role sums those partials (fixed order, so all CTAs agree) and, once every
+// matrix of the launch has tail_abs[k] * ||I - C_k||_F^2 <= trunc_tau, stops: the remaining
+// C_j (j > k) equal I up to ||B_k||_2^(2^(j-k)) <= ||I - C_k||_F^2, so P -= tail[k] I replaces them
+// (tail[k] = sum_{j>k} c_j; the dropped terms are bounded by tail_abs[k] ||I - C_k||_F^2).
 #pragma once
 #include "common.cuh"
 #include "ptx_sm100.cuh"
@@ -59,30 +65,48 @@ struct ChainParams {
   double tau;          // bound threshold for that decision
   double* scal;        // [batch][SCAL_STRIDE]
   int32_t* status;     // [batch]
-  unsigned* gbar;      // zeroed before launch
+  unsigned long long* gbar;  // [CHAIN_ROUNDS] per-round barrier words, zeroed before launch
   int order;
   int scal_mode;       // SM_GRAM / SM_PLAIN / SM_NONE
   double alpha;        // 1 + sum a + b
   float coef[CHAIN_MAX_ORDER];  // coef[k-1] multiplies C_k
+  double trunc_tau;    // 0 disables truncation
+  float tail[CHAIN_MAX_ORDER];      // tail[k] = sum_{j > k} coef[j-1]
+  float tail_abs[CHAIN_MAX_ORDER];  // tail_abs[k] = sum_{j > k} |coef[j-1]|
 };
+
+// Grid barrier, one 64-bit word per round r: every CTA adds (1 << 48) + a fixed-point (2^-33, clamped
+// to [0, 1]) partial; the wait returns the exact, order-independent sum of the round's partials.
+// Rounds: 0 = Gram norms, 1 = C_1 published, k + 1 = C_{k+1} published by step k, then the final P.
+constexpr int CHAIN_ROUNDS = CHAIN_MAX_ORDER + 2;
+constexpr double CHAIN_FIX = 8589934592.0;  // 2^33
+__device__ __forceinline__ void grid_arrive(unsigned long long* gbar, int round, double partial = 0.0) {
+  const double c = fmin(fmax(partial, 0.0), 1.0);
+  __threadfence();
+  red_release_gpu_add_u64(gbar + round, (1ull << 48) + static_cast<uint64_t>(c * CHAIN_FIX));
+}
+__device__ __forceinline__ uint64_t grid_wait(const unsigned long long* gbar, int round) {
+  const long long t0 = clock64();
+  const uint64_t T = gridDim.x;
+  uint64_t v;
+  while (((v = ld_acquire_gpu_u64(gbar + round)) >> 48) < T) {
+    __nanosleep(64);
+    if (clock64() - t0 > UNSO_WATCHDOG_CYCLES) __trap();
+  }
+  return v & ((1ull << 48) - 1);
+}
+// After round k (C_k published, `sum` = that round's partials = sum over the launch's matrices of
+// ||I - C_k||_F^2): every role takes the same decision whether the chain stops before step k.
+__device__ __forceinline__ bool chain_truncate_before(const ChainParams& p, int k, uint64_t sum) {
+  if (p.trunc_tau <= 0.0 || k < 2) return false;
+  return static_cast<double>(p.tail_abs[k]) * (static_cast<double>(sum) / CHAIN_FIX) <= p.trunc_tau;
+}
 
 constexpr int CH_STAGES = 3;
 constexpr int CH_TILE = 128 * 64 * 2;          // 16 KB operand tile
 constexpr int CH_STAGE_BYTES = 4 * CH_TILE;    // A hi, A lo, B hi, B lo
 constexpr int CH_SMEM = CH_STAGES * CH_STAGE_BYTES + 256 + 1024;
 constexpr uint32_t CH_ACC = 0, CH_P = 128, CH_C = 256;
-
-__device__ __forceinline__ void grid_arrive(unsigned* gbar) {
-  __threadfence();
-  red_release_gpu_add(gbar, 1u);
-}
-__device__ __forceinline__ void grid_wait(const unsigned* gbar, unsigned target) {
-  const long long t0 = clock64();
-  while (ld_acquire_gpu(gbar) < target) {
-    __nanosleep(64);
-    if (clock64() - t0 > UNSO_WATCHDOG_CYCLES) __trap();
-  }
-}
 
 __device__ __forceinline__ void ch_load_block(const ChainMaps& maps, int buf, int hl, uint64_t* bar, uint8_t* dst,
                                               int blk, int kt, int b) {
@@ -108,7 +132,6 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
   __shared__ double s_scale[2];  // inv_s2, inv_s
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = gridDim.x;
   const int lb = blockIdx.x / p.tiles_per_mat;  // matrix within this chunk
   const int b = p.b0 + lb;
   const int t = blockIdx.x % p.tiles_per_mat;
@@ -141,7 +164,8 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       int stage = 0;
       uint32_t phase = 0;
       for (int k = 1; k < N; ++k) {
-        grid_wait(p.gbar, static_cast<unsigned>(k + 1) * T);  // C_k published (round k)
+        const uint64_t e2 = grid_wait(p.gbar, k);  // C_k published (round k)
+        if (chain_truncate_before(p, k, e2)) break;
         CHAIN_TRACE(k, 0);
         fence_proxy_async_global();
         const int buf = (k - 1) & 1;
@@ -167,6 +191,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int k = 1; k < N; ++k) {
+        if (k >= 2 && p.trunc_tau > 0.0 && chain_truncate_before(p, k, grid_wait(p.gbar, k))) break;
         mbar_wait(tempty, acc_phase ^ 1);
         tc_fence_after();
         for (int kt = 0; kt < KT; ++kt) {
@@ -256,8 +281,8 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     if (tid == 0) {
       p.normbuf[blockIdx.x * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
       p.normbuf[blockIdx.x * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
-      grid_arrive(p.gbar);  // round 0
-      grid_wait(p.gbar, static_cast<unsigned>(T));
+      grid_arrive(p.gbar, 0);
+      grid_wait(p.gbar, 0);
       double s0 = 0.0, s1 = 0.0;
       const int first = lb * p.tiles_per_mat;
       for (int q = 0; q < p.tiles_per_mat; ++q) {  // fixed order -> deterministic
@@ -316,17 +341,42 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     (void)inv_s2;
     fence_proxy_async_global();
     named_bar_sync(1, 128);
-    if (tid == 0) grid_arrive(p.gbar);  // round 1: C_1 published
+    if (tid == 0) grid_arrive(p.gbar, 1);  // C_1 published
 
     // ---- phase B: squaring steps
+    __shared__ int s_stop;
     uint32_t acc_phase = 0;
+    int steps = 0;
+    unsigned last_round = 1;  // rounds published so far: 0 (norms), 1 (C_1), then k+1 per step k
     for (int k = 1; k < N; ++k) {
+      if (k >= 2 && p.trunc_tau > 0.0) {
+        if (tid == 0) s_stop = chain_truncate_before(p, k, grid_wait(p.gbar, k)) ? 1 : 0;
+        named_bar_sync(1, 128);
+        if (s_stop) {  // C_j = I for j > k: P -= tail[k] I on the diagonal; P stays in TMEM
+          const float tl = p.tail[k];
+          for (int c = 0; c < 4; ++c) {
+            const int gc0 = tj * 128 + c * 32;
+            uint32_t up[32];
+            tmem_ld32(lane_base + CH_P + c * 32, up);  // warp-collective: every lane
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (row_ok && gc0 + j == gr) up[j] = __float_as_uint(__uint_as_float(up[j]) - tl);
+            tmem_st32(lane_base + CH_P + c * 32, up);
+          }
+          tmem_wait_st();
+          break;
+        }
+      }
       const bool last = (k == N - 1);
       const float coef = p.coef[k];  // multiplies C_{k+1}
+      ++steps;
       mbar_wait(tfull, acc_phase);
       if (tid == 0) CHAIN_TRACE(k, 3);
       acc_phase ^= 1;
       tc_fence_after();
+      const bool want_e2 = p.trunc_tau > 0.0 && !last;
+      float e2 = 0.f;  // ||I - C_{k+1}||_F^2 over this thread's part of the tile (weighted below)
       for (int c = 0; c < 4; ++c) {
         const int gc0 = tj * 128 + c * 32;
         uint32_t ua[32], uc[32], up[32];
@@ -344,6 +394,10 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
           uc[j] = __float_as_uint(cn);
           up[j] = __float_as_uint(pv);
           split_bf16(cn, hi[j], lo[j]);
+          if (want_e2) {
+            const float dv = ok ? cn - (gc0 + j == gr ? 1.f : 0.f) : 0.f;
+            e2 = fmaf(dv, dv, e2);
+          }
         }
         if (!last) {
           tmem_st32(lane_base + CH_C + c * 32, uc);
@@ -365,10 +419,18 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       tc_fence_before();
       mbar_arrive(tempty);
       if (!last) {
+        if (want_e2) {
+          const double e2w = warp_sum(wgt * static_cast<double>(e2));
+          if (lane == 0) red[0][ew] = e2w;
+        }
         fence_proxy_async_global();
         named_bar_sync(1, 128);
-        if (tid == 0) CHAIN_TRACE(k, 4);
-        if (tid == 0) grid_arrive(p.gbar);  // round k+1: C_{k+1} published
+        if (tid == 0) {
+          CHAIN_TRACE(k, 4);
+          const double part = p.trunc_tau > 0.0 ? red[0][0] + red[0][1] + red[0][2] + red[0][3] : 0.0;
+          grid_arrive(p.gbar, k + 1, part);  // C_{k+1} published, with its ||I - C||_F^2 partial
+        }
+        last_round = static_cast<unsigned>(k + 1);
       }
     }
     // ---- final P: statistics -> identity shift d and the adaptive apply decision, then
@@ -398,10 +460,9 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       if (tid == 0) {
         p.pstat[blockIdx.x * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
         p.pstat[blockIdx.x * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
-        // rounds so far: 0 (norms), 1 (C_1), 2..N-1 (C_{k+1}, k < N-1); this is the next one
-        const unsigned round = N >= 2 ? static_cast<unsigned>(N) : 2u;
-        grid_arrive(p.gbar);
-        grid_wait(p.gbar, (round + 1) * static_cast<unsigned>(T));
+        const int round = static_cast<int>(last_round) + 1;
+        grid_arrive(p.gbar, round);
+        grid_wait(p.gbar, round);
         double tp = 0.0, s2p = 0.0;
         const int first = lb * p.tiles_per_mat;
         for (int q = 0; q < p.tiles_per_mat; ++q) {
@@ -421,6 +482,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
           o[S_SHIFT] = d * s_scale[1];
           o[S_MODE] = single ? 1.0 : 0.0;
           o[S_BOUND] = bound;
+          o[S_STEPS] = steps;
         }
       }
       named_bar_sync(1, 128);

@@ -11,9 +11,11 @@ constexpr int NORM_BLOCKS = 64;  // per-matrix partial-reduction blocks (fixed -
 
 // scal[b * SCAL_STRIDE + ...]
 // S_SHIFT: d/s, the identity shift removed from P before the bf16 split (added back as d/s * X in the
-// apply epilogue); S_MODE: 1 = the apply may skip the P_lo term (adaptive bound met); S_BOUND: that bound.
+// apply epilogue); S_MODE: 1 = the apply may skip the P_lo term (adaptive bound met); S_BOUND: that bound;
+// S_STEPS: squarings the persistent chain executed (< N-1 after truncation), -1 on other routes.
 enum ScalSlot : int {
-  S_TRACE = 0, S_FRO2 = 1, S_DEV2 = 2, S_S2 = 3, S_INV_S = 4, S_ERR = 5, S_SHIFT = 6, S_MODE = 7, S_BOUND = 8
+  S_TRACE = 0, S_FRO2 = 1, S_DEV2 = 2, S_S2 = 3, S_INV_S = 4, S_ERR = 5, S_SHIFT = 6, S_MODE = 7, S_BOUND = 8,
+  S_STEPS = 9
 };
 constexpr int SCAL_STRIDE = 16;
 
@@ -201,6 +203,7 @@ __global__ void scalars_kernel(const double* __restrict__ blk, int nblk, int mod
   o[S_SHIFT] = 0.0;
   o[S_MODE] = 0.0;
   o[S_BOUND] = -1.0;
+  o[S_STEPS] = -1.0;
   if (mode == SM_NONE) {  // bare kernel on pre-scaled input: no rescale, no degenerate check
     o[S_S2] = 1.0;
     o[S_INV_S] = 1.0;

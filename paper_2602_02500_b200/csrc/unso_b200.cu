@@ -512,7 +512,7 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
         pl.C8l[i] = take(pl, static_cast<size_t>(B * pl.hh));
         pl.C8i[i] = take(pl, static_cast<size_t>(B * pl.hh) * 2);
       }
-      pl.gbar = take(pl, 256);
+      pl.gbar = take(pl, CHAIN_ROUNDS * 8);
     } else {
       pl.C[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
       pl.C[1] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
@@ -1015,13 +1015,24 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
   cp.tau = 5e-3;
   cp.scal = at<double>(ws, pl.scal);
   cp.status = status;
-  cp.gbar = at<unsigned>(ws, pl.gbar);
+  cp.gbar = at<unsigned long long>(ws, pl.gbar);
   cp.order = p.order;
   cp.scal_mode = scal_mode(p.scaling);
   cp.alpha = 1.0;
   for (int k = 0; k < p.order; ++k) {
     cp.alpha += p.co[k];
     cp.coef[k] = static_cast<float>(p.co[k]);
+  }
+  // truncation (chain_persistent.cuh): tail[k] = sum_{j>k} c_j, c_j = co[j-1]
+  cp.trunc_tau = (p.flags & UNSO_FLAG_NO_TRUNCATION) ? 0.0 : std::ldexp(1.0, -12);
+  for (int k = 0; k <= p.order && k < CHAIN_MAX_ORDER; ++k) {
+    double t = 0.0, ta = 0.0;
+    for (int j = k + 1; j <= p.order; ++j) {
+      t += p.co[j - 1];
+      ta += std::fabs(p.co[j - 1]);
+    }
+    cp.tail[k] = static_cast<float>(t);
+    cp.tail_abs[k] = static_cast<float>(ta);
   }
   prof_mark(3, st);
   // co-resident chunks of the batch, one cooperative launch each (same stream: the barrier word
@@ -1032,7 +1043,8 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
   for (int b0 = 0; b0 < static_cast<int>(p.batch); b0 += per) {
     const int nb = std::min(per, static_cast<int>(p.batch) - b0);
     cp.b0 = b0;
-    if (cudaMemsetAsync(cp.gbar, 0, sizeof(unsigned), st) != cudaSuccess) return UNSO_ERR_CUDA;
+    if (cudaMemsetAsync(cp.gbar, 0, CHAIN_ROUNDS * sizeof(unsigned long long), st) != cudaSuccess)
+      return UNSO_ERR_CUDA;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(cp.tiles_per_mat * nb));
     cfg.blockDim = dim3(256);

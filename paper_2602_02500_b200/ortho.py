@@ -76,6 +76,7 @@ class MethodSpec:
     precision: Precision | None = None
     apply_terms: int | None = None   # bf16 mode: None = adaptive per matrix, 1 = P_hi only, 2 = P_hi + P_lo
     chain: str | None = None         # bf16 mode, large h: None = bf16 hi*hi + e4m3 cross terms, "bf16x3"
+    truncate: bool = True            # bf16 mode, persistent chain: stop once ||I - C_k||_F bounds the rest
 
     def __post_init__(self):
         kind = MethodKind(self.kind)
@@ -319,6 +320,8 @@ def _method_desc(spec: MethodSpec, precision: Precision, scaling_code: int):
     flags = {None: 0, 1: N.FLAG_SINGLE_TERM_APPLY, 2: N.FLAG_TWO_TERM_APPLY}[spec.apply_terms]
     if spec.chain == "bf16x3":
         flags |= N.FLAG_CHAIN_BF16X3
+    if not spec.truncate:
+        flags |= N.FLAG_NO_TRUNCATION
     md = N.MethodDesc(method, scaling_code, spec.gelfand_power,
                       N.PREC_BF16 if precision is Precision.BF16 else N.PREC_FP32, order, steps,
                       co.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), flags, 0)

@@ -415,3 +415,37 @@ def test_graphed_orthogonalize_matches_eager():
     xb = torch.from_numpy(ms).to(DEV)
     gr = GraphedOrthogonalize(xb, U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()), precision="bf16")
     assert torch.equal(gr(xb).clone(), U.orthogonalize(xb, gr.spec, precision="bf16").y)
+
+
+def test_chain_truncation_well_conditioned():
+    """Tall Gaussian (kappa ~ 1.2): the persistent chain stops early and the result
+    stays within the bf16 tolerance of the oracle and within the truncation bound of the full chain."""
+    g = torch.Generator().manual_seed(12)
+    x = torch.randn(65536, 512, generator=g).to(torch.bfloat16).to(DEV)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    res = U.orthogonalize(x, spec, precision="bf16")
+    full = U.orthogonalize(x, U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), truncate=False),
+                           precision="bf16")
+    torch.cuda.synchronize()
+    steps, steps_full = res.info[0]["chain_steps"], full.info[0]["chain_steps"]
+    print(f"chain steps: {steps} (full {steps_full})")
+    assert steps_full == 13 and 0 < steps < 13
+    rows = np.arange(4096)  # row sample of the oracle (the same P applies to every row)
+    ref = O.unso_rows_of_tall(x.double().cpu().numpy(), rows)
+    y = res.y.double().cpu().numpy()
+    yf = full.y.double().cpu().numpy()
+    d = rel(y, yf)
+    r = rel(y[rows], ref)
+    print(f"truncated vs full chain: {d:.2e}; vs oracle rows: {r:.2e}")
+    assert d <= 2.0 ** -12 + 2.0 ** -9  # truncation bound + bf16 output rounding
+    assert r <= TOL["bf16"]
+
+
+def test_chain_truncation_not_taken_when_ill_conditioned():
+    g = torch.Generator().manual_seed(13)
+    x = torch.randn(512, 512, generator=g).to(torch.bfloat16).to(DEV)
+    res = U.orthogonalize(x, U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()), precision="bf16")
+    torch.cuda.synchronize()
+    assert res.info[0]["chain_steps"] == 13
+    ref = O.run(x.double().cpu().numpy(), "unso")["y"]
+    assert rel(res.y.double().cpu().numpy(), ref) <= TOL["bf16"]

@@ -31,7 +31,8 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn(b, w, h, generator=g, device="cuda").to(dt)
     chain = os.environ.get("UNSO_CHAIN")  # e.g. "bf16x3"
-    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), chain=chain)
+    truncate = os.environ.get("UNSO_TRUNCATE", "1") != "0"
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), chain=chain, truncate=truncate)
     U.orthogonalize(x, spec, precision=prec, check=False)
     torch.cuda.synchronize()
     with StageProfiler(reps) as prof:
@@ -42,6 +43,9 @@ def main():
     med = t[len(t) // 2] if len(t) else t
     fl = {"gram": 2.0 * w * h * h * b, "chain": 2.0 * 12 * h ** 3 * b, "apply": 2.0 * w * h * h * b}
     out = {"case": name, "precision": prec, "total_ms": float(med.sum())}
+    info = U.orthogonalize(x, spec, precision=prec, check=True).info
+    if info:
+        out["chain_steps"] = info[0].get("chain_steps")
     for s, v in zip(PROFILE_STAGES, med):
         out[s + "_ms"] = round(float(v), 4)
         if s in fl and v > 0:
