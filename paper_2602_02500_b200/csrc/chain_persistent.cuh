@@ -50,7 +50,8 @@ struct ChainMaps {
 };
 
 struct ChainParams {
-  const float* part;   // split-K Gram partials: part[(s * batch + b) * mat + r * ld + c]
+  const float* part;   // split-K Gram partials: part[(s * batch + b) * part_mat + r * part_ld + c]
+  int64_t part_ld, part_mat;
   int splits;
   int h, nt, tiles_per_mat, batch;  // batch = TOTAL batch (split-K partial layout)
   int b0;                            // first matrix of this launch's chunk
@@ -248,7 +249,8 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       for (int j = 0; j < 32; ++j) g[j] = 0.f;
       if (row_ok) {
         for (int s = 0; s < p.splits; ++s) {
-          const float* src = p.part + (static_cast<int64_t>(s) * p.batch + b) * p.mat + static_cast<int64_t>(gr) * p.ld + gc0;
+          const float* src =
+              p.part + (static_cast<int64_t>(s) * p.batch + b) * p.part_mat + static_cast<int64_t>(gr) * p.part_ld + gc0;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 v = *reinterpret_cast<const float4*>(src + j);

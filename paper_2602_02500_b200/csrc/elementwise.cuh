@@ -21,17 +21,20 @@ constexpr int SCAL_STRIDE = 16;
 
 // ------------------------------------------------------------------ conversion
 // dst[b](r, c) = src[b](r, c) * (scal ? scal[b].inv_s : 1), any dtype -> any dtype.
+// One warp per row (grid-stride over batch x rows), lanes along the columns: one 64-bit division per
+// row instead of three per element.
 __global__ void convert_kernel(const void* __restrict__ src, int sdt, int64_t sld, int64_t sbs, void* __restrict__ dst,
                                int ddt, int64_t dld, int64_t dbs, int64_t rows, int64_t cols, int batch,
                                const double* __restrict__ scal) {
-  const int64_t per = rows * cols;
-  const int64_t total = per * batch;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t b = i / per, rc = i - b * per, r = rc / cols, c = rc - r * cols;
-    double v = load_as_f64(src, b * sbs + r * sld + c, sdt);
-    if (scal) v *= scal[b * SCAL_STRIDE + S_INV_S];
-    store_from_f64(dst, b * dbs + r * dld + c, ddt, v);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t nrows = rows * batch;
+  for (int64_t R = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); R < nrows;
+       R += nwarps) {
+    const int64_t b = R / rows, r = R - b * rows;
+    const double sc = scal ? scal[b * SCAL_STRIDE + S_INV_S] : 1.0;
+    const int64_t so = b * sbs + r * sld, d0 = b * dbs + r * dld;
+    for (int64_t c = lane; c < cols; c += 32) store_from_f64(dst, d0 + c, ddt, load_as_f64(src, so + c, sdt) * sc);
   }
 }
 
@@ -82,10 +85,11 @@ __device__ __forceinline__ void sym_tile_coords(int t, int nt, int& ti, int& tj)
   tj = row + t;
 }
 
-// G[b] = sum_s part[s][b]  (upper values mirrored into the lower triangle)
+// G[b] = sum_s part[s][b]  (upper values mirrored into the lower triangle); G has its own leading
+// dimension / batch stride (the padded workspace layout, or a dense caller buffer).
 template <typename T>
 __global__ void finalize_sum_kernel(const T* __restrict__ part, int splits, int batch, int h, int64_t ld,
-                                    T* __restrict__ G) {
+                                    T* __restrict__ G, int64_t gld, int64_t gbs) {
   __shared__ double tile[32][33];
   const int nt = (h + 31) / 32;
   int ti, tj;
@@ -103,13 +107,13 @@ __global__ void finalize_sum_kernel(const T* __restrict__ part, int splits, int 
     tile[r][tx] = s;
   }
   __syncthreads();
-  T* g = G + static_cast<int64_t>(b) * mat;
+  T* g = G + static_cast<int64_t>(b) * gbs;
   for (int r = ty; r < 32; r += 8) {
     const int gr = ti * 32 + r, gc = tj * 32 + tx;
-    if (gr < h && gc < h) g[static_cast<int64_t>(gr) * ld + gc] = static_cast<T>((ti == tj && r > tx) ? tile[tx][r] : tile[r][tx]);
+    if (gr < h && gc < h) g[static_cast<int64_t>(gr) * gld + gc] = static_cast<T>((ti == tj && r > tx) ? tile[tx][r] : tile[r][tx]);
     if (ti != tj) {
       const int mr = tj * 32 + r, mc = ti * 32 + tx;
-      if (mr < h && mc < h) g[static_cast<int64_t>(mr) * ld + mc] = static_cast<T>(tile[tx][r]);
+      if (mr < h && mc < h) g[static_cast<int64_t>(mr) * gld + mc] = static_cast<T>(tile[tx][r]);
     }
   }
 }

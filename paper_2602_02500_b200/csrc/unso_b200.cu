@@ -568,12 +568,15 @@ static int32_t gram_simt(const Problem& p, const void* x, int dt, int64_t ld, in
   return UNSO_OK;
 }
 
+// Split-K partials -> symmetric G, in the padded workspace layout (gld = 0) or a dense (gld, gbs) buffer.
 template <typename T>
-static int32_t finalize_gram(const Problem& p, const Plan& pl, void* ws, int splits, T* G, cudaStream_t st) {
+static int32_t finalize_gram(const Problem& p, const Plan& pl, void* ws, int splits, T* G, cudaStream_t st,
+                             int64_t gld = 0, int64_t gbs = 0) {
   const int nt = static_cast<int>((p.h + 31) / 32);
   dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
   finalize_sum_kernel<T><<<grid, 256, 0, st>>>(at<T>(ws, pl.part), splits, static_cast<int>(p.batch),
-                                                static_cast<int>(p.h), pl.ldc, G);
+                                                static_cast<int>(p.h), pl.ldc, G, gld ? gld : pl.ldc,
+                                                gld ? gbs : pl.hh);
   UNSO_CHECK_LAUNCH();
   return UNSO_OK;
 }
@@ -981,7 +984,7 @@ static bool chain_persistent_fits(const Problem& p) {
 }
 
 static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
-                                           int32_t* status, cudaStream_t st) {
+                                           int64_t part_ld, int64_t part_mat, int32_t* status, cudaStream_t st) {
   const int h = static_cast<int>(p.h);
   ChainMaps maps;
   for (int buf = 0; buf < 2; ++buf) {
@@ -995,6 +998,8 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
   ChainParams cp;
   std::memset(&cp, 0, sizeof(cp));
   cp.part = part;
+  cp.part_ld = part_ld;
+  cp.part_mat = part_mat;
   cp.splits = splits;
   cp.h = h;
   cp.nt = (h + 127) / 128;
@@ -1074,12 +1079,24 @@ static Bf16Route bf16_route(const Problem& p) {
 // Everything after the Gram: scale, chain, P, apply.  `split_done`: K1 already wrote G as
 // bf16 hi/lo + norm partials (glue-free route with one split); otherwise `part` holds split-K
 // fp32 partials (or the reduced Gram with splits == 1).
+// `dense_ld` > 0: `part` is one dense reduced Gram per matrix (leading dimension dense_ld, used in
+// place by the persistent route), otherwise it is in the padded workspace layout.
 static int32_t unso_bf16_after_gram(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
                                     int64_t bsx, const float* part, int splits, bool split_done, void* y,
-                                    int32_t* status, cudaStream_t st) {
+                                    int32_t* status, cudaStream_t st, int64_t dense_ld = 0) {
   const Bf16Route route = bf16_route(p);
+  if (dense_ld > 0 && route != ROUTE_PERSISTENT) {  // the other routes read the padded layout
+    float* G = at<float>(ws, pl.G);
+    convert_kernel<<<grid_for(p.batch * p.h * p.h), 256, 0, st>>>(part, DT_F32, dense_ld, dense_ld * p.h, G, DT_F32,
+                                                                  pl.ldc, pl.hh, p.h, p.h, static_cast<int>(p.batch),
+                                                                  nullptr);
+    UNSO_CHECK_LAUNCH();
+    part = G;
+    dense_ld = 0;
+  }
   if (route == ROUTE_PERSISTENT) {
-    UNSO_TRY(scale_chain_bf16_persistent(p, pl, ws, part, splits, status, st));
+    UNSO_TRY(scale_chain_bf16_persistent(p, pl, ws, part, splits, dense_ld > 0 ? dense_ld : pl.ldc,
+                                         dense_ld > 0 ? dense_ld * p.h : pl.hh, status, st));
   } else if (route == ROUTE_GLUE_FREE) {
     int nnorm;
     if (split_done) {
@@ -1101,7 +1118,7 @@ static int32_t unso_bf16_after_gram(const Problem& p, const Plan& pl, void* ws, 
       const int nt = static_cast<int>((p.h + 31) / 32);
       dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));
       finalize_sum_kernel<float><<<grid, 256, 0, st>>>(part, splits, static_cast<int>(p.batch), static_cast<int>(p.h),
-                                                       pl.ldc, G);
+                                                       pl.ldc, G, pl.ldc, pl.hh);
       UNSO_CHECK_LAUNCH();
     }
     UNSO_TRY(scale_chain_bf16_multi(p, pl, ws, G, status, st));
@@ -1438,23 +1455,13 @@ int32_t unso_gram(const unso_matrix_desc* x, const void* x_ptr, void* g_ptr, con
   const int64_t h = p.h;
   if (p.prec == UNSO_PREC_FP32) {
     UNSO_TRY(gram_simt(p, x_ptr, p.dt, p.ld, p.bs, pl, workspace, pl.splits, st));
-    UNSO_TRY(finalize_gram<double>(p, pl, workspace, pl.splits, at<double>(workspace, pl.G), st));
-    convert_kernel<<<grid_for(p.batch * h * h), 256, 0, st>>>(at<double>(workspace, pl.G), DT_F64, pl.ldc, pl.hh,
-                                                              g_ptr, DT_F64, h, h * h, h, h,
-                                                              static_cast<int>(p.batch), nullptr);
-    UNSO_CHECK_LAUNCH();
-    return UNSO_OK;
+    return finalize_gram<double>(p, pl, workspace, pl.splits, static_cast<double*>(g_ptr), st, h, h * h);
   }
   const __nv_bfloat16* xb;
   int64_t ldx, bsx;
   UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
   UNSO_TRY(gram_bf16(p, pl, workspace, xb, ldx, bsx, st));
-  UNSO_TRY(finalize_gram<float>(p, pl, workspace, pl.splits, at<float>(workspace, pl.G), st));
-  convert_kernel<<<grid_for(p.batch * h * h), 256, 0, st>>>(at<float>(workspace, pl.G), DT_F32, pl.ldc, pl.hh, g_ptr,
-                                                            DT_F32, h, h * h, h, h, static_cast<int>(p.batch),
-                                                            nullptr);
-  UNSO_CHECK_LAUNCH();
-  return UNSO_OK;
+  return finalize_gram<float>(p, pl, workspace, pl.splits, static_cast<float*>(g_ptr), st, h, h * h);
 }
 
 int32_t unso_orthogonalize_from_gram(const unso_matrix_desc* x, const void* x_ptr, const void* g_ptr, void* y_ptr,
@@ -1477,12 +1484,15 @@ int32_t unso_orthogonalize_from_gram(const unso_matrix_desc* x, const void* x_pt
     UNSO_CHECK_LAUNCH();
     return unso_fp32_from_G(p, pl, workspace, x_ptr, at<double>(workspace, pl.G), y_ptr, d_status, st);
   }
-  convert_kernel<<<grid_for(p.batch * h * h), 256, 0, st>>>(g_ptr, DT_F32, h, h * h, at<float>(workspace, pl.G), DT_F32,
-                                                            pl.ldc, pl.hh, h, h, static_cast<int>(p.batch), nullptr);
-  UNSO_CHECK_LAUNCH();
   const __nv_bfloat16* xb;
   int64_t ldx, bsx;
   UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
+  if (h % 4 == 0 && (reinterpret_cast<uintptr_t>(g_ptr) & 15) == 0)  // dense G read in place (float4 rows)
+    return unso_bf16_after_gram(p, pl, workspace, xb, ldx, bsx, static_cast<const float*>(g_ptr), 1, false, y_ptr,
+                                d_status, st, h);
+  convert_kernel<<<grid_for(p.batch * h * h), 256, 0, st>>>(g_ptr, DT_F32, h, h * h, at<float>(workspace, pl.G), DT_F32,
+                                                            pl.ldc, pl.hh, h, h, static_cast<int>(p.batch), nullptr);
+  UNSO_CHECK_LAUNCH();
   return unso_bf16_after_gram(p, pl, workspace, xb, ldx, bsx, at<float>(workspace, pl.G), 1, false, y_ptr, d_status,
                               st);
 }

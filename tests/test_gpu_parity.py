@@ -449,3 +449,27 @@ def test_chain_truncation_not_taken_when_ill_conditioned():
     assert res.info[0]["chain_steps"] == 13
     ref = O.run(x.double().cpu().numpy(), "unso")["y"]
     assert rel(res.y.double().cpu().numpy(), ref) <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("precision,h", [("bf16", 512), ("bf16", 2048), ("fp32", 256)])
+def test_row_sharded_native_stages_match_unsharded(precision, h):
+    """The cfg4 scheme on one GPU: per-shard Gram (unso_gram), the sum of the shard Grams standing in for
+    the NCCL all-reduce, then unso_orthogonalize_from_gram per shard; the concatenated rows equal the
+    unsharded orthogonalize and the oracle (row sample)."""
+    from paper_2602_02500_b200.distributed import native_finish, native_gram, row_shard_bounds
+    g = torch.Generator().manual_seed(14 + h)
+    w = 16 * h
+    x = torch.randn(w, h, generator=g).to(torch.bfloat16 if precision == "bf16" else torch.float32).to(DEV)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    world = 4
+    shards = [x[slice(*row_shard_bounds(w, world, r))] for r in range(world)]
+    gsum = sum(native_gram(s, spec, precision) for s in shards)
+    ys = [native_finish(s, gsum.clone(), spec, precision)[0] for s in shards]
+    y = torch.cat(ys)
+    full = U.orthogonalize(x, spec, precision=precision).y
+    torch.cuda.synchronize()
+    rows = np.arange(0, w, 7)[:2048]
+    ref = O.unso_rows_of_tall(x.double().cpu().numpy(), rows)
+    tol = TOL[precision] + (2.0 ** -9 if precision == "bf16" else 0.0)
+    assert rel(y.double().cpu().numpy()[rows], ref) <= tol
+    assert rel(y.double().cpu().numpy(), full.double().cpu().numpy()) <= (5e-3 if precision == "bf16" else 1e-6)
