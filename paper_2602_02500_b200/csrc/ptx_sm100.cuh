@@ -182,6 +182,11 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
+// Generic-proxy shared-memory writes later read by tcgen05.mma / TMA (async proxy).
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- grid-scope sync helpers
 // Generic-proxy global writes consumed later by TMA (async proxy) in other CTAs.
 __device__ __forceinline__ void fence_proxy_async_global() {

@@ -26,6 +26,7 @@
 #include "simt_gemm.cuh"
 #include "umma_gemm.cuh"
 #include "chain_persistent.cuh"
+#include "chain_small.cuh"
 #include "umma2_gemm.cuh"
 #include "chain_pair.cuh"
 #include "ns_bf16.cuh"
@@ -983,18 +984,10 @@ static bool chain_persistent_fits(const Problem& p) {
   return (p.batch + per - 1) / per <= 4;
 }
 
-static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
-                                           int64_t part_ld, int64_t part_mat, int32_t* status, cudaStream_t st) {
+// Parameters shared by the on-chip chain kernels (chain_persistent.cuh, chain_small.cuh).
+static ChainParams chain_params(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
+                                int64_t part_ld, int64_t part_mat, int32_t* status) {
   const int h = static_cast<int>(p.h);
-  ChainMaps maps;
-  for (int buf = 0; buf < 2; ++buf) {
-    const void* base[2] = {at<__nv_bfloat16>(ws, pl.Chi[buf]), at<__nv_bfloat16>(ws, pl.Clo[buf])};
-    for (int hl = 0; hl < 2; ++hl) {
-      if (!umma_make_kmajor_map(&maps.m[buf][hl][0], base[hl], h, h, pl.ldc, p.batch, pl.hh, 128) ||
-          !umma_make_mnmajor_map(&maps.m[buf][hl][1], base[hl], h, h, pl.ldc, p.batch, pl.hh))
-        return UNSO_ERR_CUDA;
-    }
-  }
   ChainParams cp;
   std::memset(&cp, 0, sizeof(cp));
   cp.part = part;
@@ -1039,6 +1032,22 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
     cp.tail[k] = static_cast<float>(t);
     cp.tail_abs[k] = static_cast<float>(ta);
   }
+  return cp;
+}
+
+static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
+                                           int64_t part_ld, int64_t part_mat, int32_t* status, cudaStream_t st) {
+  const int h = static_cast<int>(p.h);
+  ChainMaps maps;
+  for (int buf = 0; buf < 2; ++buf) {
+    const void* base[2] = {at<__nv_bfloat16>(ws, pl.Chi[buf]), at<__nv_bfloat16>(ws, pl.Clo[buf])};
+    for (int hl = 0; hl < 2; ++hl) {
+      if (!umma_make_kmajor_map(&maps.m[buf][hl][0], base[hl], h, h, pl.ldc, p.batch, pl.hh, 128) ||
+          !umma_make_mnmajor_map(&maps.m[buf][hl][1], base[hl], h, h, pl.ldc, p.batch, pl.hh))
+        return UNSO_ERR_CUDA;
+    }
+  }
+  ChainParams cp = chain_params(p, pl, ws, part, splits, part_ld, part_mat, status);
   prof_mark(3, st);
   // co-resident chunks of the batch, one cooperative launch each (same stream: the barrier word
   // and per-tile buffers are reused after the previous chunk completes)
@@ -1068,9 +1077,35 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
   return UNSO_OK;
 }
 
+// h <= 128: one CTA per matrix, the chain entirely on chip (chain_small.cuh).
+static bool chain_small_fits(const Problem& p) {
+  return p.h <= 128 && p.order >= 1 && p.order <= CHAIN_MAX_ORDER && p.scaling != UNSO_SCALING_GELFAND &&
+         std::getenv("UNSO_NO_SMALL_CHAIN") == nullptr;
+}
+
+static int32_t scale_chain_bf16_small(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
+                                      int64_t part_ld, int64_t part_mat, int32_t* status, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(chain_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CS_SMEM) != cudaSuccess)
+      return UNSO_ERR_CUDA;
+    configured = true;
+  }
+  ChainParams cp = chain_params(p, pl, ws, part, splits, part_ld, part_mat, status);
+  prof_mark(3, st);
+  cp.b0 = 0;
+  chain_small_kernel<<<static_cast<unsigned>(p.batch), CS_THREADS, CS_SMEM, st>>>(cp);
+  UNSO_CHECK_LAUNCH();
+  ++g_launches;
+  prof_mark(4, st);
+  prof_mark(5, st);
+  return UNSO_OK;
+}
+
 // Which scale+chain implementation a BF16 UNSO problem takes.
-enum Bf16Route { ROUTE_PERSISTENT, ROUTE_GLUE_FREE, ROUTE_LEGACY };
+enum Bf16Route { ROUTE_SMALL, ROUTE_PERSISTENT, ROUTE_GLUE_FREE, ROUTE_LEGACY };
 static Bf16Route bf16_route(const Problem& p) {
+  if (chain_small_fits(p)) return ROUTE_SMALL;
   if (chain_persistent_fits(p)) return ROUTE_PERSISTENT;
   if (use_pair_engine() && p.order >= 2 && p.scaling != UNSO_SCALING_GELFAND) return ROUTE_GLUE_FREE;
   return ROUTE_LEGACY;
@@ -1085,7 +1120,7 @@ static int32_t unso_bf16_after_gram(const Problem& p, const Plan& pl, void* ws, 
                                     int64_t bsx, const float* part, int splits, bool split_done, void* y,
                                     int32_t* status, cudaStream_t st, int64_t dense_ld = 0) {
   const Bf16Route route = bf16_route(p);
-  if (dense_ld > 0 && route != ROUTE_PERSISTENT) {  // the other routes read the padded layout
+  if (dense_ld > 0 && route != ROUTE_PERSISTENT && route != ROUTE_SMALL) {  // the others read the padded layout
     float* G = at<float>(ws, pl.G);
     convert_kernel<<<grid_for(p.batch * p.h * p.h), 256, 0, st>>>(part, DT_F32, dense_ld, dense_ld * p.h, G, DT_F32,
                                                                   pl.ldc, pl.hh, p.h, p.h, static_cast<int>(p.batch),
@@ -1094,7 +1129,10 @@ static int32_t unso_bf16_after_gram(const Problem& p, const Plan& pl, void* ws, 
     part = G;
     dense_ld = 0;
   }
-  if (route == ROUTE_PERSISTENT) {
+  if (route == ROUTE_SMALL) {
+    UNSO_TRY(scale_chain_bf16_small(p, pl, ws, part, splits, dense_ld > 0 ? dense_ld : pl.ldc,
+                                    dense_ld > 0 ? dense_ld * p.h : pl.hh, status, st));
+  } else if (route == ROUTE_PERSISTENT) {
     UNSO_TRY(scale_chain_bf16_persistent(p, pl, ws, part, splits, dense_ld > 0 ? dense_ld : pl.ldc,
                                          dense_ld > 0 ? dense_ld * p.h : pl.hh, status, st));
   } else if (route == ROUTE_GLUE_FREE) {
