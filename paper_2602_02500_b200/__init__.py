@@ -3,7 +3,7 @@
 Drop-in for the reference package's orthogonalization entry points
 (``unso.ortho`` / ``unso.scalarpoly``, re-exported like unso/__init__.py:4-100),
 operating on CUDA tensors.  All matrix arithmetic runs in the in-tree CUDA
-library ``libunso_b200.so`` (sm_100a: tcgen05/TMEM/TMA + fp64 DFMA parity path);
+library ``libunso_b200.so`` (sm_100a: tcgen05/TMEM/TMA + fp64 DMMA parity path);
 there is no CPU fallback.
 """
 
