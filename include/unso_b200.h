@@ -39,7 +39,7 @@ typedef enum unso_status {
 typedef enum unso_dtype { UNSO_DTYPE_F32 = 0, UNSO_DTYPE_BF16 = 1, UNSO_DTYPE_F64 = 2 } unso_dtype;
 
 /* Arithmetic recipe.
- *   FP32: fp32 I/O, fp64-grade Gram + squaring chain (DFMA), fp64-accumulated apply;
+ *   FP32: fp32 I/O, fp64-grade Gram + squaring chain (fp64 tensor cores, DMMA), fp64-accumulated apply;
  *         parity <= 1e-5 against the fp64 reference on every config.
  *   BF16: tcgen05 tensor cores, bf16 operands / f32 accumulation; the h x h chain in
  *         C-form with bf16x3 split products, the apply with a bf16x2 split P;
