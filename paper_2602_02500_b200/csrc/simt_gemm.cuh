@@ -15,6 +15,7 @@
 // a fragment load hit all banks in the minimum two wavefronts.
 #pragma once
 #include "common.cuh"
+#include "ptx_sm100.cuh"
 
 namespace unso {
 
@@ -90,7 +91,7 @@ __device__ __forceinline__ void simt_stash(double (*S)[SIMT_BM + SIMT_PAD], cons
 }
 
 template <class Epi>
-__global__ void __launch_bounds__(128) simt_gemm_kernel(SimtOperand A, SimtOperand B, int M, int N, int K, int syrk,
+__global__ void __launch_bounds__(128, 4) simt_gemm_kernel(SimtOperand A, SimtOperand B, int M, int N, int K, int syrk,
                                                         int tiles_m, int tiles_n, int splits, Epi epi) {
   __shared__ __align__(16) double As[2][SIMT_BK][SIMT_BM + SIMT_PAD];
   __shared__ __align__(16) double Bs[2][SIMT_BK][SIMT_BN + SIMT_PAD];
@@ -163,12 +164,179 @@ __global__ void __launch_bounds__(128) simt_gemm_kernel(SimtOperand A, SimtOpera
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Pipelined variant (operands 16-byte aligned): raw-dtype tiles streamed into shared memory by
+// cp.async (3 stages, zero-filled edges), widened to f64 at the fragment load.  No register
+// staging, so 3-4 CTAs (12-16 warps) fit per SM to hide the DMMA and load latencies.
+// Padded strides keep the fragment loads conflict-free (K-major tile [m][16+pk], MN-major
+// [k][64+pm]); every row stride is a multiple of 16 bytes for the cp.async destinations.
+template <int DT> struct DmmaLayout {
+  static constexpr int E = DT == DT_F64 ? 8 : (DT == DT_F32 ? 4 : 2);
+  static constexpr int KS = SIMT_BK + (DT == DT_BF16 ? 8 : 4);   // K-major row stride (elements)
+  static constexpr int MS = SIMT_BM + (DT == DT_F64 ? 4 : 8);    // MN-major row stride (elements)
+  static constexpr int BYTES = (64 * KS > SIMT_BK * MS ? 64 * KS : SIMT_BK * MS) * E;
+  static constexpr int EPC = 16 / E;                              // elements per 16-byte chunk
+};
+constexpr int DMMA_STAGES = 3;
+
+template <int DT>
+__device__ __forceinline__ double dmma_lds(const uint8_t* base, int idx) {
+  if (DT == DT_F64) return reinterpret_cast<const double*>(base)[idx];
+  if (DT == DT_F32) return static_cast<double>(reinterpret_cast<const float*>(base)[idx]);
+  return static_cast<double>(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[idx]));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes) : "memory");
+}
+
+// 64 rows x 16 k of one operand, tile origin (r0, k0), into one stage buffer
+template <int DT>
+__device__ __forceinline__ void dmma_issue(uint8_t* dst, const char* base, const SimtOperand& op, int r0, int k0, int R,
+                                           int K) {
+  using L = DmmaLayout<DT>;
+  if (op.kmajor) {
+    constexpr int CPR = SIMT_BK / L::EPC;  // chunks per tile row
+    for (int c = threadIdx.x; c < 64 * CPR; c += 128) {
+      const int row = c / CPR, kc = (c % CPR) * L::EPC;
+      const int gr = r0 + row, gk = k0 + kc;
+      const int valid = (gr < R && gk < K) ? min(L::EPC, K - gk) : 0;
+      const char* src = base + (static_cast<int64_t>(valid ? gr : 0) * op.ld + (valid ? gk : 0)) * L::E;
+      cp_async16(dst + (row * L::KS + kc) * L::E, src, valid * L::E);
+    }
+  } else {
+    constexpr int CPR = SIMT_BM / L::EPC;
+    for (int c = threadIdx.x; c < SIMT_BK * CPR; c += 128) {
+      const int row = c / CPR, mc = (c % CPR) * L::EPC;
+      const int gk = k0 + row, gm = r0 + mc;
+      const int valid = (gk < K && gm < R) ? min(L::EPC, R - gm) : 0;
+      const char* src = base + (static_cast<int64_t>(valid ? gk : 0) * op.ld + (valid ? gm : 0)) * L::E;
+      cp_async16(dst + (row * L::MS + mc) * L::E, src, valid * L::E);
+    }
+  }
+}
+
+template <int DTA, int DTB, class Epi>
+__global__ void __launch_bounds__(128, 3) dmma_gemm_kernel(SimtOperand A, SimtOperand B, int M, int N, int K, int syrk,
+                                                           int tiles_m, int tiles_n, int splits, Epi epi) {
+  using LA = DmmaLayout<DTA>;
+  using LB = DmmaLayout<DTB>;
+  constexpr int STAGE = LA::BYTES + LB::BYTES;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp >> 1, wn = warp & 1, gid = lane >> 2, tig = lane & 3;
+  const int split = blockIdx.y, b = blockIdx.z;
+  int tm, tn;
+  simt_tile_coords(blockIdx.x, tiles_m, tiles_n, syrk, tm, tn);
+  const int m0 = tm * SIMT_BM, n0 = tn * SIMT_BN;
+  const int ktiles = (K + SIMT_BK - 1) / SIMT_BK;
+  const int kt0 = static_cast<int>(static_cast<int64_t>(split) * ktiles / splits);
+  const int kt1 = static_cast<int>(static_cast<int64_t>(split + 1) * ktiles / splits);
+  const char* pa = static_cast<const char*>(A.p) + static_cast<int64_t>(b) * A.bstride * LA::E;
+  const char* pb = static_cast<const char*>(B.p) + static_cast<int64_t>(b) * B.bstride * LB::E;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = kt1 - kt0;
+#pragma unroll
+  for (int s = 0; s < DMMA_STAGES - 1; ++s) {
+    if (s < nk) {
+      dmma_issue<DTA>(dsm + s * STAGE, pa, A, m0, (kt0 + s) * SIMT_BK, M, K);
+      dmma_issue<DTB>(dsm + s * STAGE + LA::BYTES, pb, B, n0, (kt0 + s) * SIMT_BK, N, K);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int it = 0; it < nk; ++it) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(DMMA_STAGES - 2) : "memory");
+    __syncthreads();  // stage it landed for every thread; stage it-1 is free to refill
+    const int nxt = it + DMMA_STAGES - 1;
+    if (nxt < nk) {
+      uint8_t* st = dsm + (nxt % DMMA_STAGES) * STAGE;
+      dmma_issue<DTA>(st, pa, A, m0, (kt0 + nxt) * SIMT_BK, M, K);
+      dmma_issue<DTB>(st + LA::BYTES, pb, B, n0, (kt0 + nxt) * SIMT_BK, N, K);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const uint8_t* sa = dsm + (it % DMMA_STAGES) * STAGE;
+    const uint8_t* sb = sa + LA::BYTES;
+#pragma unroll
+    for (int kk = 0; kk < SIMT_BK / 4; ++kk) {
+      const int k = kk * 4 + tig;
+      double a[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = wm * 32 + i * 8 + gid;
+        a[i] = A.kmajor ? dmma_lds<DTA>(sa, m * LA::KS + k) : dmma_lds<DTA>(sa, k * LA::MS + m);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = wn * 32 + j * 8 + gid;
+        bv[j] = B.kmajor ? dmma_lds<DTB>(sb, n * LB::KS + k) : dmma_lds<DTB>(sb, k * LB::MS + n);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_884(acc[i][j], a[i], bv[j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + wm * 32 + i * 8 + gid;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = n0 + wn * 32 + j * 8 + 2 * tig + e;
+        if (n >= N) continue;
+        if (syrk && n < m) continue;
+        epi(b, split, m, n, acc[i][j][e]);
+      }
+    }
+  }
+}
+
+template <int DTA, int DTB, class Epi>
+inline cudaError_t launch_dmma(const SimtOperand& A, const SimtOperand& B, int M, int N, int K, int batch, bool syrk,
+                               int splits, const Epi& epi, cudaStream_t stream, int tm, int tn, int tiles) {
+  constexpr int smem = DMMA_STAGES * (DmmaLayout<DTA>::BYTES + DmmaLayout<DTB>::BYTES);
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(dmma_gemm_kernel<DTA, DTB, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(tiles, splits, batch);
+  dmma_gemm_kernel<DTA, DTB, Epi><<<grid, 128, smem, stream>>>(A, B, M, N, K, syrk ? 1 : 0, tm, tn, splits, epi);
+  return cudaGetLastError();
+}
+
+inline bool dmma_aligned(const SimtOperand& op) {
+  const int e = dtype_size(op.dtype);
+  return (reinterpret_cast<uintptr_t>(op.p) & 15) == 0 && (op.ld * e) % 16 == 0 && (op.bstride * e) % 16 == 0;
+}
+
 template <class Epi>
 inline cudaError_t launch_simt_gemm(const SimtOperand& A, const SimtOperand& B, int M, int N, int K, int batch,
                                     bool syrk, int splits, const Epi& epi, cudaStream_t stream) {
   const int tm = (M + SIMT_BM - 1) / SIMT_BM, tn = (N + SIMT_BN - 1) / SIMT_BN;
   const int tiles = syrk ? tm * (tm + 1) / 2 : tm * tn;
   if (syrk && tm != tn) return cudaErrorInvalidValue;
+  if (dmma_aligned(A) && dmma_aligned(B)) {
+    const int da = A.dtype, db = B.dtype;
+    if (da == DT_F64 && db == DT_F64) return launch_dmma<DT_F64, DT_F64>(A, B, M, N, K, batch, syrk, splits, epi, stream, tm, tn, tiles);
+    if (da == DT_F32 && db == DT_F32) return launch_dmma<DT_F32, DT_F32>(A, B, M, N, K, batch, syrk, splits, epi, stream, tm, tn, tiles);
+    if (da == DT_BF16 && db == DT_BF16) return launch_dmma<DT_BF16, DT_BF16>(A, B, M, N, K, batch, syrk, splits, epi, stream, tm, tn, tiles);
+    if (da == DT_F32 && db == DT_F64) return launch_dmma<DT_F32, DT_F64>(A, B, M, N, K, batch, syrk, splits, epi, stream, tm, tn, tiles);
+    if (da == DT_F64 && db == DT_F32) return launch_dmma<DT_F64, DT_F32>(A, B, M, N, K, batch, syrk, splits, epi, stream, tm, tn, tiles);
+    if (da == DT_BF16 && db == DT_F64) return launch_dmma<DT_BF16, DT_F64>(A, B, M, N, K, batch, syrk, splits, epi, stream, tm, tn, tiles);
+    if (da == DT_F64 && db == DT_BF16) return launch_dmma<DT_F64, DT_BF16>(A, B, M, N, K, batch, syrk, splits, epi, stream, tm, tn, tiles);
+  }
   dim3 grid(tiles, splits, batch);
   simt_gemm_kernel<Epi><<<grid, 128, 0, stream>>>(A, B, M, N, K, syrk ? 1 : 0, tm, tn, splits, epi);
   return cudaGetLastError();
