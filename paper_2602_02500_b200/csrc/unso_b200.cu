@@ -27,6 +27,7 @@
 #include "umma_gemm.cuh"
 #include "chain_persistent.cuh"
 #include "chain_small.cuh"
+#include "chain_f64.cuh"
 #include "umma2_gemm.cuh"
 #include "chain_pair.cuh"
 #include "ns_bf16.cuh"
@@ -519,6 +520,7 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       pl.C[1] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
       pl.P = take(pl, static_cast<size_t>(B * pl.hh) * 8);
       pl.Pout = take(pl, static_cast<size_t>(B * pl.hh) * 8);
+      pl.gbar = take(pl, CHAIN_ROUNDS * 8);  // chain_f64_kernel rounds
     }
   } else if (bf) {
     // NS in BF16: fp32 state ping-pong + bf16 operand copy (always), G hi/lo, operator B (P), B hi/lo
@@ -628,6 +630,68 @@ static int scal_mode(int scaling) {
 }
 
 // ---------------------------------------------------------------- UNSO, FP32 precision
+// h <= 256: all squarings in one cooperative launch per co-resident batch chunk (chain_f64.cuh).
+// Returns false when the problem does not qualify (the caller then runs the per-step launches).
+static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, double alpha, cudaStream_t st) {
+  if (p.h > CF_MAX_H || p.order < 2 || p.order > CHAIN_MAX_ORDER || std::getenv("UNSO_NO_F64_CHAIN")) return false;
+  (void)alpha;
+  const int h = static_cast<int>(p.h);
+  const int K16 = (h + 15) & ~15;
+  const int smem = 2 * CF_TILE * (K16 + 4) * 8;
+  static int configured_smem = 0;
+  if (smem > configured_smem) {
+    if (cudaFuncSetAttribute(chain_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * CF_TILE * (CF_MAX_H + 4) * 8) !=
+        cudaSuccess)
+      return false;
+    configured_smem = 2 * CF_TILE * (CF_MAX_H + 4) * 8;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_f64_kernel, 128, smem) != cudaSuccess || per_sm < 1)
+    return false;
+  ChainF64Params cp;
+  std::memset(&cp, 0, sizeof(cp));
+  cp.C[0] = at<double>(ws, pl.C[0]);
+  cp.C[1] = at<double>(ws, pl.C[1]);
+  cp.P = at<double>(ws, pl.P);
+  cp.ld = pl.ldc;
+  cp.mat = pl.hh;
+  cp.h = h;
+  cp.nt = (h + CF_TILE - 1) / CF_TILE;
+  cp.tiles_per_mat = cp.nt * (cp.nt + 1) / 2;
+  cp.order = p.order;
+  cp.gbar = at<unsigned long long>(ws, pl.gbar);
+  cp.scal = at<double>(ws, pl.scal);
+  cp.trunc_tau = (p.flags & UNSO_FLAG_NO_TRUNCATION) ? 0.0 : std::ldexp(1.0, -30);
+  for (int k = 0; k < p.order; ++k) cp.coef[k] = p.co[k];
+  for (int k = 0; k <= p.order && k < CHAIN_MAX_ORDER; ++k) {
+    for (int j = k + 1; j <= p.order; ++j) {
+      cp.tail[k] += p.co[j - 1];
+      cp.tail_abs[k] += std::fabs(p.co[j - 1]);
+    }
+  }
+  const int cap = std::min(per_sm * device_sm_count(), CF_MAX_GRID);
+  if (cap < cp.tiles_per_mat) return false;
+  const int per = cap / cp.tiles_per_mat;
+  for (int b0 = 0; b0 < static_cast<int>(p.batch); b0 += per) {
+    const int nb = std::min(per, static_cast<int>(p.batch) - b0);
+    cp.b0 = b0;
+    if (cudaMemsetAsync(cp.gbar, 0, CHAIN_ROUNDS * sizeof(unsigned long long), st) != cudaSuccess) return false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(cp.tiles_per_mat * nb));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, chain_f64_kernel, cp) != cudaSuccess) return false;
+    ++g_launches;
+  }
+  return true;
+}
+
 static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, const void* x, const double* G, void* y,
                                 int32_t* status, cudaStream_t st) {
   UNSO_TRY(norms_and_scalars<double>(p, pl, ws, G, scal_mode(p.scaling), status, st));
@@ -643,6 +707,9 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
     UNSO_CHECK_LAUNCH();
   }
   prof_mark(3, st);
+  if (chain_f64_persistent(p, pl, ws, alpha, st)) {
+    prof_mark(4, st);
+  } else {
   int cur = 0;
   for (int k = 1; k < N; ++k) {  // produces C_{k+1}
     SimtOperand C{at<double>(ws, pl.C[cur]), pl.ldc, pl.hh, DT_F64, 1};
@@ -657,6 +724,7 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
     cur ^= 1;
   }
   prof_mark(4, st);
+  }
   {
     const int nt = (h + 31) / 32;
     dim3 grid(nt * (nt + 1) / 2, static_cast<unsigned>(p.batch));

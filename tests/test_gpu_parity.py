@@ -473,3 +473,23 @@ def test_row_sharded_native_stages_match_unsharded(precision, h):
     tol = TOL[precision] + (2.0 ** -9 if precision == "bf16" else 0.0)
     assert rel(y.double().cpu().numpy()[rows], ref) <= tol
     assert rel(y.double().cpu().numpy(), full.double().cpu().numpy()) <= (5e-3 if precision == "bf16" else 1e-6)
+
+
+@pytest.mark.parametrize("h", [128, 256])
+def test_fp32_persistent_chain_truncation(h):
+    """fp32 mode, h <= 256: one cooperative launch runs the fp64 chain; a well-conditioned input
+    stops early (dropped terms <= 2^-30 relative) and stays within 1e-5 of the oracle."""
+    g = torch.Generator().manual_seed(40 + h)
+    x = torch.randn(64 * h, h, generator=g, dtype=torch.float64).float().to(DEV)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    res = U.orthogonalize(x, spec, precision="fp32")
+    full = U.orthogonalize(x, U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), truncate=False),
+                           precision="fp32")
+    torch.cuda.synchronize()
+    steps = res.info[0]["chain_steps"]
+    print(f"h={h}: fp64 chain steps {steps} (full {full.info[0]['chain_steps']})")
+    assert 0 < steps < 13 and full.info[0]["chain_steps"] == 13
+    rows = np.arange(0, 64 * h, 5)
+    ref = O.unso_rows_of_tall(x.double().cpu().numpy(), rows)
+    assert rel(res.y.double().cpu().numpy()[rows], ref) <= TOL["fp32"]
+    assert rel(res.y.double().cpu().numpy(), full.y.double().cpu().numpy()) <= 1e-7
