@@ -1173,6 +1173,11 @@ static int32_t scale_chain_bf16_small(const Problem& p, const Plan& pl, void* ws
 // Which scale+chain implementation a BF16 UNSO problem takes.
 enum Bf16Route { ROUTE_SMALL, ROUTE_PERSISTENT, ROUTE_GLUE_FREE, ROUTE_LEGACY };
 static Bf16Route bf16_route(const Problem& p) {
+  if (const char* f = std::getenv("UNSO_BF16_ROUTE")) {  // developer override (A/B timing)
+    if (!std::strcmp(f, "glue") && use_pair_engine() && p.order >= 2 && p.scaling != UNSO_SCALING_GELFAND)
+      return ROUTE_GLUE_FREE;
+    if (!std::strcmp(f, "persistent") && chain_persistent_fits(p)) return ROUTE_PERSISTENT;
+  }
   if (chain_small_fits(p)) return ROUTE_SMALL;
   if (chain_persistent_fits(p)) return ROUTE_PERSISTENT;
   if (use_pair_engine() && p.order >= 2 && p.scaling != UNSO_SCALING_GELFAND) return ROUTE_GLUE_FREE;
