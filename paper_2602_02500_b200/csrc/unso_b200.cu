@@ -263,34 +263,36 @@ struct UEpiOut {
   // All indexing below is compile-time (fully unrolled, predicated tails): the 32-value chunk
   // stays in registers (a dynamic index would spill it to local memory, ~18 GB of L1 traffic
   // per cfg4 apply in round-1 ncu).
+  __device__ __forceinline__ void add_shift(int b, int row, int col0, float (&v)[32]) const {
+    if (!x) return;
+    const float sh = static_cast<float>(scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_SHIFT]);
+    if (sh == 0.0f) return;
+    const __nv_bfloat16* xr = x + static_cast<int64_t>(b) * xbs + static_cast<int64_t>(row) * xld + col0;
+    if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        const uint4 t = *reinterpret_cast<const uint4*>(xr + j);
+        const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[j + 2 * q] = fmaf(sh, bf16_lo_to_f32(w[q]), v[j + 2 * q]);
+          v[j + 2 * q + 1] = fmaf(sh, bf16_hi_to_f32(w[q]), v[j + 2 * q + 1]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < N) v[j] = fmaf(sh, __bfloat162float(xr[j]), v[j]);
+    }
+  }
+
   __device__ __forceinline__ void operator()(int b, int, int row, int col0, const float (&vin)[32]) const {
     if (row >= M) return;
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = vin[j];
     const bool full = col0 + 32 <= N;
-    if (x) {
-      const float sh = static_cast<float>(scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_SHIFT]);
-      if (sh != 0.0f) {
-        const __nv_bfloat16* xr = x + static_cast<int64_t>(b) * xbs + static_cast<int64_t>(row) * xld + col0;
-        if (full && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            const uint4 t = *reinterpret_cast<const uint4*>(xr + j);
-            const uint32_t w[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              v[j + 2 * q] = fmaf(sh, bf16_lo_to_f32(w[q]), v[j + 2 * q]);
-              v[j + 2 * q + 1] = fmaf(sh, bf16_hi_to_f32(w[q]), v[j + 2 * q + 1]);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < N) v[j] = fmaf(sh, __bfloat162float(xr[j]), v[j]);
-        }
-      }
-    }
+    add_shift(b, row, col0, v);
     const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + col0;
     if (dt == DT_BF16) {
       __nv_bfloat16* y = static_cast<__nv_bfloat16*>(out) + o;
