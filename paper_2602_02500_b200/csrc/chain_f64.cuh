@@ -2,14 +2,18 @@
 // every matrix of a co-resident batch chunk in ONE cooperative launch (replacing N-1 launches of
 // the DMMA engine, each of which is latency-bound at these sizes).
 //
-// One CTA per 32 x 32 upper tile (ti <= tj) of C; 4 warps of 16 x 16 (2 x 2 DMMA m8n8k4 fragments).
-// The tile's C_k and P values stay in registers for the whole chain; per step the CTA streams
-// row blocks ti and tj of C_k (full symmetric, f64, written by the previous step) into shared
-// memory with cp.async, accumulates C_k^2 on the fp64 tensor cores, and writes C_{k+1} (tile +
-// mirror) for the next step.  Steps are separated by the per-round 64-bit grid-barrier words of
-// chain_persistent.cuh, which also carry the ||I - C_k||_F^2 partials of the truncation test
-// (here in 2^-50 fixed point, partials clamped to 2^-15 so that up to CF_MAX_GRID CTAs cannot carry
-// into the arrival count; fp32 mode stops only when the dropped terms are below 2^-30 relative).
+// One CTA per T x T upper tile (ti <= tj) of C, T = 16 (h <= 128) or 32.  Per step the CTA pulls row
+// blocks ti and tj of
+// C_k (full symmetric, f64, written by the previous step) into shared memory with one bulk copy
+// per row (cp.async.bulk, completion on an mbarrier), the 4 warps each accumulate the WHOLE tile
+// over a quarter of K on the fp64 tensor cores ((T/8)^2 independent m8n8k4 accumulators per warp),
+// the quarters are summed through shared memory, and every thread updates its T^2/128 contiguous
+// elements of C and P (resident in registers for the whole chain) and
+// writes C_{k+1} (tile + mirror).  Steps are separated by the per-round 64-bit grid-barrier words
+// of chain_persistent.cuh, which also carry the ||I - C_k||_F^2 partials of the truncation test
+// (here in 2^-50 fixed point, partials clamped to 2^-15 so that up to CF_MAX_GRID CTAs cannot
+// carry into the arrival count; fp32 mode stops only when the dropped terms are below 2^-30
+// relative).
 //
 // Inputs as the multi-launch fp32 path: C[0] = C_1 and P = alpha I - c_1 C_1 (prep_f64_kernel).
 // Output: P (full symmetric) for finalize_p_kernel<0> + the apply; scal[b].S_STEPS.
@@ -19,11 +23,17 @@
 
 namespace unso {
 
-constexpr int CF_TILE = 32;
 constexpr int CF_MAX_H = 256;
 constexpr double CF_FIX = 1125899906842624.0;  // 2^50
-constexpr double CF_CLAMP = 1.0 / 32768.0;  // 2^-15: 2^35 units per CTA, so <= 4096 CTAs stay below bit 48
+constexpr double CF_CLAMP = 1.0 / 32768.0;      // 2^-15: 2^35 units per CTA, <= 4096 CTAs stay below bit 48
 constexpr int CF_MAX_GRID = 4096;
+// tile edge: 16 for h <= 128 (more CTAs, shorter steps), 32 up to CF_MAX_H
+__host__ __device__ inline int cf_tile(int h) { return h <= 128 ? 16 : 32; }
+// dynamic shared memory: A and B row blocks [T][K16 + 4] doubles, 4 partial tiles [T][T+1], the mbarrier
+__host__ __device__ inline int cf_smem_bytes(int h, int T) {
+  const int k16 = (h + 15) & ~15;
+  return 2 * T * (k16 + 4) * 8 + 4 * T * (T + 1) * 8 + 16;
+}
 
 struct ChainF64Params {
   double* C[2];        // C_k ping-pong, full symmetric, [b][h][ld]
@@ -44,17 +54,31 @@ __device__ __forceinline__ void cf_arrive(unsigned long long* gbar, int round, d
   red_release_gpu_add_u64(gbar + round, (1ull << 48) + static_cast<uint64_t>(c * CF_FIX));
 }
 
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int T>
 __global__ void __launch_bounds__(128, 1) chain_f64_kernel(const __grid_constant__ ChainF64Params p) {
+  constexpr int FM = T / 8;                 // 8 x 8 DMMA fragments per tile edge
+  constexpr int RED = T * (T + 1);          // one warp's partial tile (doubles, padded rows)
+  constexpr int EPT = T * T / 128;          // tile elements per thread in the epilogue
+  constexpr int TPR = T / EPT;              // threads per tile row
   extern __shared__ __align__(16) uint8_t dsm[];
   const int K16 = (p.h + 15) & ~15;
   const int S = K16 + 4;  // row stride (doubles): fragment loads conflict-free, 16-byte aligned rows
   double* As = reinterpret_cast<double*>(dsm);
-  double* Bs = As + CF_TILE * S;
+  double* Bs = As + T * S;
+  double* part = Bs + T * S;  // [4][T][T + 1]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(part + 4 * RED);
   __shared__ double red[4];
   __shared__ int s_stop;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = warp >> 1, wn = warp & 1, gid = lane >> 2, tig = lane & 3;
+  const int gid = lane >> 2, tig = lane & 3;
   const int lb = blockIdx.x / p.tiles_per_mat;
   const int b = p.b0 + lb;
   int ti, tj;
@@ -62,23 +86,32 @@ __global__ void __launch_bounds__(128, 1) chain_f64_kernel(const __grid_constant
   const int N = p.order;
   const int64_t mb = static_cast<int64_t>(b) * p.mat;
   const double wgt = ti == tj ? 1.0 : 2.0;
+  const int arows = min(T, p.h - ti * T), brows = min(T, p.h - tj * T);
+  const uint32_t row_bytes = static_cast<uint32_t>(p.h) * 8;
 
-  // this thread's 8 tile positions and their C_1 / P values
-  int rr[8], cc[8];
-  bool ok[8];
-  double cv[8], pv[8];
+  // zero both row blocks once: columns >= h and rows past h are never written by the copies
+  for (int i = threadIdx.x; i < 2 * T * S; i += 128) As[i] = 0.0;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // this thread's EPT contiguous tile elements: row tr, columns tc0 .. tc0+EPT-1
+  const int tr = threadIdx.x / TPR, tc0 = (threadIdx.x % TPR) * EPT;
+  const int gr = ti * T + tr;
+  double cv[EPT], pv[EPT];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int i = q >> 2, j = (q >> 1) & 1, e = q & 1;
-    rr[q] = ti * CF_TILE + wm * 16 + i * 8 + gid;
-    cc[q] = tj * CF_TILE + wn * 16 + j * 8 + 2 * tig + e;
-    ok[q] = rr[q] < p.h && cc[q] < p.h;
-    const int64_t o = mb + static_cast<int64_t>(rr[q]) * p.ld + cc[q];
-    cv[q] = ok[q] ? p.C[0][o] : 0.0;
-    pv[q] = ok[q] ? p.P[o] : 0.0;
+  for (int q = 0; q < EPT; ++q) {
+    const int gc = tj * T + tc0 + q;
+    const bool ok = gr < p.h && gc < p.h;
+    const int64_t o = mb + static_cast<int64_t>(gr) * p.ld + gc;
+    cv[q] = ok ? p.C[0][o] : 0.0;
+    pv[q] = ok ? p.P[o] : 0.0;
   }
 
   int steps = 0;
+  uint32_t phase = 0;
   for (int k = 1; k < N; ++k) {
     const double* cur = p.C[(k - 1) & 1];
     if (k >= 2) {
@@ -89,67 +122,101 @@ __global__ void __launch_bounds__(128, 1) chain_f64_kernel(const __grid_constant
       __syncthreads();
       if (s_stop) {  // C_j = I for j > k
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (ok[q] && rr[q] == cc[q]) pv[q] -= p.tail[k];
+        for (int q = 0; q < EPT; ++q)
+          if (gr < p.h && gr == tj * T + tc0 + q) pv[q] -= p.tail[k];
         break;
       }
     }
     ++steps;
-    // row blocks ti (A) and tj (B) of C_k -> shared memory (columns >= h zero-filled)
-    const int cpr = K16 / 2;  // 16-byte chunks per row
-    for (int c = threadIdx.x; c < 2 * CF_TILE * cpr; c += 128) {
-      const int which = c / (CF_TILE * cpr), rem = c % (CF_TILE * cpr);
-      const int row = rem / cpr, col = (rem % cpr) * 2;
-      const int grow = (which ? tj : ti) * CF_TILE + row;
-      const int valid = (grow < p.h && col < p.h) ? min(2, p.h - col) : 0;
-      const double* src = cur + mb + static_cast<int64_t>(valid ? grow : 0) * p.ld + (valid ? col : 0);
-      cp_async16((which ? Bs : As) + row * S + col, src, valid * 8);
+    if (threadIdx.x == 0) CHAIN_TRACE(k, 0);
+    // row blocks ti (A) and tj (B) of C_k -> shared memory, one bulk copy per row
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(bar, (arows + brows) * row_bytes);
+      __syncwarp();
+      for (int r = lane; r < arows + brows; r += 32) {
+        const bool isa = r < arows;
+        const int row = isa ? r : r - arows;
+        const int grow = (isa ? ti : tj) * T + row;
+        bulk_copy_g2s((isa ? As : Bs) + row * S, cur + mb + static_cast<int64_t>(grow) * p.ld, row_bytes, bar);
+      }
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    double acc[2][2][2];
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    if (threadIdx.x == 0) CHAIN_TRACE(k, 1);
+    // warp w: the whole T x T tile over k in [w K16/4, (w+1) K16/4)
+    double acc[FM][FM][2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < FM; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int ks = 0; ks < K16 / 4; ++ks) {
-      const int kk = ks * 4 + tig;
-      const double a0 = As[(wm * 16 + gid) * S + kk], a1 = As[(wm * 16 + 8 + gid) * S + kk];
-      const double b0v = Bs[(wn * 16 + gid) * S + kk], b1v = Bs[(wn * 16 + 8 + gid) * S + kk];
-      dmma_884(acc[0][0], a0, b0v);
-      dmma_884(acc[0][1], a0, b1v);
-      dmma_884(acc[1][0], a1, b0v);
-      dmma_884(acc[1][1], a1, b1v);
+      for (int j = 0; j < FM; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int kq = K16 / 4;
+    for (int ks = warp * kq; ks < (warp + 1) * kq; ks += 4) {
+      const int kk = ks + tig;
+      double a[FM], bv[FM];
+#pragma unroll
+      for (int i = 0; i < FM; ++i) a[i] = As[(i * 8 + gid) * S + kk];
+#pragma unroll
+      for (int j = 0; j < FM; ++j) bv[j] = Bs[(j * 8 + gid) * S + kk];
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FM; ++j) dmma_884(acc[i][j], a[i], bv[j]);
     }
+    double* mine = part + warp * RED;
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FM; ++j) {
+        mine[(i * 8 + gid) * (T + 1) + j * 8 + 2 * tig] = acc[i][j][0];
+        mine[(i * 8 + gid) * (T + 1) + j * 8 + 2 * tig + 1] = acc[i][j][1];
+      }
+    __syncthreads();  // partials complete; As/Bs free for the next step's copies
+    if (threadIdx.x == 0) CHAIN_TRACE(k, 2);
     const bool last = k == N - 1;
     const double coef = p.coef[k];  // multiplies C_{k+1}
     double e2 = 0.0;
-    double* nxt = p.C[k & 1];
+    double cn[EPT];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const double cn = ok[q] ? 2.0 * cv[q] - acc[q >> 2][(q >> 1) & 1][q & 1] : 0.0;
-      pv[q] -= coef * cn;
-      cv[q] = cn;
-      const double dv = ok[q] ? cn - (rr[q] == cc[q] ? 1.0 : 0.0) : 0.0;
+    for (int q = 0; q < EPT; ++q) {
+      const int gc = tj * T + tc0 + q;
+      const bool ok = gr < p.h && gc < p.h;
+      const int o = tr * (T + 1) + tc0 + q;
+      const double s2 = part[o] + part[RED + o] + part[2 * RED + o] + part[3 * RED + o];
+      cn[q] = ok ? 2.0 * cv[q] - s2 : 0.0;
+      pv[q] -= coef * cn[q];
+      cv[q] = cn[q];
+      const double dv = ok ? cn[q] - (gr == gc ? 1.0 : 0.0) : 0.0;
       e2 += wgt * dv * dv;
-      if (!last && ok[q]) {
-        nxt[mb + static_cast<int64_t>(rr[q]) * p.ld + cc[q]] = cn;
-        nxt[mb + static_cast<int64_t>(cc[q]) * p.ld + rr[q]] = cn;
-      }
     }
     if (last) break;
+    double* nxt = p.C[k & 1];
+    if (gr < p.h) {
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        const int gc = tj * T + tc0 + q;
+        if (gc < p.h) {
+          nxt[mb + static_cast<int64_t>(gr) * p.ld + gc] = cn[q];
+          nxt[mb + static_cast<int64_t>(gc) * p.ld + gr] = cn[q];
+        }
+      }
+    }
     e2 = warp_sum(e2);
     if (lane == 0) red[warp] = e2;
-    __syncthreads();  // also: every warp is done with As/Bs before the next step refills them
-    if (threadIdx.x == 0) cf_arrive(p.gbar, k + 1, red[0] + red[1] + red[2] + red[3]);
+    __syncthreads();  // red complete; every thread is done reading the partial tiles
+    if (threadIdx.x == 0) {
+      cf_arrive(p.gbar, k + 1, red[0] + red[1] + red[2] + red[3]);
+      CHAIN_TRACE(k, 3);
+    }
   }
   // final P (tile + mirror) for finalize_p_kernel<0>
+  if (gr < p.h) {
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    if (!ok[q]) continue;
-    p.P[mb + static_cast<int64_t>(rr[q]) * p.ld + cc[q]] = pv[q];
-    p.P[mb + static_cast<int64_t>(cc[q]) * p.ld + rr[q]] = pv[q];
+    for (int q = 0; q < EPT; ++q) {
+      const int gc = tj * T + tc0 + q;
+      if (gc >= p.h) continue;
+      p.P[mb + static_cast<int64_t>(gr) * p.ld + gc] = pv[q];
+      p.P[mb + static_cast<int64_t>(gc) * p.ld + gr] = pv[q];
+    }
   }
   if (threadIdx.x == 0 && blockIdx.x % p.tiles_per_mat == 0) p.scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_STEPS] = steps;
 }

@@ -635,20 +635,25 @@ static int scal_mode(int scaling) {
 // h <= 256: all squarings in one cooperative launch per co-resident batch chunk (chain_f64.cuh).
 // Returns false when the problem does not qualify (the caller then runs the per-step launches).
 static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, double alpha, cudaStream_t st) {
-  if (p.h > CF_MAX_H || p.order < 2 || p.order > CHAIN_MAX_ORDER || std::getenv("UNSO_NO_F64_CHAIN")) return false;
+  // rows are pulled with 16-byte-granular bulk copies: h must be even
+  if (p.h > CF_MAX_H || (p.h & 1) || p.order < 2 || p.order > CHAIN_MAX_ORDER || std::getenv("UNSO_NO_F64_CHAIN"))
+    return false;
   (void)alpha;
   const int h = static_cast<int>(p.h);
-  const int K16 = (h + 15) & ~15;
-  const int smem = 2 * CF_TILE * (K16 + 4) * 8;
-  static int configured_smem = 0;
-  if (smem > configured_smem) {
-    if (cudaFuncSetAttribute(chain_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * CF_TILE * (CF_MAX_H + 4) * 8) !=
-        cudaSuccess)
+  const int T = cf_tile(h);
+  const int smem = cf_smem_bytes(h, T);
+  auto kernel = T == 16 ? chain_f64_kernel<16> : chain_f64_kernel<32>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(chain_f64_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             cf_smem_bytes(128, 16)) != cudaSuccess ||
+        cudaFuncSetAttribute(chain_f64_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             cf_smem_bytes(CF_MAX_H, 32)) != cudaSuccess)
       return false;
-    configured_smem = 2 * CF_TILE * (CF_MAX_H + 4) * 8;
+    configured = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_f64_kernel, 128, smem) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem) != cudaSuccess || per_sm < 1)
     return false;
   ChainF64Params cp;
   std::memset(&cp, 0, sizeof(cp));
@@ -658,7 +663,7 @@ static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, dou
   cp.ld = pl.ldc;
   cp.mat = pl.hh;
   cp.h = h;
-  cp.nt = (h + CF_TILE - 1) / CF_TILE;
+  cp.nt = (h + T - 1) / T;
   cp.tiles_per_mat = cp.nt * (cp.nt + 1) / 2;
   cp.order = p.order;
   cp.gbar = at<unsigned long long>(ws, pl.gbar);
@@ -688,7 +693,7 @@ static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, dou
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, chain_f64_kernel, cp) != cudaSuccess) return false;
+    if (cudaLaunchKernelEx(&cfg, kernel, cp) != cudaSuccess) return false;
     ++g_launches;
   }
   return true;
