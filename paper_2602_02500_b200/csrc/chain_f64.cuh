@@ -15,8 +15,11 @@
 // carry into the arrival count; fp32 mode stops only when the dropped terms are below 2^-30
 // relative).
 //
-// Inputs as the multi-launch fp32 path: C[0] = C_1 and P = alpha I - c_1 C_1 (prep_f64_kernel).
-// Output: P (full symmetric) for finalize_p_kernel<0> + the apply; scal[b].S_STEPS.
+// Phase A (as chain_persistent.cuh): from the reduced Gram G (full symmetric f64) every CTA reduces
+// its tile's trace / weighted ||G||^2 partials, all CTAs sum them in a fixed order after grid round
+// 0 (deterministic), derive s^2 (gram / plain / none scaling), write scal[b] and status[b], and form
+// C_1 = G/s^2 (written for step 1, round 1) and P = alpha I - c_1 C_1 (registers).
+// Output: P (full symmetric) for finalize_p_kernel<0> + the apply; scal[b] incl. S_STEPS.
 #pragma once
 #include "chain_persistent.cuh"
 #include "simt_gemm.cuh"
@@ -36,8 +39,13 @@ __host__ __device__ inline int cf_smem_bytes(int h, int T) {
 }
 
 struct ChainF64Params {
+  const double* G;     // reduced Gram, full symmetric, [b][h][ld]
   double* C[2];        // C_k ping-pong, full symmetric, [b][h][ld]
   double* P;
+  double* normbuf;     // [grid][2] phase-A partials
+  int32_t* status;
+  int scal_mode;       // SM_GRAM / SM_PLAIN / SM_NONE
+  double alpha;        // 1 + sum of the coefficients
   int64_t ld, mat;
   int h, nt, tiles_per_mat, b0, order;
   unsigned long long* gbar;  // [CHAIN_ROUNDS], zeroed before launch
@@ -74,7 +82,8 @@ __global__ void __launch_bounds__(128, 1) chain_f64_kernel(const __grid_constant
   double* Bs = As + T * S;
   double* part = Bs + T * S;  // [4][T][T + 1]
   uint64_t* bar = reinterpret_cast<uint64_t*>(part + 4 * RED);
-  __shared__ double red[4];
+  __shared__ double red[4], red2[4];
+  __shared__ double s_inv_s2;
   __shared__ int s_stop;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -101,23 +110,80 @@ __global__ void __launch_bounds__(128, 1) chain_f64_kernel(const __grid_constant
   const int tr = threadIdx.x / TPR, tc0 = (threadIdx.x % TPR) * EPT;
   const int gr = ti * T + tr;
   double cv[EPT], pv[EPT];
+  // ---- phase A: norms of G -> s^2 (round 0), C_1 = G / s^2 (round 1), P = alpha I - c_1 C_1
+  {
+    double tr = 0.0, fr = 0.0;
 #pragma unroll
-  for (int q = 0; q < EPT; ++q) {
-    const int gc = tj * T + tc0 + q;
-    const bool ok = gr < p.h && gc < p.h;
-    const int64_t o = mb + static_cast<int64_t>(gr) * p.ld + gc;
-    cv[q] = ok ? p.C[0][o] : 0.0;
-    pv[q] = ok ? p.P[o] : 0.0;
+    for (int q = 0; q < EPT; ++q) {
+      const int gc = tj * T + tc0 + q;
+      const bool ok = gr < p.h && gc < p.h;
+      cv[q] = ok ? p.G[mb + static_cast<int64_t>(gr) * p.ld + gc] : 0.0;
+      if (ok && gr == gc) tr += cv[q];
+      fr += wgt * cv[q] * cv[q];
+    }
+    tr = warp_sum(tr);
+    fr = warp_sum(fr);
+    if (lane == 0) {
+      red[warp] = tr;
+      red2[warp] = fr;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      p.normbuf[blockIdx.x * 2 + 0] = red[0] + red[1] + red[2] + red[3];
+      p.normbuf[blockIdx.x * 2 + 1] = red2[0] + red2[1] + red2[2] + red2[3];
+      cf_arrive(p.gbar, 0, 0.0);
+      grid_wait(p.gbar, 0);
+      double s0 = 0.0, s1 = 0.0;
+      const int first = lb * p.tiles_per_mat;
+      for (int t = 0; t < p.tiles_per_mat; ++t) {  // fixed order: every CTA of the matrix agrees
+        s0 += __ldcg(&p.normbuf[(first + t) * 2 + 0]);
+        s1 += __ldcg(&p.normbuf[(first + t) * 2 + 1]);
+      }
+      double s2 = p.scal_mode == SM_PLAIN ? s0 : sqrt(s1);
+      if (p.scal_mode == SM_NONE) s2 = 1.0;
+      const double inv_s = 1.0 / sqrt(s2);
+      const bool bad = p.scal_mode != SM_NONE &&
+                       (!(s0 > 0.0) || !isfinite(s0) || !(s2 > 0.0) || !isfinite(s2) || !isfinite(inv_s));
+      s_inv_s2 = 1.0 / s2;
+      if (blockIdx.x % p.tiles_per_mat == 0) {
+        double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
+        o[S_TRACE] = s0;
+        o[S_FRO2] = s1;
+        o[S_S2] = s2;
+        o[S_INV_S] = inv_s;
+        o[S_DEV2] = 0.0;
+        o[S_SHIFT] = 0.0;  // the fp64 apply uses P itself
+        o[S_MODE] = 0.0;
+        o[S_BOUND] = -1.0;
+        if (p.status) p.status[b] = bad ? 2 : 0;
+      }
+    }
+    __syncthreads();
+    const double inv_s2 = s_inv_s2;
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+      const int gc = tj * T + tc0 + q;
+      const bool ok = gr < p.h && gc < p.h;
+      cv[q] *= inv_s2;
+      pv[q] = ok ? (gr == gc ? p.alpha : 0.0) - p.coef[0] * cv[q] : 0.0;
+      if (ok && N > 1) {
+        p.C[0][mb + static_cast<int64_t>(gr) * p.ld + gc] = cv[q];
+        p.C[0][mb + static_cast<int64_t>(gc) * p.ld + gr] = cv[q];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) cf_arrive(p.gbar, 1, 0.0);  // C_1 published
   }
 
   int steps = 0;
   uint32_t phase = 0;
   for (int k = 1; k < N; ++k) {
     const double* cur = p.C[(k - 1) & 1];
-    if (k >= 2) {
+    {
       if (threadIdx.x == 0) {
         const uint64_t sum = grid_wait(p.gbar, k);  // C_k published, with its ||I - C_k||_F^2 partials
-        s_stop = p.trunc_tau > 0.0 && p.tail_abs[k] * (static_cast<double>(sum) / CF_FIX) <= p.trunc_tau;
+        s_stop = p.trunc_tau > 0.0 && k >= 2 &&
+                 p.tail_abs[k] * (static_cast<double>(sum) / CF_FIX) <= p.trunc_tau;
       }
       __syncthreads();
       if (s_stop) {  // C_j = I for j > k

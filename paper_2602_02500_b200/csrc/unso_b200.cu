@@ -522,7 +522,9 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       pl.C[1] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
       pl.P = take(pl, static_cast<size_t>(B * pl.hh) * 8);
       pl.Pout = take(pl, static_cast<size_t>(B * pl.hh) * 8);
-      pl.gbar = take(pl, CHAIN_ROUNDS * 8);  // chain_f64_kernel rounds
+      pl.gbar = take(pl, CHAIN_ROUNDS * 8);  // chain_f64_kernel rounds and phase-A partials
+      const int64_t nt16 = (p.h + 15) / 16;
+      pl.normbuf = take(pl, static_cast<size_t>(nt16 * (nt16 + 1) / 2 * B) * 2 * 8);
     }
   } else if (bf) {
     // NS in BF16: fp32 state ping-pong + bf16 operand copy (always), G hi/lo, operator B (P), B hi/lo
@@ -634,11 +636,12 @@ static int scal_mode(int scaling) {
 // ---------------------------------------------------------------- UNSO, FP32 precision
 // h <= 256: all squarings in one cooperative launch per co-resident batch chunk (chain_f64.cuh).
 // Returns false when the problem does not qualify (the caller then runs the per-step launches).
-static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, double alpha, cudaStream_t st) {
+static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, const double* G, int32_t* status,
+                                 cudaStream_t st) {
   // rows are pulled with 16-byte-granular bulk copies: h must be even
-  if (p.h > CF_MAX_H || (p.h & 1) || p.order < 2 || p.order > CHAIN_MAX_ORDER || std::getenv("UNSO_NO_F64_CHAIN"))
+  if (p.h > CF_MAX_H || (p.h & 1) || p.order < 2 || p.order > CHAIN_MAX_ORDER ||
+      p.scaling == UNSO_SCALING_GELFAND || std::getenv("UNSO_NO_F64_CHAIN"))
     return false;
-  (void)alpha;
   const int h = static_cast<int>(p.h);
   const int T = cf_tile(h);
   const int smem = cf_smem_bytes(h, T);
@@ -657,6 +660,12 @@ static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, dou
     return false;
   ChainF64Params cp;
   std::memset(&cp, 0, sizeof(cp));
+  cp.G = G;
+  cp.normbuf = at<double>(ws, pl.normbuf);
+  cp.status = status;
+  cp.scal_mode = scal_mode(p.scaling);
+  cp.alpha = 1.0;
+  for (double v : p.co) cp.alpha += v;
   cp.C[0] = at<double>(ws, pl.C[0]);
   cp.C[1] = at<double>(ws, pl.C[1]);
   cp.P = at<double>(ws, pl.P);
@@ -701,10 +710,14 @@ static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, dou
 
 static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, const void* x, const double* G, void* y,
                                 int32_t* status, cudaStream_t st) {
-  UNSO_TRY(norms_and_scalars<double>(p, pl, ws, G, scal_mode(p.scaling), status, st));
-  if (p.scaling == UNSO_SCALING_GELFAND) UNSO_TRY(gelfand_scale<double>(p, pl, ws, G, DT_F64, status, st));
   const int h = static_cast<int>(p.h);
   const int N = p.order;
+  if (chain_f64_persistent(p, pl, ws, G, status, st)) {  // norms, C_1 and the whole chain in one launch
+    prof_mark(3, st);
+    prof_mark(4, st);
+  } else {
+  UNSO_TRY(norms_and_scalars<double>(p, pl, ws, G, scal_mode(p.scaling), status, st));
+  if (p.scaling == UNSO_SCALING_GELFAND) UNSO_TRY(gelfand_scale<double>(p, pl, ws, G, DT_F64, status, st));
   double alpha = 1.0;
   for (double v : p.co) alpha += v;
   {
@@ -714,9 +727,6 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
     UNSO_CHECK_LAUNCH();
   }
   prof_mark(3, st);
-  if (chain_f64_persistent(p, pl, ws, alpha, st)) {
-    prof_mark(4, st);
-  } else {
   int cur = 0;
   for (int k = 1; k < N; ++k) {  // produces C_{k+1}
     SimtOperand C{at<double>(ws, pl.C[cur]), pl.ldc, pl.hh, DT_F64, 1};
