@@ -83,31 +83,65 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-static bool make_map(CUtensorMap* m, const void* base, cuuint64_t d0, cuuint64_t d1, cuuint64_t d2, int64_t ld,
-                     int64_t bstride, cuuint32_t b0, cuuint32_t b1) {
+// 3-D SWIZZLE_128B map, memoised per host thread: a map is a pure function of (dtype, base, dims,
+// strides, box), and training loops hand the same buffers every step, so most calls skip the
+// driver encode (a few microseconds each, several per orthogonalization).
+static bool encode_map_3d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, const cuuint64_t (&dims)[3],
+                          const cuuint64_t (&strides)[2], cuuint32_t b0, cuuint32_t b1) {
+  struct Entry {
+    CUtensorMap map;
+    const void* base;
+    cuuint64_t dims[3], strides[2];
+    cuuint32_t b0, b1;
+    int dt;
+    bool used;
+  };
+  constexpr int kEntries = 64;
+  thread_local Entry cache[kEntries];
+  thread_local int next = 0;
+  for (Entry& e : cache) {
+    if (e.used && e.base == base && e.dt == static_cast<int>(dt) && e.b0 == b0 && e.b1 == b1 &&
+        e.dims[0] == dims[0] && e.dims[1] == dims[1] && e.dims[2] == dims[2] && e.strides[0] == strides[0] &&
+        e.strides[1] == strides[1]) {
+      *m = e.map;
+      return true;
+    }
+  }
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return false;
-  cuuint64_t dims[3] = {d0, d1, d2};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(bstride) * 2};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  Entry& e = cache[next];
+  next = (next + 1) % kEntries;
+  e.map = *m;
+  e.base = base;
+  for (int i = 0; i < 3; ++i) e.dims[i] = dims[i];
+  e.strides[0] = strides[0];
+  e.strides[1] = strides[1];
+  e.b0 = b0;
+  e.b1 = b1;
+  e.dt = static_cast<int>(dt);
+  e.used = true;
+  return true;
+}
+
+static bool make_map(CUtensorMap* m, const void* base, cuuint64_t d0, cuuint64_t d1, cuuint64_t d2, int64_t ld,
+                     int64_t bstride, cuuint32_t b0, cuuint32_t b1) {
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(bstride) * 2};
+  return encode_map_3d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, dims, strides, b0, b1);
 }
 
 // e4m3 operand maps (byte elements, SWIZZLE_128B, 128-byte TMA rows).
 static bool make_map_u8(CUtensorMap* m, const void* base, int64_t d0, int64_t d1, int64_t d2, int64_t ld, int64_t bs,
                         cuuint32_t b0, cuuint32_t b1) {
-  EncodeTiledFn fn = encode_tiled();
-  if (!fn) return false;
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d0), static_cast<cuuint64_t>(d1), static_cast<cuuint64_t>(d2)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(d2 <= 1 ? d1 * ld : bs)};
-  cuuint32_t box[3] = {b0, b1, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d0), static_cast<cuuint64_t>(d1), static_cast<cuuint64_t>(d2)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(d2 <= 1 ? d1 * ld : bs)};
+  return encode_map_3d(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, base, dims, strides, b0, b1);
 }
 
 bool umma_make_kmajor_map(CUtensorMap* m, const void* base, int64_t rows, int64_t k, int64_t ld, int64_t batch,

@@ -79,6 +79,7 @@ class MethodSpec:
     truncate: bool = True            # bf16 mode, persistent chain: stop once ||I - C_k||_F bounds the rest
 
     def __post_init__(self):
+        object.__setattr__(self, "_cache", {})  # per-spec memo of the native method descriptor / FLOP model
         kind = MethodKind(self.kind)
         object.__setattr__(self, "kind", kind)
         if self.scaling is not None:
@@ -306,6 +307,16 @@ def _resolve_precision(spec: MethodSpec, t: torch.Tensor, precision) -> Precisio
 
 
 def _method_desc(spec: MethodSpec, precision: Precision, scaling_code: int):
+    """(MethodDesc, coefficient array) for the ABI, memoised on the (immutable) spec; the array is
+    kept alive with the descriptor that points into it."""
+    key = ("desc", precision, scaling_code)
+    hit = spec._cache.get(key)
+    if hit is None:
+        hit = spec._cache[key] = _build_method_desc(spec, precision, scaling_code)
+    return hit
+
+
+def _build_method_desc(spec: MethodSpec, precision: Precision, scaling_code: int):
     if spec.kind is MethodKind.UNSO:
         co = spec.coeffs.device_coefficients()
         method, order, steps = N.METHOD_UNSO, spec.coeffs.order, 0
@@ -349,8 +360,8 @@ class _Workspace:
 workspace_pool = _Workspace()
 
 
-def _status_check(status: torch.Tensor, check: bool) -> None:
-    if check and bool((status != 0).any().item()):
+def _status_check(status: torch.Tensor | None, check: bool) -> None:
+    if check and status is not None and bool((status != 0).any().item()):
         bad = torch.nonzero(status).flatten().tolist()
         raise DegenerateInputError(
             f"matrices {bad}: input is identically zero or the scaling denominator is not a positive finite number")
@@ -372,10 +383,12 @@ def _run(m: torch.Tensor, spec: MethodSpec, scaling_code: int, precision, out, c
         y = out if out is not None else torch.empty(m.shape, dtype=m.dtype, device=device)
         if y.shape != m.shape or y.dtype != m.dtype or not y.is_contiguous():
             raise ShapeError("out must be a contiguous tensor with the input's shape and dtype")
-        status = torch.zeros(xd.batch, dtype=torch.int32, device=device)
+        # the status words are only read back when checking (the ABI accepts a null status)
+        status = torch.zeros(xd.batch, dtype=torch.int32, device=device) if check else None
         code = lib.unso_orthogonalize(ctypes.byref(xd), ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(y.data_ptr()),
                                       ctypes.byref(md), ctypes.c_void_p(ws.data_ptr()), ctypes.c_size_t(ws.numel()),
-                                      ctypes.c_void_p(status.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+                                      ctypes.c_void_p(status.data_ptr() if status is not None else None),
+                                      ctypes.c_void_p(stream.cuda_stream))
         launches = N.launch_count()
         info = None
         if code == N.OK and check:
@@ -403,11 +416,15 @@ def orthogonalize(m: torch.Tensor, spec: MethodSpec, *, precision=None, out=None
     h, w, tall = _hw(m)
     scaling = spec.effective_scaling
     y, prec, launches, info = _run(m, spec, _SCALING[scaling], precision, out, check)
-    return OrthoResult(y=y, flops=kernel_model_flops(h, w, spec), was_transposed=tall,
-                       preprocess_flops=preprocess_model_flops(h, w, scaling, spec.gelfand_power),
-                       kernel_matmul_shapes=model_matmul_shapes(h, w, spec),
-                       executed_matmul_shapes=executed_matmul_shapes(h, w, spec), precision=prec.value,
-                       launches=launches, info=info)
+    key = ("model", h, w)
+    meta = spec._cache.get(key)
+    if meta is None:
+        meta = spec._cache[key] = (kernel_model_flops(h, w, spec),
+                                   preprocess_model_flops(h, w, scaling, spec.gelfand_power),
+                                   model_matmul_shapes(h, w, spec), executed_matmul_shapes(h, w, spec))
+    return OrthoResult(y=y, flops=meta[0], was_transposed=tall, preprocess_flops=meta[1],
+                       kernel_matmul_shapes=list(meta[2]), executed_matmul_shapes=list(meta[3]),
+                       precision=prec.value, launches=launches, info=info)
 
 
 def scale_denominator(m: torch.Tensor, scaling: Scaling, gelfand_power: int = 2, check: bool = True) -> torch.Tensor:
