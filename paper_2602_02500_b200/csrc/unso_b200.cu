@@ -238,7 +238,12 @@ struct UEpiPartialF32 {
     if (row >= h) return;
     float* dst = part + (static_cast<int64_t>(split) * batch + b) * bs + static_cast<int64_t>(row) * ld + col0;
 #pragma unroll
-    for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    for (int j = 0; j < 32; j += 8) {  // 256-bit stores (ld is a multiple of 256, col0 of 32)
+      uint32_t w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w[q] = __float_as_uint(v[j + q]);
+      st_global_v8(dst + j, w);
+    }
   }
 };
 
@@ -302,7 +307,18 @@ struct UEpiOut {
     const float sh = static_cast<float>(scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_SHIFT]);
     if (sh == 0.0f) return;
     const __nv_bfloat16* xr = x + static_cast<int64_t>(b) * xbs + static_cast<int64_t>(row) * xld + col0;
-    if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
+    if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(xr) & 31) == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 16) {
+        uint32_t w[8];
+        ld_global_v8(xr + j, w);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          v[j + 2 * q] = fmaf(sh, bf16_lo_to_f32(w[q]), v[j + 2 * q]);
+          v[j + 2 * q + 1] = fmaf(sh, bf16_hi_to_f32(w[q]), v[j + 2 * q + 1]);
+        }
+      }
+    } else if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
 #pragma unroll
       for (int j = 0; j < 32; j += 8) {
         const uint4 t = *reinterpret_cast<const uint4*>(xr + j);
@@ -330,7 +346,15 @@ struct UEpiOut {
     const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + col0;
     if (dt == DT_BF16) {
       __nv_bfloat16* y = static_cast<__nv_bfloat16*>(out) + o;
-      if (full && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+      if (full && (reinterpret_cast<uintptr_t>(y) & 31) == 0) {  // two 256-bit stores: whole sectors
+#pragma unroll
+        for (int j = 0; j < 32; j += 16) {
+          uint32_t w[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) w[q] = pack_bf16x2(v[j + 2 * q], v[j + 2 * q + 1]);
+          st_global_v8(y + j, w);
+        }
+      } else if (full && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
 #pragma unroll
         for (int j = 0; j < 32; j += 8)
           *reinterpret_cast<uint4*>(y + j) =
