@@ -408,9 +408,9 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
             const int nb = k & 1;
             const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              *reinterpret_cast<uint4*>(p.chi[nb] + o + j) = *reinterpret_cast<const uint4*>(hi + j);
-              *reinterpret_cast<uint4*>(p.clo[nb] + o + j) = *reinterpret_cast<const uint4*>(lo + j);
+            for (int j = 0; j < 32; j += 16) {  // 256-bit stores: whole sectors (ld % 256 == 0)
+              st_global_v8(p.chi[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(hi + j));
+              st_global_v8(p.clo[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(lo + j));
             }
           }
         } else {

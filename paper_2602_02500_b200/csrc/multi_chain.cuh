@@ -59,9 +59,9 @@ struct UEpiGramSplit {
     if (!rok) return;
     const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + col0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      *reinterpret_cast<uint4*>(hi + o + 8 * j) = make_uint4(hw[4 * j], hw[4 * j + 1], hw[4 * j + 2], hw[4 * j + 3]);
-      *reinterpret_cast<uint4*>(lo + o + 8 * j) = make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
+    for (int j = 0; j < 2; ++j) {  // 256-bit stores: whole sectors (ld % 256 == 0)
+      st_global_v8(hi + o + 16 * j, *reinterpret_cast<const uint32_t(*)[8]>(hw + 8 * j));
+      st_global_v8(lo + o + 16 * j, *reinterpret_cast<const uint32_t(*)[8]>(lw + 8 * j));
     }
   }
 };
