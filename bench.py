@@ -44,6 +44,8 @@ def parse_args():
     ap.add_argument("--rows", type=int, default=262144)
     ap.add_argument("--cols", type=int, default=2048)
     ap.add_argument("--precision", choices=["bf16", "fp32"], default="bf16")
+    ap.add_argument("--collective", choices=["nccl", "nvlink"], default="nccl",
+                    help="N > 1: Gram all-reduce through NCCL, or the peer-memory reduction (unso_gram_push/...)")
     ap.add_argument("--apply-terms", type=int, choices=[1, 2], default=None,
                     help="bf16 apply split: default adaptive per matrix (device-side bound)")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -217,7 +219,7 @@ def main():
         if world == 1:
             U.orthogonalize(x, spec, out=y, check=False)
         else:
-            orthogonalize_row_sharded(x, spec, out=y, check=False)
+            orthogonalize_row_sharded(x, spec, out=y, check=False, collective=args.collective)
 
     # ---- correctness gate (untimed): status + orthogonality of the output
     apply_info = None
@@ -226,7 +228,7 @@ def main():
         launches_per_step = res.launches
         apply_info = res.info[0] if res.info else None
     else:
-        orthogonalize_row_sharded(x, spec, out=y, check=True)
+        orthogonalize_row_sharded(x, spec, out=y, check=True, collective=args.collective)
         launches_per_step = None
     torch.cuda.synchronize()
     ortho_err = float(U.ortho_error_device(y)[0]) if world == 1 else None
@@ -309,7 +311,7 @@ def main():
                 if world == 1:
                     U.orthogonalize(xd[j], spec, out=yd[j], check=False)
                 else:
-                    orthogonalize_row_sharded(xd[j], spec, out=yd[j], check=False)
+                    orthogonalize_row_sharded(xd[j], spec, out=yd[j], check=False, collective=args.collective)
                 ev_cmp[j].record(s_cmp)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev_cmp[j])
@@ -379,7 +381,8 @@ def main():
                                             + {None: "adaptive bf16/bf16x2 (shifted P)", 1: "bf16", 2: "bf16x2"}[
                                                 args.apply_terms] + " apply")
                        if args.precision == "bf16" else "fp64-grade DFMA",
-                       "parallelism": f"row-shard x{world} + NCCL all-reduce of G" if world > 1 else "1 GPU",
+                       "parallelism": (f"row-shard x{world} + " + ("NCCL all-reduce of G" if args.collective == "nccl" else
+                                 "NVLink peer-memory reduction of G")) if world > 1 else "1 GPU",
                        "l2": "input 1 GiB > 126 MB L2 (no flush needed)"},
             "matrices_per_s": 1e3 / ms_step,
             "pct_bf16_peak": value / peak,

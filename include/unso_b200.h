@@ -127,6 +127,35 @@ int32_t unso_orthogonalize_from_gram(const unso_matrix_desc* x, const void* x_pt
                                      const unso_method_desc* method, void* workspace, size_t workspace_bytes,
                                      int32_t* d_status, void* stream);
 
+/* Row-sharded path with the Gram reduction over NVLink peer memory instead of an all-reduce
+ * (BF16 precision, one matrix).  Every rank owns three peer-mapped buffers (e.g.
+ * torch symmetric memory) whose device addresses on every rank are listed here:
+ *   slots  unso_gram_peer_bytes(h, world, splits, 0) bytes: partial Gram tiles pushed to their owner,
+ *   g      unso_gram_peer_bytes(h, world, splits, 1) bytes: the reduced dense h x h fp32 Gram,
+ *   flags  unso_gram_peer_bytes(h, world, splits, 2) bytes: zero-initialised once, then never reset
+ *          (`epoch` must increase by one per call).
+ * Per call and rank, in stream order: unso_gram_push (local Gram on the CTA pairs, partial tiles
+ * stored straight into the owners' slots, then "pushed" published), unso_gram_reduce (wait for all
+ * ranks' pushes, sum the owned tiles in a fixed order, write them into every rank's g, publish),
+ * unso_gram_wait (wait until every rank delivered); g then holds the same reduced Gram on every
+ * rank and feeds unso_orthogonalize_from_gram.  The three calls are separate so that one GPU can
+ * emulate all ranks phase by phase.  `splits` (split-K slices, >= 1, <= local rows / 64) must be
+ * equal on every rank. */
+#define UNSO_MAX_PEERS 8
+typedef struct unso_gram_peers {
+  void* slots[UNSO_MAX_PEERS];
+  void* g[UNSO_MAX_PEERS];
+  uint32_t* flags[UNSO_MAX_PEERS];
+} unso_gram_peers;
+size_t unso_gram_peer_bytes(int64_t h, int32_t world, int32_t splits, int32_t which);
+int32_t unso_gram_push(const unso_matrix_desc* x_local, const void* x_ptr, const unso_method_desc* method,
+                       const unso_gram_peers* peers, int32_t rank, int32_t world, int32_t splits, uint32_t epoch,
+                       void* workspace, size_t workspace_bytes, void* stream);
+int32_t unso_gram_reduce(int64_t h, const unso_gram_peers* peers, int32_t rank, int32_t world, int32_t splits,
+                         uint32_t epoch, void* workspace, size_t workspace_bytes, void* stream);
+int32_t unso_gram_wait(int64_t h, const unso_gram_peers* peers, int32_t rank, int32_t world, uint32_t epoch,
+                       void* stream);
+
 /* The preprocess denominator alone (ortho.py:140-168): d_denom[b] = ||A A^T||_F^(1/2) (gram),
  * ||A||_F (plain) or ||(A A^T)^k||_F^(1/2k) (gelfand), fp64 accumulation; d_status[b] = 2 when the
  * input is zero or the denominator is not positive and finite. Only scaling/gelfand_power are read. */

@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "unso_version", "unso_status_string", "unso_workspace_size", "unso_orthogonalize", "unso_gram",
     "unso_gram_dtype", "unso_orthogonalize_from_gram", "unso_scale_denominator", "unso_ortho_error",
     "unso_last_launch_count", "unso_profile_begin", "unso_profile_read", "unso_profile_end",
-    "unso_query_scalars",
+    "unso_query_scalars", "unso_gram_peer_bytes", "unso_gram_push", "unso_gram_reduce", "unso_gram_wait",
 )
 SCALARS = 16
 SCALAR_NAMES = ("trace", "fro2", "dev2", "s2", "inv_s", "ortho_error", "shift", "apply_single", "apply_bound",
@@ -55,6 +55,15 @@ class MethodDesc(ctypes.Structure):
                 ("precision", ctypes.c_int32), ("order", ctypes.c_int32), ("steps", ctypes.c_int32),
                 ("coeffs", ctypes.POINTER(ctypes.c_double)), ("flags", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
+
+
+MAX_PEERS = 8
+
+
+class GramPeers(ctypes.Structure):
+    """unso_gram_peers: every rank's peer-mapped slot / Gram / flag buffers."""
+    _fields_ = [("slots", ctypes.c_void_p * MAX_PEERS), ("g", ctypes.c_void_p * MAX_PEERS),
+                ("flags", ctypes.c_void_p * MAX_PEERS)]
 
 
 _lib = None
@@ -92,6 +101,17 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.unso_query_scalars.argtypes = [XD, MD, P, P, P]
     lib.unso_profile_end.restype = None
     lib.unso_profile_end.argtypes = []
+    GP = ctypes.POINTER(GramPeers)
+    lib.unso_gram_peer_bytes.restype = ctypes.c_size_t
+    lib.unso_gram_peer_bytes.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+    lib.unso_gram_push.restype = ctypes.c_int32
+    lib.unso_gram_push.argtypes = [XD, P, MD, GP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
+                                   P, ctypes.c_size_t, P]
+    lib.unso_gram_reduce.restype = ctypes.c_int32
+    lib.unso_gram_reduce.argtypes = [ctypes.c_int64, GP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.c_uint32, P, ctypes.c_size_t, P]
+    lib.unso_gram_wait.restype = ctypes.c_int32
+    lib.unso_gram_wait.argtypes = [ctypes.c_int64, GP, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P]
 
 
 def lib() -> ctypes.CDLL:

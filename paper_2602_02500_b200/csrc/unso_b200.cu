@@ -28,6 +28,7 @@
 #include "chain_persistent.cuh"
 #include "chain_small.cuh"
 #include "chain_f64.cuh"
+#include "gram_allreduce.cuh"
 #include "umma2_gemm.cuh"
 #include "chain_pair.cuh"
 #include "ns_bf16.cuh"
@@ -1648,6 +1649,95 @@ int32_t unso_gram(const unso_matrix_desc* x, const void* x_ptr, void* g_ptr, con
   UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
   UNSO_TRY(gram_bf16(p, pl, workspace, xb, ldx, bsx, st));
   return finalize_gram<float>(p, pl, workspace, pl.splits, static_cast<float*>(g_ptr), st, h, h * h);
+}
+
+// ---------------------------------------------------------------- Gram reduction over NVLink peers
+static bool gar_peers(const unso_gram_peers* in, int32_t world, GarPeers& out) {
+  if (!in || world < 1 || world > GAR_MAX_WORLD) return false;
+  for (int r = 0; r < world; ++r) {
+    if (!in->slots[r] || !in->g[r] || !in->flags[r]) return false;
+    out.slots[r] = static_cast<float*>(in->slots[r]);
+    out.g[r] = static_cast<float*>(in->g[r]);
+    out.flags[r] = in->flags[r];
+  }
+  return true;
+}
+
+size_t unso_gram_peer_bytes(int64_t h, int32_t world, int32_t splits, int32_t which) {
+  if (h < 1 || h > (1 << 16) || world < 1 || world > GAR_MAX_WORLD || splits < 1 || splits > 64) return 0;
+  if (which == 0)
+    return static_cast<size_t>(gar_slot_offset(world, 0, 0, splits, gar_owned_max(static_cast<int>(h), world))) * 4;
+  if (which == 1) return static_cast<size_t>(h * h) * 4;
+  if (which == 2) return static_cast<size_t>(2 * world) * 4;
+  return 0;
+}
+
+int32_t unso_gram_push(const unso_matrix_desc* x, const void* x_ptr, const unso_method_desc* method,
+                       const unso_gram_peers* peers, int32_t rank, int32_t world, int32_t splits, uint32_t epoch,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  Problem p;
+  UNSO_TRY(make_problem(x, method, p));
+  if (p.method != UNSO_METHOD_UNSO || p.prec != UNSO_PREC_BF16 || p.batch != 1 || !use_pair_engine())
+    return UNSO_ERR_UNSUPPORTED;
+  GarPeers gp;
+  if (!x_ptr || !gar_peers(peers, world, gp) || rank < 0 || rank >= world || splits < 1 || splits > 64 ||
+      (p.w + 63) / 64 < splits)
+    return UNSO_ERR_VALUE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Plan pl = make_plan(p, true);
+  UNSO_TRY(check_ws(pl, workspace, workspace_bytes));
+  const __nv_bfloat16* xb;
+  int64_t ldx, bsx;
+  UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
+  const int h = static_cast<int>(p.h);
+  UEpiPushF32 epi{gp, rank, world, splits, gar_owned_max(h, world), h, (h + GAR_TILE - 1) / GAR_TILE};
+  const UmmaWork w2 = umma2_make_work(h, h, static_cast<int>(p.w), 256, 1, true, splits);
+  CUtensorMap mx;
+  cudaError_t e;
+  if (p.tall) {
+    if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, 1, bsx)) return UNSO_ERR_CUDA;
+    e = launch_umma2<Cfg2GramMN>(mx, mx, mx, mx, w2, epi, st);
+  } else {
+    if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, 1, bsx, 128)) return UNSO_ERR_CUDA;
+    e = launch_umma2<Cfg2GramK>(mx, mx, mx, mx, w2, epi, st);
+  }
+  if (e != cudaSuccess) return UNSO_ERR_CUDA;
+  gar_signal_kernel<<<1, 1, 0, st>>>(gp, rank, world, 0, epoch);
+  UNSO_CHECK_LAUNCH();
+  g_launches += 2;
+  return UNSO_OK;
+}
+
+int32_t unso_gram_reduce(int64_t h, const unso_gram_peers* peers, int32_t rank, int32_t world, int32_t splits,
+                         uint32_t epoch, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  GarPeers gp;
+  if (h < 1 || !gar_peers(peers, world, gp) || rank < 0 || rank >= world || splits < 1 || splits > 64)
+    return UNSO_ERR_VALUE;
+  if (!workspace || workspace_bytes < sizeof(unsigned)) return UNSO_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned* done = static_cast<unsigned*>(workspace);
+  if (cudaMemsetAsync(done, 0, sizeof(unsigned), st) != cudaSuccess) return UNSO_ERR_CUDA;
+  const int hh = static_cast<int>(h);
+  const int owned = gar_owned_max(hh, world);
+  dim3 grid(static_cast<unsigned>(owned), 64);
+  gar_reduce_kernel<<<grid, 256, 0, st>>>(gp, rank, world, splits, owned, hh, (hh + GAR_TILE - 1) / GAR_TILE, epoch,
+                                          done);
+  UNSO_CHECK_LAUNCH();
+  g_launches = 1;
+  return UNSO_OK;
+}
+
+int32_t unso_gram_wait(int64_t h, const unso_gram_peers* peers, int32_t rank, int32_t world, uint32_t epoch,
+                       void* stream) {
+  g_launches = 0;
+  GarPeers gp;
+  if (h < 1 || !gar_peers(peers, world, gp) || rank < 0 || rank >= world) return UNSO_ERR_VALUE;
+  gar_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(gp.flags[rank], world, 1, epoch);
+  UNSO_CHECK_LAUNCH();
+  g_launches = 1;
+  return UNSO_OK;
 }
 
 int32_t unso_orthogonalize_from_gram(const unso_matrix_desc* x, const void* x_ptr, const void* g_ptr, void* y_ptr,

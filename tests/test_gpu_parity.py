@@ -493,3 +493,63 @@ def test_fp32_persistent_chain_truncation(h):
     ref = O.unso_rows_of_tall(x.double().cpu().numpy(), rows)
     assert rel(res.y.double().cpu().numpy()[rows], ref) <= TOL["fp32"]
     assert rel(res.y.double().cpu().numpy(), full.y.double().cpu().numpy()) <= 1e-7
+
+
+@pytest.mark.parametrize("h,world", [(512, 4), (2048, 4), (640, 3)])
+def test_nvlink_gram_reduction_emulated_ranks(h, world):
+    """The peer-memory Gram reduction (unso_gram_push / _reduce / _wait) with `world`
+    ranks emulated on one GPU phase by phase: every rank ends with the same bit-identical reduced
+    Gram, equal to the sum of the shard Grams, and the sharded orthogonalization matches the
+    unsharded one."""
+    from paper_2602_02500_b200.distributed import (NvlinkGramReducer, gram_push_splits, native_finish, native_gram,
+                                                   row_shard_bounds)
+    g = torch.Generator().manual_seed(50 + h)
+    w = 8 * h
+    x = torch.randn(w, h, generator=g).to(torch.bfloat16).to(DEV)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+    shards = [x[slice(*row_shard_bounds(w, world, r))] for r in range(world)]
+    splits = gram_push_splits(h, min(s.shape[0] for s in shards))
+    reducers = NvlinkGramReducer.emulated(h, world, splits, DEV)
+    for it in range(2):  # two calls: the epoch-tagged flags need no reset
+        for r in range(world):
+            reducers[r].push(shards[r], spec, "bf16")
+        for r in range(world):
+            reducers[r].reduce()
+        gs = [reducers[r].wait() for r in range(world)]
+        torch.cuda.synchronize()
+        for r in range(1, world):
+            assert torch.equal(gs[r], gs[0])
+        ref = sum(native_gram(s, spec, "bf16").double() for s in shards)
+        assert float((gs[0].double() - ref).norm() / ref.norm()) <= 1e-6
+    y = torch.cat([native_finish(s, gs[r].clone(), spec, "bf16")[0] for r, s in enumerate(shards)])
+    full = U.orthogonalize(x, spec, precision="bf16").y
+    torch.cuda.synchronize()
+    assert rel(y.double().cpu().numpy(), full.double().cpu().numpy()) <= 5e-3
+
+
+def test_nvlink_gram_reduction_symmetric_memory_world1():
+    """The same path through torch symmetric memory (the real peer mappings) on a 1-rank group."""
+    import os
+    import torch.distributed as dist
+    from paper_2602_02500_b200.distributed import orthogonalize_row_sharded
+    own = not dist.is_initialized()
+    if own:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        g = torch.Generator().manual_seed(77)
+        x = torch.randn(16384, 1024, generator=g).to(torch.bfloat16).to(DEV)
+        spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
+        try:
+            y = orthogonalize_row_sharded(x, spec, collective="nvlink")
+        except (RuntimeError, NotImplementedError) as exc:  # symmetric memory unavailable on this node
+            pytest.skip(f"torch symmetric memory unavailable: {exc}")
+        full = U.orthogonalize(x, spec).y
+        torch.cuda.synchronize()
+        assert rel(y.double().cpu().numpy(), full.double().cpu().numpy()) <= 5e-3
+    finally:
+        if own:
+            from paper_2602_02500_b200 import distributed as D
+            D._REDUCERS.clear()
+            dist.destroy_process_group()
