@@ -95,3 +95,20 @@ def test_no_oracle_import_in_product():
             if f.endswith(".py"):
                 src = open(os.path.join(root, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
+
+
+def test_gram_peer_buffer_sizes():
+    """unso_gram_peer_bytes (host-only): slot buffer = world x splits x ceil(tiles / world) 256x256 fp32
+    tiles, Gram = h^2 fp32, flags = 2 x world words; invalid arguments give 0."""
+    lib = N.lib()
+    for h, world, splits in ((2048, 8, 2), (512, 4, 4), (640, 3, 1), (128, 1, 1)):
+        nt = (h + 255) // 256
+        tiles = nt * (nt + 1) // 2
+        owned = -(-tiles // world)
+        assert lib.unso_gram_peer_bytes(h, world, splits, 0) == world * splits * owned * 256 * 256 * 4
+        assert lib.unso_gram_peer_bytes(h, world, splits, 1) == h * h * 4
+        assert lib.unso_gram_peer_bytes(h, world, splits, 2) == 2 * world * 4
+    assert lib.unso_gram_peer_bytes(2048, 9, 1, 0) == 0
+    assert lib.unso_gram_peer_bytes(2048, 2, 0, 0) == 0
+    from paper_2602_02500_b200.distributed import gram_push_splits
+    assert gram_push_splits(2048, 32768) == 2 and gram_push_splits(128, 64) == 1
