@@ -212,10 +212,8 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
             const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * CH_TILE, ks)
                                      : operand_desc<false>(st + 3 * CH_TILE, ks);
             umma_bf16(tmem + CH_ACC, ah, bh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
-#ifndef UNSO_EXP_ONETERM  // timing experiment only: hi*hi alone, loads unchanged
             umma_bf16(tmem + CH_ACC, ah, bl, idesc, 1u);
             umma_bf16(tmem + CH_ACC, al, bh, idesc, 1u);
-#endif
           }
           umma_commit(&empty[stage]);
           if (++stage == CH_STAGES) {

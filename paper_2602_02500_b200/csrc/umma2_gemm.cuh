@@ -66,10 +66,8 @@ __device__ __forceinline__ bool filtered_out(const UmmaWork& w, int b) {
 // Epilogues with a rows4(b, split, row0, col0, stage) member take the accumulator through shared memory.
 template <class E, class = void>
 struct epi_has_rows4 : std::false_type {};
-#ifndef UNSO_EXP_NO_ROWS4  // timing experiment: force the register-direct epilogue
 template <class E>
 struct epi_has_rows4<E, std::void_t<decltype(&E::rows4)>> : std::true_type {};
-#endif
 
 // lane = row: the lane's 32 accumulator columns go to the warp's 4 KB block, 16-byte chunk j at slot
 // j ^ (row & 7) (conflict-free for these row-wise writes and for rows4's 4-rows-per-instruction
