@@ -353,7 +353,7 @@ struct UEpiOut {
           uint32_t w[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) w[q] = pack_bf16x2(v[j + 2 * q], v[j + 2 * q + 1]);
-          st_global_v8(y + j, w);
+          st_global_cs_v8(y + j, w);
         }
       } else if (full && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
 #pragma unroll
