@@ -35,6 +35,7 @@ from .ortho import (
     scale_denominator,
     unso,
 )
+from .muon import Muon
 from .scalarpoly import (
     BRule,
     CesistaStepParams,
@@ -51,7 +52,7 @@ from .scalarpoly import (
 )
 
 __all__ = [
-    "BRule", "CesistaStepParams", "CoefficientSet", "DEFAULT_MUON_ITERATIONS", "DEFAULT_ORIGINAL_ITERATIONS",
+    "Muon", "BRule", "CesistaStepParams", "CoefficientSet", "DEFAULT_MUON_ITERATIONS", "DEFAULT_ORIGINAL_ITERATIONS",
     "DegenerateInputError", "FlopsCounter", "MUON_COEFFICIENTS", "MethodKind", "MethodSpec", "NativeError",
     "OrthoResult", "ParseError", "Precision", "Scaling", "ShapeError", "UnsupportedError", "cesista_ns",
     "constraint_point", "constraint_residual", "default_cesista_triples", "default_coefficients", "derive_b",
