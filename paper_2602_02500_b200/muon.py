@@ -76,26 +76,31 @@ class Muon(torch.optim.Optimizer):
                 buf = state.get("momentum_buffer")
                 if buf is None:
                     buf = state["momentum_buffer"] = torch.zeros_like(g)
-                buf.mul_(mu).add_(g)
-                upd = g.add(buf, alpha=mu) if nesterov else buf.clone()
+                torch.add(g, buf, alpha=mu, out=buf)  # M <- mu M + G, one pass
                 if p.dim() == 2:
-                    buckets[(tuple(p.shape), upd.dtype, upd.device)].append((p, upd))
+                    buckets[(tuple(p.shape), g.dtype, g.device)].append(p)
                 else:
                     if wd:
                         p.mul_(1.0 - lr * wd)
-                    p.add_(upd, alpha=-lr)
-            for (shape, _, _), items in buckets.items():
+                    p.add_(g.add(buf, alpha=mu) if nesterov else buf, alpha=-lr)
+            for (shape, dtype, device), items in buckets.items():
                 rows, cols = shape
-                stacked = torch.stack([u for _, u in items]).contiguous()
+                # the update of every matrix of the group is written straight into the stacked batch
+                stacked = torch.empty((len(items), rows, cols), dtype=dtype, device=device)
+                for i, p in enumerate(items):
+                    buf = self.state[p]["momentum_buffer"]
+                    if nesterov:
+                        torch.add(p.grad, buf, alpha=mu, out=stacked[i])
+                    else:
+                        stacked[i].copy_(buf)
+                zero = torch.linalg.vector_norm(stacked.flatten(1), ord=float("inf"), dim=1) == 0
                 ortho = self._ortho(stacked)
-                zero = stacked.flatten(1).abs().amax(1) == 0     # zero update -> zero step (not degenerate)
-                if bool(zero.any()):
+                if bool(zero.any()):  # zero update -> zero step (not a degenerate input)
                     ortho = torch.where(zero[:, None, None], torch.zeros_like(ortho), ortho)
                 scale = math.sqrt(max(1.0, rows / cols))
-                for (p, _), o in zip(items, ortho):
-                    if wd:
-                        p.mul_(1.0 - lr * wd)
-                    p.add_(o.to(p.dtype), alpha=-lr * scale)
+                if wd:
+                    torch._foreach_mul_(items, 1.0 - lr * wd)
+                torch._foreach_add_(items, [o.to(items[0].dtype) for o in ortho.unbind(0)], alpha=-lr * scale)
         return loss
 
 
