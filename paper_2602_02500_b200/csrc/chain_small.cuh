@@ -12,6 +12,10 @@
 // Same arithmetic as chain_persistent (C-form, fp32 C and P resident in TMEM, bf16x3 products,
 // the truncation test of SURVEY 8f-4 and the adaptive-apply decision), same outputs: scal[b],
 // status[b], and the shifted symmetric P/s as bf16 hi/lo in the padded workspace layout.
+//
+// FUSED_GRAM: the CTA also computes G = X^T X itself (tall bf16 X, w rows): warp 0 streams 64-row
+// MN-major tiles of X through the (still idle) operand buffers as a 4-stage TMA pipeline, the MMA
+// warp accumulates G in TMEM, and phase A reads G from TMEM -- no Gram launch, no split-K partials.
 #pragma once
 #include "chain_persistent.cuh"
 
@@ -30,14 +34,23 @@ __device__ __forceinline__ uint32_t cs_offset(int r, int c) {
   return static_cast<uint32_t>(chunk * CS_CHUNK + r * 128 + ((((byte >> 4) ^ (r & 7))) << 4) + (byte & 15));
 }
 
-__global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid_constant__ ChainParams p) {
+struct SmallGram {
+  CUtensorMap x;  // MN-major bf16 map of the tall X (box {64, 64}), batch in the 3rd dimension
+  int w;          // rows of X (the contraction length)
+};
+
+template <bool FUSED_GRAM>
+__global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid_constant__ ChainParams p,
+                                                                     const __grid_constant__ SmallGram sg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* c_hi = smem;
   uint8_t* c_lo = smem + CS_OPERAND;
   uint64_t* ready = reinterpret_cast<uint64_t*>(smem + 2 * CS_OPERAND);  // operands of C_k written
-  uint64_t* tfull = ready + 1;                                             // C_k^2 accumulated
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = ready + 1;                                             // C_k^2 (or G) accumulated
+  uint64_t* gfull = tfull + 1;                                             // [4] Gram stages loaded
+  uint64_t* gempty = gfull + 4;                                            // [4] Gram stages consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gempty + 4);
   __shared__ double red[2][CS_EPI_WARPS];
   __shared__ double s_scale[2];
   __shared__ int s_stop;
@@ -48,6 +61,11 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
   if (warp == 0 && lane == 0) {
     mbar_init(ready, CS_EPI);
     mbar_init(tfull, 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&gfull[i], 1);
+      mbar_init(&gempty[i], 1);
+    }
+    if (FUSED_GRAM) tma_prefetch_desc(&sg.x);
     fence_mbar_init();
     s_stop = 0;
   }
@@ -58,12 +76,40 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 128) CHAIN_TRACE(0, 0);
 
-  if (warp == 1) {
+  const int gk = FUSED_GRAM ? (sg.w + 63) / 64 : 0;  // 64-row k-blocks of X
+  if (FUSED_GRAM && warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ Gram producer (4 x 16 KB stages)
+      for (int kt = 0; kt < gk; ++kt) {
+        const int s = kt & 3;
+        mbar_wait(&gempty[s], ((kt >> 2) & 1) ^ 1);
+        mbar_arrive_expect_tx(&gfull[s], 16384);
+        load_operand_tile<true, 128>(&sg.x, &gfull[s], smem + s * 16384, kt * 64, 0, b);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
     if (lane == 0) {
       // ---------------------------------------------------------------- MMA issuer
       const uint32_t idesc = idesc_bf16(128, 128, 0, 0);
       const uint32_t hi = smem_u32(c_hi), lo = smem_u32(c_lo);
       uint32_t phase = 0;
+      if (FUSED_GRAM) {  // G = X^T X into the accumulator (A = B = the MN-major X tile)
+        const uint32_t gdesc = idesc_bf16(128, 128, 1, 1);
+        for (int kt = 0; kt < gk; ++kt) {
+          const int s = kt & 3;
+          mbar_wait(&gfull[s], (kt >> 2) & 1);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + s * 16384);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t d = operand_desc<true>(st, ks);
+            umma_bf16(tmem + CH_ACC, d, d, gdesc, (kt > 0 || ks > 0) ? 1u : 0u);
+          }
+          umma_commit(&gempty[s]);
+        }
+        umma_commit(tfull);
+      }
       for (int k = 1; k < N; ++k) {
         mbar_wait(ready, phase);  // C_k's operands in shared memory (and the truncation verdict)
         phase ^= 1;
@@ -129,7 +175,12 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
     // over the idle operand buffers, 16-byte chunks XOR-swizzled by row so the row-per-lane reads
     // below are conflict-free.
     float* gs = reinterpret_cast<float*>(c_hi);
-    {
+    uint32_t acc_phase = 0;
+    if (FUSED_GRAM) {
+      mbar_wait(tfull, 0);
+      acc_phase = 1;
+      tc_fence_after();
+    } else {
       constexpr int PER = 128 * 32 / CS_EPI;  // float4 positions per thread
       float4 acc[PER];
 #pragma unroll
@@ -156,19 +207,25 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
         *reinterpret_cast<float4*>(gs + rr * 128 + ((c4 ^ (rr & 7)) << 2)) = acc[q];
       }
     }
-    if (tid == 0) CHAIN_TRACE(60, 0);
     named_bar_sync(1, CS_EPI);
-    if (tid == 0) CHAIN_TRACE(60, 1);
     double tr = 0.0, fr = 0.0;
     for (int c = c_begin; c < c_end; ++c) {
       float g[32];
+      if (FUSED_GRAM) {
+        uint32_t u[32];
+        tmem_ld32(lane_base + CH_ACC + c * 32, u);
+        tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(gs + r * 128 + (((c * 8 + j / 4) ^ (r & 7)) << 2));
-        g[j] = v.x;
-        g[j + 1] = v.y;
-        g[j + 2] = v.z;
-        g[j + 3] = v.w;
+        for (int j = 0; j < 32; ++j) g[j] = __uint_as_float(u[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(gs + r * 128 + (((c * 8 + j / 4) ^ (r & 7)) << 2));
+          g[j] = v.x;
+          g[j + 1] = v.y;
+          g[j + 2] = v.z;
+          g[j + 3] = v.w;
+        }
       }
       uint32_t u[32];
 #pragma unroll
@@ -182,9 +239,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
       tmem_st32(lane_base + CH_C + c * 32, u);
     }
     tmem_wait_st();
-    if (tid == 0) CHAIN_TRACE(60, 2);
     reduce2(tr, fr);
-    if (tid == 0) CHAIN_TRACE(60, 3);
     if (tid == 0) {
       const double s0 = total(0), s1 = total(1);
       double s2 = p.scal_mode == SM_PLAIN ? s0 : sqrt(s1);
@@ -227,7 +282,6 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
     if (tid == 0) CHAIN_TRACE(0, 1);
 
     // ---- squarings
-    uint32_t acc_phase = 0;
     int steps = 0;
     for (int k = 1; k < N; ++k) {
       const bool last = k == N - 1;

@@ -1227,23 +1227,49 @@ static bool chain_small_fits(const Problem& p) {
          std::getenv("UNSO_NO_SMALL_CHAIN") == nullptr;
 }
 
+// `xb` non-null: the kernel also computes the Gram of the tall bf16 X itself (FUSED_GRAM); `part`
+// is then unused.  Otherwise phase A reads the split-K partials (or a dense reduced Gram).
 static int32_t scale_chain_bf16_small(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
-                                      int64_t part_ld, int64_t part_mat, int32_t* status, cudaStream_t st) {
+                                      int64_t part_ld, int64_t part_mat, int32_t* status, cudaStream_t st,
+                                      const __nv_bfloat16* xb = nullptr, int64_t ldx = 0, int64_t bsx = 0) {
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(chain_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CS_SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(chain_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CS_SMEM) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(chain_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CS_SMEM) !=
+            cudaSuccess)
       return UNSO_ERR_CUDA;
     configured = true;
   }
   ChainParams cp = chain_params(p, pl, ws, part, splits, part_ld, part_mat, status);
-  prof_mark(3, st);
+  SmallGram sg;
+  std::memset(&sg, 0, sizeof(sg));
+  if (xb) {
+    if (!umma_make_mnmajor_map(&sg.x, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
+    sg.w = static_cast<int>(p.w);
+  } else {
+    prof_mark(3, st);
+  }
   cp.b0 = 0;
-  chain_small_kernel<<<static_cast<unsigned>(p.batch), CS_THREADS, CS_SMEM, st>>>(cp);
+  if (xb)
+    chain_small_kernel<true><<<static_cast<unsigned>(p.batch), CS_THREADS, CS_SMEM, st>>>(cp, sg);
+  else
+    chain_small_kernel<false><<<static_cast<unsigned>(p.batch), CS_THREADS, CS_SMEM, st>>>(cp, sg);
   UNSO_CHECK_LAUNCH();
   ++g_launches;
+  if (xb) {
+    prof_mark(2, st);
+    prof_mark(3, st);
+  }
   prof_mark(4, st);
   prof_mark(5, st);
   return UNSO_OK;
+}
+
+// tall bf16 X with h <= 128 and few enough rows that one CTA per matrix does the Gram too
+static bool small_fused_gram(const Problem& p) {
+  return chain_small_fits(p) && p.tall && p.w <= 8192 && use_pair_engine() &&
+         std::getenv("UNSO_NO_FUSED_SMALL_GRAM") == nullptr;
 }
 
 // Which scale+chain implementation a BF16 UNSO problem takes.
@@ -1565,6 +1591,10 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
   int64_t ldx, bsx;
   UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
   prof_mark(1, st);
+  if (p.method == UNSO_METHOD_UNSO && bf16_route(p) == ROUTE_SMALL && small_fused_gram(p)) {
+    UNSO_TRY(scale_chain_bf16_small(p, pl, workspace, nullptr, 1, 0, 0, d_status, st, xb, ldx, bsx));
+    return apply_bf16(p, pl, workspace, xb, ldx, bsx, y_ptr, st);
+  }
   const bool split_out = bf16_route(p) == ROUTE_GLUE_FREE && pl.splits == 1;
   if (split_out)
     UNSO_TRY(gram_bf16_split(p, pl, workspace, xb, ldx, bsx, st));
