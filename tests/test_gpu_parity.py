@@ -215,6 +215,35 @@ def test_cfg2_full_fp32_mode():
     assert worst <= TOL["fp32"]
 
 
+@pytest.mark.parametrize("method", ["unso", "muon5"])
+def test_cfg2_singular_value_map(method):
+    """configs[1]'s stated purpose: the singular values of Y are the scalar map applied to the
+    (scaled) singular values of X, g^N(s) (`scalar_map` ortho.py:286-310).  Y's spectrum is taken
+    in fp64 on the device; the expected map is evaluated from the fp64 spectrum of the same
+    (mode-rounded) input.  fp32 mode: |d sigma| <= 1e-5; bf16 mode: <= 2e-2."""
+    rng = np.random.default_rng(2)
+    ms = np.stack([O.controlled_spectrum_matrix(2048, 512, np.exp(rng.uniform(np.log(1e-4), 0, 512)), 100 + i)
+                   for i in range(16)]).astype(np.float32)
+    spec = (U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()) if method == "unso"
+            else U.MethodSpec(U.MethodKind.MUON_NS, iterations=5))
+    fmap = U.scalar_map(spec)
+    for precision, dtype in (("fp32", torch.float32), ("bf16", torch.bfloat16)):
+        x = torch.from_numpy(ms).to(DEV, dtype)
+        res = U.orthogonalize(x, spec, precision=precision)
+        sy = torch.linalg.svdvals(res.y.double()).cpu().numpy()
+        sx = torch.linalg.svdvals(x.double()).cpu().numpy()
+        if method == "unso":   # gram scaling: X / ||X^T X||_F^(1/2)
+            scale = (sx ** 4).sum(axis=1, keepdims=True) ** 0.25
+        else:                  # plain scaling: X / ||X||_F
+            scale = np.sqrt((sx ** 2).sum(axis=1, keepdims=True))
+        want = np.sort(fmap(sx / scale), axis=1)[:, ::-1]
+        got = np.sort(sy, axis=1)[:, ::-1]
+        err = float(np.abs(got - want).max())
+        print(f"cfg2 {method} {precision}: max |sigma(Y) - g(sigma(X))| = {err:.2e} "
+              f"(sigma(Y) in [{got.min():.3e}, {got.max():.3e}])")
+        assert err <= TOL[precision], (precision, err)
+
+
 @pytest.mark.parametrize("shape,scale,seed", [((4096, 1024), 1.0, 5), ((1024, 1024), 0.02, 6), ((640, 1536), 1.0, 7)])
 def test_bf16_mode_gaussian_shapes(shape, scale, seed):
     m = (O.gaussian_matrix(*shape, seed) * scale).astype(np.float32)
