@@ -53,6 +53,9 @@ def parse_args():
     ap.add_argument("--ref-sample-rows", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the row-sharded multi-rank path (process group, Gram reduction) even at world size 1; "
+                         "used to exercise the N > 1 code under torchrun on a single GPU")
     return ap.parse_args()
 
 
@@ -197,11 +200,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier()
 
     rows, cols = args.rows, args.cols
@@ -216,14 +220,14 @@ def main():
     y = torch.empty_like(x)
 
     def step():
-        if world == 1:
+        if not sharded:
             U.orthogonalize(x, spec, out=y, check=False)
         else:
             orthogonalize_row_sharded(x, spec, out=y, check=False, collective=args.collective)
 
     # ---- correctness gate (untimed): status + orthogonality of the output
     apply_info = None
-    if world == 1:
+    if not sharded:
         res = U.orthogonalize(x, spec, out=y, check=True)
         launches_per_step = res.launches
         apply_info = res.info[0] if res.info else None
@@ -231,11 +235,29 @@ def main():
         orthogonalize_row_sharded(x, spec, out=y, check=True, collective=args.collective)
         launches_per_step = None
     torch.cuda.synchronize()
-    ortho_err = float(U.ortho_error_device(y)[0]) if world == 1 else None
+    if not sharded:
+        ortho_err = float(U.ortho_error_device(y)[0])
+    else:   # untimed check: ||Y^T Y - I||_F with the shard Grams summed over the group
+        yf = y.float()
+        gy = (yf.T @ yf) if rows > cols else (yf @ yf.T)
+        dist.all_reduce(gy)
+        gy -= torch.eye(gy.shape[0], device=dev)
+        ortho_err = float(torch.linalg.norm(gy))
     if launches_per_step is None:
-        launches_per_step = 0
-        # gram + finish: count from the library's per-call counters
-        U.distributed.native_gram(x, spec, None)
+        # our kernels per step, from the library's per-call counters: the Gram stage (or the
+        # push / reduce / wait kernels of the peer-memory reduction) plus the finish stage
+        if args.collective == "nccl":
+            g = U.distributed.native_gram(x, spec, None)
+            launches_per_step = N.launch_count()
+        else:
+            red = U.distributed._nvlink_reducer(cols, x.shape[0], None, dev)
+            red.push(x, spec, None)
+            launches_per_step = N.launch_count()
+            red.reduce()
+            launches_per_step += N.launch_count()
+            g = red.wait()
+            launches_per_step += N.launch_count()
+        U.distributed.native_finish(x, g, spec, None, y)
         launches_per_step += N.launch_count()
         torch.cuda.synchronize()
 
@@ -250,7 +272,7 @@ def main():
     time.sleep(0.2)
     stream = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    prof = N.StageProfiler(args.steps) if world == 1 else None
+    prof = N.StageProfiler(args.steps) if not sharded else None
     if prof:
         prof.__enter__()
     barrier()
@@ -270,7 +292,7 @@ def main():
     time.sleep(0.1)
     sampler.stop()
     ms_t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-    if world > 1:
+    if sharded:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_total = float(ms_t.item())
     ms_step = ms_total / args.steps
@@ -308,7 +330,7 @@ def main():
                 s_cmp.wait_event(ev_h2d[j])
                 if started[j]:
                     s_cmp.wait_event(ev_d2h[j])      # step i-2's result left yd[j]
-                if world == 1:
+                if not sharded:
                     U.orthogonalize(xd[j], spec, out=yd[j], check=False)
                 else:
                     orthogonalize_row_sharded(xd[j], spec, out=yd[j], check=False, collective=args.collective)
@@ -331,7 +353,7 @@ def main():
         e1.record(s_d2h)
         torch.cuda.synchronize()
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
+        if sharded:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e_ms = float(et.item()) / args.e2e_steps
         nbytes = x.numel() * x.element_size()
@@ -382,7 +404,7 @@ def main():
                                                 args.apply_terms] + " apply")
                        if args.precision == "bf16" else "fp64-grade DFMA",
                        "parallelism": (f"row-shard x{world} + " + ("NCCL all-reduce of G" if args.collective == "nccl" else
-                                 "NVLink peer-memory reduction of G")) if world > 1 else "1 GPU",
+                                 "NVLink peer-memory reduction of G")) if sharded else "1 GPU",
                        "l2": "input 1 GiB > 126 MB L2 (no flush needed)"},
             "matrices_per_s": 1e3 / ms_step,
             "pct_bf16_peak": value / peak,
@@ -400,7 +422,7 @@ def main():
                 "shift": apply_info["shift"]},
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 

@@ -249,7 +249,7 @@ def orthogonalize_row_sharded(x_local: torch.Tensor, spec: MethodSpec, *, group=
             raise DegenerateInputError("input is identically zero or the scaling denominator is not positive finite")
         return y
     g = stages.gram(x_local, spec, precision)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)
     y, status = stages.finish(x_local, g, spec, precision, out)
     if check and status is not None and bool((status != 0).any()):
