@@ -48,7 +48,8 @@ def parse_args():
                     help="N > 1: Gram all-reduce through NCCL, or the peer-memory reduction (unso_gram_push/...)")
     ap.add_argument("--apply-terms", type=int, choices=[1, 2], default=None,
                     help="bf16 apply split: default adaptive per matrix (device-side bound)")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30,
+                    help="pipelined e2e steps (fill and drain of the three-stream pipeline amortised over them)")
     ap.add_argument("--cpu-sample-rows", type=int, default=32768)
     ap.add_argument("--ref-sample-rows", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -1,0 +1,109 @@
+"""Full-size parity at BASELINE.json's own shapes, through the size-independent property of the
+path: Y = X P(X^T X) has the singular vectors of X and singular values g(sigma), the method's
+scalar map (`scalar_map` ortho.py:286-310) applied to the scaled singular values of X.  The CPU
+oracle cannot run these sizes in seconds (~100 s per cfg3 layer / cfg5 matrix), so
+the check is sigma(Y) against g(sigma(X)) with both spectra taken in fp64 on the device (a
+checker, not the product path), plus the orthogonality error ||Y^T Y - I||_F = sqrt(sum
+(sigma_i^2 - 1)^2) next to the value exact arithmetic gives for the same input (the reference's
+own value in exact arithmetic).  Inputs are seeded synthetic matrices with BASELINE's shapes and
+distributions.  Tolerances: max |sigma(Y) - g(sigma(X))| <= 2e-2 in bf16 mode, <= 1e-5 in fp32
+mode (sigma(Y) lies in [0, ~1.2])."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_02500_b200 as U
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+TOL = {"fp32": 1e-5, "bf16": 2e-2}
+
+
+def spectrum_gram(z: torch.Tensor) -> np.ndarray:
+    """Singular values from the eigenvalues of the short-side Gram (fp64); accurate to ~1e-7
+    absolute, ample for the bf16-mode bar."""
+    z = z.double()
+    g = z.T @ z if z.shape[0] >= z.shape[1] else z @ z.T
+    ev = torch.linalg.eigvalsh(g).clamp_min(0.0)
+    return torch.sqrt(ev).flip(0).cpu().numpy()
+
+
+def spectrum_svd(z: torch.Tensor) -> np.ndarray:
+    return torch.linalg.svdvals(z.double()).cpu().numpy()
+
+
+def check_map(x, y, spec, precision, spectrum=spectrum_gram, label=""):
+    sx = spectrum(x)
+    sy = spectrum(y)
+    if spec.effective_scaling is U.Scaling.FROBENIUS_GRAM:
+        scale = float((sx ** 4).sum()) ** 0.25
+    else:
+        scale = float(np.sqrt((sx ** 2).sum()))
+    want = np.sort(U.scalar_map(spec)(sx / scale))[::-1]
+    got = np.sort(sy)[::-1]
+    err = float(np.abs(got - want).max())
+    ortho = float(np.sqrt(((got ** 2 - 1.0) ** 2).sum()))
+    ortho_exact = float(np.sqrt(((want ** 2 - 1.0) ** 2).sum()))
+    print(f"{label} {precision}: max |sigma(Y) - g(sigma(X))| = {err:.2e}; ortho error {ortho:.6f} "
+          f"(exact arithmetic on this input: {ortho_exact:.6f})")
+    assert err <= TOL[precision], (label, precision, err)
+    return err
+
+
+def gaussian(rows, cols, std, seed, dtype):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    return (torch.randn(rows, cols, generator=g, device=DEV) * std).to(dtype)
+
+
+def pareto_spectrum_matrix(rows, cols, seed):
+    """configs[4]: X = U diag(s) V^T, Haar U, V; s = 1 + Pareto(1.5) min-max rescaled to [1e-6, 1]."""
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    k = min(rows, cols)
+
+    def haar(n):
+        q, r = torch.linalg.qr(torch.randn(n, k, generator=g, device=DEV, dtype=torch.float64))
+        return q * torch.sign(torch.diagonal(r))
+    rng = np.random.default_rng(seed)
+    s = 1.0 + rng.pareto(1.5, k)
+    s = 1e-6 + (s - s.min()) / (s.max() - s.min()) * (1.0 - 1e-6)
+    st = torch.from_numpy(s).to(DEV)
+    return (haar(rows) * st[None, :]) @ haar(cols).T
+
+
+SPECS = {
+    "unso": lambda: U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()),
+    "muon5": lambda: U.MethodSpec(U.MethodKind.MUON_NS, iterations=5),
+}
+
+
+@pytest.mark.parametrize("method", ["unso", "muon5"])
+@pytest.mark.parametrize("shape", [(4096, 4096), (14336, 4096), (4096, 14336)])
+def test_cfg3_layer_shapes(shape, method):
+    """configs[2]: the three layer shapes (q/k/v/o square, up/gate tall, down wide), bf16,
+    N(0, 0.02^2) gradient-like entries."""
+    x = gaussian(*shape, 0.02, 7 * shape[0] + shape[1], torch.bfloat16)
+    res = U.orthogonalize(x, SPECS[method](), precision="bf16")
+    check_map(x, res.y, SPECS[method](), "bf16", label=f"cfg3 {shape[0]}x{shape[1]} {method}")
+
+
+@pytest.mark.parametrize("method", ["unso", "muon5"])
+def test_cfg4_full(method):
+    """configs[3]: one 262144 x 2048 bf16 N(0, 1) matrix."""
+    x = gaussian(262144, 2048, 1.0, 1234, torch.bfloat16)
+    res = U.orthogonalize(x, SPECS[method](), precision="bf16")
+    check_map(x, res.y, SPECS[method](), "bf16", label=f"cfg4 {method}")
+
+
+@pytest.mark.parametrize("method", ["unso", "muon5"])
+def test_cfg5_full_bf16_and_fp32(method):
+    """configs[4]: 16384 x 8192 fp32 with the heavy-tailed Pareto spectrum, both modes (one of the
+    batch of four; the batch path is covered at reduced size in test_gpu_parity)."""
+    x = pareto_spectrum_matrix(16384, 8192, 5).float()
+    spec = SPECS[method]()
+    res = U.orthogonalize(x, spec, precision="bf16")
+    xb = x.to(torch.bfloat16)   # the values the bf16 mode computes on
+    check_map(xb, res.y, spec, "bf16", label=f"cfg5 {method}")
+    res = U.orthogonalize(x, spec, precision="fp32")
+    # fp32 bar: tiny singular values (1e-6) need the SVD, not the Gram's eigenvalues
+    check_map(x, res.y, spec, "fp32", spectrum=spectrum_svd, label=f"cfg5 {method}")
