@@ -244,6 +244,18 @@ def main():
         dist.all_reduce(gy)
         gy -= torch.eye(gy.shape[0], device=dev)
         ortho_err = float(torch.linalg.norm(gy))
+    # The reference's own orthogonality error on this input: Y_ref = X P(X^T X) has singular values
+    # g(sigma(X)) (the scalar map, ortho.py:286-310), so ||Y_ref^T Y_ref - I||_F follows from the
+    # spectrum of X (fp64 Gram, summed over the shards, eigenvalues on the device; untimed).
+    xg = x.double()
+    gx = (xg.T @ xg) if rows > cols else (xg @ xg.T)
+    del xg
+    if sharded:
+        dist.all_reduce(gx)
+    sx = torch.sqrt(torch.linalg.eigvalsh(gx).clamp_min(0.0)).cpu().numpy()
+    del gx
+    sy = U.scalar_map(spec)(sx / float((sx ** 4).sum()) ** 0.25)
+    ortho_ref = float(np.sqrt(((sy ** 2 - 1.0) ** 2).sum()))
     if launches_per_step is None:
         # our kernels per step, from the library's per-call counters: the Gram stage (or the
         # push / reduce / wait kernels of the peer-memory reduction) plus the finish stage
@@ -418,6 +430,9 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "ortho_error": ortho_err,
+            "ortho_error_reference": ortho_ref,
+            "ortho_error_reference_how": "exact-arithmetic value of the reference polynomial on this input: "
+                                         "sqrt(sum (g(sigma_i)^2 - 1)^2), sigma from the fp64 Gram of X",
             "apply_decision": None if apply_info is None else {
                 "single_term": bool(apply_info["apply_single"]), "bound": apply_info["apply_bound"],
                 "shift": apply_info["shift"]},

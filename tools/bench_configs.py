@@ -55,6 +55,22 @@ def rel(a, b):
     return float((a.double() - b.double()).norm() / b.double().norm())
 
 
+def ortho_pair(x0, y0, spec):
+    """(ours, reference) orthogonality error ||Y^T Y - I||_F of matrix 0: ours from Y; the
+    reference's from the scalar map of sigma(X) (Y_ref = X P(X^T X) has singular values g(sigma)),
+    i.e. its exact-arithmetic value on the same input.  Spectra from fp64 Grams on the device."""
+    def gram(z):
+        z = z.double()
+        return z.T @ z if z.shape[0] >= z.shape[1] else z @ z.T
+    gy = gram(y0)
+    ours = float((gy - torch.eye(gy.shape[0], device=gy.device, dtype=gy.dtype)).norm())
+    sx = torch.sqrt(torch.linalg.eigvalsh(gram(x0)).clamp_min(0.0)).cpu().numpy()
+    scale = float((sx ** 4).sum()) ** 0.25 if spec.effective_scaling is U.Scaling.FROBENIUS_GRAM else \
+        float(np.sqrt((sx ** 2).sum()))
+    sy = U.scalar_map(spec)(sx / scale)
+    return ours, float(np.sqrt(((sy ** 2 - 1.0) ** 2).sum()))
+
+
 def run(name, x, spec, precision, nmat, h, w, reps=3, check_against=None):
     ms = timed(lambda: U.orthogonalize(x, spec, precision=precision, check=False), reps=reps)
     f = U.kernel_model_flops(h, w, spec) * nmat
@@ -65,6 +81,10 @@ def run(name, x, spec, precision, nmat, h, w, reps=3, check_against=None):
         out["apply_single"] = [bool(i["apply_single"]) for i in res.info][:4]
     if check_against is not None:
         out["rel_vs_fp64_path"] = rel(res.y, check_against)
+    x0 = x if x.dim() == 2 else x[0]
+    y0 = res.y if res.y.dim() == 2 else res.y[0]
+    out["ortho_error"], out["ortho_error_reference"] = ortho_pair(
+        x0.to(torch.bfloat16) if precision == "bf16" else x0, y0, spec)
     print(json.dumps(out), flush=True)
     return out
 
