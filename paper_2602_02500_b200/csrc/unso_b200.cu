@@ -697,9 +697,10 @@ static int scal_mode(int scaling) {
 // Returns false when the problem does not qualify (the caller then runs the per-step launches).
 static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, const double* G, int32_t* status,
                                  cudaStream_t st) {
+  static const bool no_f64_chain = std::getenv("UNSO_NO_F64_CHAIN") != nullptr;  // developer override, read once
   // rows are pulled with 16-byte-granular bulk copies: h must be even
   if (p.h > CF_MAX_H || (p.h & 1) || p.order < 2 || p.order > CHAIN_MAX_ORDER ||
-      p.scaling == UNSO_SCALING_GELFAND || std::getenv("UNSO_NO_F64_CHAIN"))
+      p.scaling == UNSO_SCALING_GELFAND || no_f64_chain)
     return false;
   const int h = static_cast<int>(p.h);
   const int T = cf_tile(h);
@@ -1223,8 +1224,9 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
 
 // h <= 128: one CTA per matrix, the chain entirely on chip (chain_small.cuh).
 static bool chain_small_fits(const Problem& p) {
+  static const bool no_small_chain = std::getenv("UNSO_NO_SMALL_CHAIN") != nullptr;  // developer override
   return p.h <= 128 && p.order >= 1 && p.order <= CHAIN_MAX_ORDER && p.scaling != UNSO_SCALING_GELFAND &&
-         std::getenv("UNSO_NO_SMALL_CHAIN") == nullptr;
+         !no_small_chain;
 }
 
 // `xb` non-null: the kernel also computes the Gram of the tall bf16 X itself (FUSED_GRAM); `part`
@@ -1268,14 +1270,16 @@ static int32_t scale_chain_bf16_small(const Problem& p, const Plan& pl, void* ws
 
 // tall bf16 X with h <= 128 and few enough rows that one CTA per matrix does the Gram too
 static bool small_fused_gram(const Problem& p) {
+  static const bool no_fused = std::getenv("UNSO_NO_FUSED_SMALL_GRAM") != nullptr;  // developer override
   return chain_small_fits(p) && p.tall && p.w <= 8192 && use_pair_engine() &&
-         std::getenv("UNSO_NO_FUSED_SMALL_GRAM") == nullptr;
+         !no_fused;
 }
 
 // Which scale+chain implementation a BF16 UNSO problem takes.
 enum Bf16Route { ROUTE_SMALL, ROUTE_PERSISTENT, ROUTE_GLUE_FREE, ROUTE_LEGACY };
 static Bf16Route bf16_route(const Problem& p) {
-  if (const char* f = std::getenv("UNSO_BF16_ROUTE")) {  // developer override (A/B timing)
+  static const char* const route_override = std::getenv("UNSO_BF16_ROUTE");  // developer override (A/B timing)
+  if (const char* f = route_override) {
     if (!std::strcmp(f, "glue") && use_pair_engine() && p.order >= 2 && p.scaling != UNSO_SCALING_GELFAND)
       return ROUTE_GLUE_FREE;
     if (!std::strcmp(f, "persistent") && chain_persistent_fits(p)) return ROUTE_PERSISTENT;
