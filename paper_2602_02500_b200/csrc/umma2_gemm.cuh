@@ -105,11 +105,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   if (work.mode_flag && work.mode_want >= 0) {
     // Both CTAs of the pair see the same items: if none passes the filter, leave before any
     // barrier / TMEM setup (the companion launch of the adaptive apply then costs ~a launch).
+    // Items are batch-major (T per matrix): walk the matrices this cluster has items in, one flag
+    // read per matrix (not per item: an all-filtered launch then costs ~a launch).
     bool any = false;
-    for (int idx = cluster; idx < work.num_work && !any; idx += nclusters) {
-      int b, split, tm, tn, kt0, kt1;
-      umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
-      any = !filtered_out(work, b);
+    const int T = work.num_work / work.batch;
+    const int blast = (cluster < work.num_work) ? (work.num_work - 1 - (work.num_work - 1 - cluster) % nclusters) / T : -1;
+    for (int b = (cluster < work.num_work ? cluster / T : 0); b <= blast && !any; ++b) {
+      const int base = b * T;
+      const int i0 = base + ((cluster - base) % nclusters + nclusters) % nclusters;
+      if (i0 < base + T) any = !filtered_out(work, b);
     }
     if (!any) return;
   }
