@@ -9,6 +9,13 @@ transformer step (224 matrices of 4096 x {4096, 14336}) tensor-core bound instea
 
 The orthogonalizer is any MethodSpec of this package: the learned UNSO polynomial (default) or the
 NS/Muon quintic iteration.  Non-2-D parameters are updated with plain momentum SGD.
+
+Data-parallel use (BASELINE configs[2] "grouped batch distributed across 1/2/4/8 GPUs"): with
+``process_group`` set (or the default group initialised and ``distribute=True``), every rank holds
+the same (all-reduced) gradients, each shape group is split into contiguous, equal shares of its
+matrices, every rank orthogonalizes only its share, and the results are all-gathered before the
+identical update on every rank.  Equal shapes cost the same, so equal shares are the LPT optimum
+within a group; no communication besides the one all-gather per group.
 """
 
 from __future__ import annotations
@@ -18,6 +25,7 @@ from collections import defaultdict
 from typing import Callable, Iterable
 
 import torch
+import torch.distributed as dist
 
 from .ortho import MethodKind, MethodSpec, orthogonalize
 from .scalarpoly import default_coefficients
@@ -43,11 +51,14 @@ class Muon(torch.optim.Optimizer):
         spec: MethodSpec of the orthogonalizer (default: UNSO with the shipped coefficients).
         precision: "bf16" (tensor cores) or "fp32" (fp64-grade parity path).
         orthogonalize_fn: override (stacked 3-D tensor -> stacked result); for testing.
+        process_group: process group over which the orthogonalizations are shared (data parallel).
+        distribute: share the work over the default group when it is initialised (default False;
+            implied by process_group).
     """
 
     def __init__(self, params: Iterable, lr: float = 0.02, momentum: float = 0.95, nesterov: bool = True,
                  weight_decay: float = 0.0, spec: MethodSpec | None = None, precision: str = "bf16",
-                 orthogonalize_fn: Callable | None = None):
+                 orthogonalize_fn: Callable | None = None, process_group=None, distribute: bool = False):
         if lr <= 0.0:
             raise ValueError("lr must be positive")
         if not 0.0 <= momentum < 1.0:
@@ -58,6 +69,29 @@ class Muon(torch.optim.Optimizer):
         self.precision = precision
         self._ortho = orthogonalize_fn or (
             lambda u: orthogonalize(u, self.spec, precision=self.precision, check=False).y)
+        self.process_group = process_group
+        self.distribute = distribute or process_group is not None
+
+    def _orthogonalize_group(self, stacked: torch.Tensor) -> torch.Tensor:
+        """Orthogonalize a stacked group; under data parallelism each rank does an equal contiguous
+        share and the shares are all-gathered (same result on every rank)."""
+        if not self.distribute or not (dist.is_available() and dist.is_initialized()):
+            return self._ortho(stacked)
+        world, rank = dist.get_world_size(self.process_group), dist.get_rank(self.process_group)
+        n = stacked.shape[0]
+        per = -(-n // world)
+        lo, hi = min(n, rank * per), min(n, (rank + 1) * per)
+        mine = torch.zeros((per,) + tuple(stacked.shape[1:]), dtype=stacked.dtype, device=stacked.device)
+        if hi > lo:
+            mine[: hi - lo] = self._ortho(stacked[lo:hi])
+        if dist.get_backend(self.process_group) == "nccl":
+            full = torch.empty((world * per,) + tuple(stacked.shape[1:]), dtype=stacked.dtype, device=stacked.device)
+            dist.all_gather_into_tensor(full, mine, group=self.process_group)
+        else:
+            parts = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(parts, mine, group=self.process_group)
+            full = torch.cat(parts)
+        return full[:n]
 
     @torch.no_grad()
     def step(self, closure=None):
@@ -94,7 +128,7 @@ class Muon(torch.optim.Optimizer):
                     else:
                         stacked[i].copy_(buf)
                 zero = torch.linalg.vector_norm(stacked.flatten(1), ord=float("inf"), dim=1) == 0
-                ortho = self._ortho(stacked)
+                ortho = self._orthogonalize_group(stacked)
                 if bool(zero.any()):  # zero update -> zero step (not a degenerate input)
                     ortho = torch.where(zero[:, None, None], torch.zeros_like(ortho), ortho)
                 scale = math.sqrt(max(1.0, rows / cols))

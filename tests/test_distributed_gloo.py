@@ -73,6 +73,38 @@ def _worker_batch(rank, world, port, mats, q):
     dist.destroy_process_group()
 
 
+def _muon_params(seed):
+    g = torch.Generator().manual_seed(seed)
+    shapes = [(24, 16)] * 5 + [(16, 40)] * 2 + [(9,)]
+    params = [torch.nn.Parameter(torch.randn(*sh, generator=g, dtype=torch.float64)) for sh in shapes]
+    grads = [torch.randn(*sh, generator=g, dtype=torch.float64) for sh in shapes]
+    return params, grads
+
+
+def _oracle_stacked(calls):
+    def fn(t):
+        calls.append(int(t.shape[0]))
+        return torch.from_numpy(np.stack([O.run(a.numpy(), "unso")["y"] for a in t]))
+    return fn
+
+
+def _worker_muon(rank, world, port, q):
+    from paper_2602_02500_b200.muon import Muon
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    params, grads = _muon_params(3)
+    calls = []
+    opt = Muon(params, lr=0.05, momentum=0.9, weight_decay=0.01, orthogonalize_fn=_oracle_stacked(calls),
+               distribute=True)
+    for step in range(2):                      # two steps: the momentum buffer carries over
+        for p, g in zip(params, grads):
+            p.grad = g * (step + 1)
+        opt.step()
+    q.put((rank, calls, [p.detach().numpy() for p in params]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def _spawn(target, world, *args):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -81,7 +113,7 @@ def _spawn(target, world, *args):
     for p in procs:
         p.start()
     results = []
-    n_expected = world if target is _worker_row_shard else 1
+    n_expected = world if target in (_worker_row_shard, _worker_muon) else 1
     for _ in range(n_expected):
         results.append(q.get(timeout=120))
     for p in procs:
@@ -141,3 +173,23 @@ def test_batch_distribution_gloo():
 def test_sharded_requires_unso():
     with pytest.raises(ValueError):
         orthogonalize_row_sharded(torch.zeros(4, 2), MethodSpec(MethodKind.MUON_NS))
+
+
+def test_muon_data_parallel_split_gloo():
+    """Muon(distribute=True) on 2 ranks: each rank orthogonalizes half of every shape group (5 -> 3 + 2,
+    2 -> 1 + 1) and after the all-gather both ranks hold exactly the single-process result."""
+    from paper_2602_02500_b200.muon import Muon
+    results = _spawn(_worker_muon, 2)
+    params, grads = _muon_params(3)
+    calls = []
+    opt = Muon(params, lr=0.05, momentum=0.9, weight_decay=0.01, orthogonalize_fn=_oracle_stacked(calls))
+    for step in range(2):
+        for p, g in zip(params, grads):
+            p.grad = g * (step + 1)
+        opt.step()
+    assert sorted(calls) == [2, 2, 5, 5]
+    by_rank = {r: (c, ps) for r, c, ps in results}
+    assert sorted(by_rank[0][0]) == [1, 1, 3, 3] and sorted(by_rank[1][0]) == [1, 1, 2, 2]
+    for r in (0, 1):
+        for got, want in zip(by_rank[r][1], params):
+            assert np.array_equal(got, want.detach().numpy())

@@ -62,3 +62,32 @@ def test_muon_step_on_device():
         step = (p0 - p.detach()).double().cpu().numpy() / 0.05 / math.sqrt(max(1.0, p.shape[0] / p.shape[1]))
         ref = O.run(p.grad.to(torch.bfloat16).double().cpu().numpy(), "unso")["y"]
         assert np.linalg.norm(step - ref) / np.linalg.norm(ref) <= 2e-2
+
+
+@pytest.mark.gpu
+def test_muon_distribute_over_nccl_group_world1():
+    """The data-parallel path (equal shares + NCCL all_gather_into_tensor) on a real one-rank NCCL
+    group gives the same parameters as the plain step."""
+    import socket
+    import torch.distributed as dist
+    dev = torch.device("cuda:0")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{port}", device_id=dev)
+    try:
+        g = torch.Generator(device=dev).manual_seed(5)
+        base = [torch.randn(512, 256, generator=g, device=dev) * 0.02 for _ in range(3)]
+        grads = [torch.randn(512, 256, generator=g, device=dev) * 0.02 for _ in range(3)]
+        results = []
+        for distribute in (False, True):
+            params = [torch.nn.Parameter(b.clone()) for b in base]
+            for p, gr in zip(params, grads):
+                p.grad = gr.clone()
+            Muon(params, lr=0.05, precision="bf16", distribute=distribute).step()
+            results.append([p.detach() for p in params])
+        for a, b in zip(*results):
+            assert torch.equal(a, b)
+    finally:
+        dist.destroy_process_group()
