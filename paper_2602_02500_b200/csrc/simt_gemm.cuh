@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(128, 4) simt_gemm_kernel(SimtOperand A, SimtOp
 // ------------------------------------------------------------------------------------------
 // Pipelined variant (operands 16-byte aligned): raw-dtype tiles streamed into shared memory by
 // cp.async (3 stages, zero-filled edges), widened to f64 at the fragment load.  No register
-// staging, so 3-4 CTAs (12-16 warps) fit per SM to hide the DMMA and load latencies.
+// staging, so 4 CTAs (16 warps) fit per SM to hide the DMMA and load latencies.
 // Padded strides keep the fragment loads conflict-free (K-major tile [m][16+pk], MN-major
 // [k][64+pm]); every row stride is a multiple of 16 bytes for the cp.async destinations.
 template <int DT> struct DmmaLayout {
@@ -177,7 +177,10 @@ template <int DT> struct DmmaLayout {
   static constexpr int BYTES = (64 * KS > SIMT_BK * MS ? 64 * KS : SIMT_BK * MS) * E;
   static constexpr int EPC = 16 / E;                              // elements per 16-byte chunk
 };
-constexpr int DMMA_STAGES = 3;
+// Two stages with 4 CTAs (16 warps) per SM beat three stages with 3 CTAs: the batched chain of
+// configs[1] (16 x 36 upper 64x64 tiles = 576 CTAs) then runs in one wave of 592 slots
+// (fp32-mode chain 1.86 -> 1.40 ms; cfg5 chain -5 %; Gram / apply unchanged).
+constexpr int DMMA_STAGES = 2;
 
 template <int DT>
 __device__ __forceinline__ double dmma_lds(const uint8_t* base, int idx) {
@@ -217,7 +220,7 @@ __device__ __forceinline__ void dmma_issue(uint8_t* dst, const char* base, const
 }
 
 template <int DTA, int DTB, class Epi>
-__global__ void __launch_bounds__(128, 3) dmma_gemm_kernel(SimtOperand A, SimtOperand B, int M, int N, int K, int syrk,
+__global__ void __launch_bounds__(128, 4) dmma_gemm_kernel(SimtOperand A, SimtOperand B, int M, int N, int K, int syrk,
                                                            int tiles_m, int tiles_n, int splits, Epi epi) {
   using LA = DmmaLayout<DTA>;
   using LB = DmmaLayout<DTB>;
