@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     const int tid = threadIdx.x - 128;
 
     // ---- phase A: G tile = sum of split-K partials -> TMEM C region; tile norms
+    if (tid == 0) CHAIN_TRACE(0, 0);
     double tr = 0.0, fr = 0.0;
     const double wgt = (ti == tj) ? 1.0 : 2.0;
     for (int c = 0; c < 4; ++c) {
@@ -281,8 +282,10 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     if (tid == 0) {
       p.normbuf[blockIdx.x * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
       p.normbuf[blockIdx.x * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+      CHAIN_TRACE(0, 1);
       grid_arrive(p.gbar, 0);
       grid_wait(p.gbar, 0);
+      CHAIN_TRACE(0, 2);
       double s0 = 0.0, s1 = 0.0;
       const int first = lb * p.tiles_per_mat;
       for (int q = 0; q < p.tiles_per_mat; ++q) {  // fixed order -> deterministic
@@ -341,7 +344,10 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     (void)inv_s2;
     fence_proxy_async_global();
     named_bar_sync(1, 128);
-    if (tid == 0) grid_arrive(p.gbar, 1);  // C_1 published
+    if (tid == 0) {
+      CHAIN_TRACE(0, 3);
+      grid_arrive(p.gbar, 1);  // C_1 published
+    }
 
     // ---- phase B: squaring steps
     __shared__ int s_stop;
@@ -436,6 +442,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     // ---- final P: statistics -> identity shift d and the adaptive apply decision, then
     //      R/s = (P - d I)/s split into bf16 hi/lo, written symmetric for the apply.
     {
+      if (tid == 0) CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 0);
       double trp = 0.0, sp2 = 0.0;
       for (int c = 0; c < 4; ++c) {
         const int gc0 = tj * 128 + c * 32;
@@ -461,8 +468,10 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         p.pstat[blockIdx.x * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
         p.pstat[blockIdx.x * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
         const int round = static_cast<int>(last_round) + 1;
+        CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 1);
         grid_arrive(p.gbar, round);
         grid_wait(p.gbar, round);
+        CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 2);
         double tp = 0.0, s2p = 0.0;
         const int first = lb * p.tiles_per_mat;
         for (int q = 0; q < p.tiles_per_mat; ++q) {
@@ -487,27 +496,96 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       }
       named_bar_sync(1, 128);
       const double d = s_scale[0];
-      for (int c = 0; c < 4; ++c) {
-        const int gc0 = tj * 128 + c * 32;
-        uint32_t up[32];
-        tmem_ld32(lane_base + CH_P + c * 32, up);  // warp-collective: every lane, row_ok or not
-        tmem_wait_ld();
-        if (row_ok) {
+      if ((p.h & 31) == 0) {
+        // Whole 32 x 32 blocks: every lane stores its row segment with 16-byte vector stores, and
+        // the mirror block goes through a per-warp shared-memory transpose (the pipeline stages
+        // are idle now), so every global store is a run of whole sectors.
+        uint32_t* tb = reinterpret_cast<uint32_t*>(smem) + ew * 32 * 33;
+        const int gr0 = ti * 128 + ew * 32;
+        for (int c = 0; c < 4; ++c) {
+          const int gc0 = tj * 128 + c * 32;
+          uint32_t up[32];
+          tmem_ld32(lane_base + CH_P + c * 32, up);  // warp-collective: every lane
+          tmem_wait_ld();
+          const bool diag = ti == tj && c == ew;        // block straddling the diagonal
+          if (gr0 >= p.h || gc0 >= p.h || (ti == tj && c < ew)) continue;  // warp-uniform
+          uint32_t hl[32];                              // (hi << 16) | lo of row gr, columns gc0 + j
+#pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const int gc = gc0 + j;
-            if (gc >= p.h || (ti == tj && gc < gr)) continue;
-            const double rv = static_cast<double>(__uint_as_float(up[j])) - (gc == gr ? d : 0.0);
+            const double rv = static_cast<double>(__uint_as_float(up[j])) - (gc0 + j == gr ? d : 0.0);
             __nv_bfloat16 hi, lo;
             split_bf16(static_cast<float>(rv * s_scale[1]), hi, lo);
-            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
-            const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
-            p.phi[o] = hi;
-            p.plo[o] = lo;
-            p.phi[om] = hi;
-            p.plo[om] = lo;
+            hl[j] = (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16) | __bfloat16_as_ushort(lo);
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = hl[j];
+          __syncwarp();
+          if (diag) {  // lower half of the block from the transposed upper half: exact symmetry
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < lane) hl[j] = tb[j * 33 + lane];
+          }
+          const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            uint4 vh, vl;
+            vh.x = (hl[j] >> 16) | (hl[j + 1] & 0xFFFF0000u);
+            vh.y = (hl[j + 2] >> 16) | (hl[j + 3] & 0xFFFF0000u);
+            vh.z = (hl[j + 4] >> 16) | (hl[j + 5] & 0xFFFF0000u);
+            vh.w = (hl[j + 6] >> 16) | (hl[j + 7] & 0xFFFF0000u);
+            vl.x = (hl[j] & 0xFFFFu) | (hl[j + 1] << 16);
+            vl.y = (hl[j + 2] & 0xFFFFu) | (hl[j + 3] << 16);
+            vl.z = (hl[j + 4] & 0xFFFFu) | (hl[j + 5] << 16);
+            vl.w = (hl[j + 6] & 0xFFFFu) | (hl[j + 7] << 16);
+            *reinterpret_cast<uint4*>(p.phi + o + j) = vh;
+            *reinterpret_cast<uint4*>(p.plo + o + j) = vl;
+          }
+          if (!diag) {  // mirror: lane writes row gc0 + lane, columns gr0 .. gr0 + 31
+            const int64_t om = mbase + static_cast<int64_t>(gc0 + lane) * p.ld + gr0;
+#pragma unroll
+            for (int m = 0; m < 32; m += 8) {
+              uint32_t w[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) w[e] = tb[(m + e) * 33 + lane];
+              uint4 vh, vl;
+              vh.x = (w[0] >> 16) | (w[1] & 0xFFFF0000u);
+              vh.y = (w[2] >> 16) | (w[3] & 0xFFFF0000u);
+              vh.z = (w[4] >> 16) | (w[5] & 0xFFFF0000u);
+              vh.w = (w[6] >> 16) | (w[7] & 0xFFFF0000u);
+              vl.x = (w[0] & 0xFFFFu) | (w[1] << 16);
+              vl.y = (w[2] & 0xFFFFu) | (w[3] << 16);
+              vl.z = (w[4] & 0xFFFFu) | (w[5] << 16);
+              vl.w = (w[6] & 0xFFFFu) | (w[7] << 16);
+              *reinterpret_cast<uint4*>(p.phi + om + m) = vh;
+              *reinterpret_cast<uint4*>(p.plo + om + m) = vl;
+            }
+          }
+          __syncwarp();
+        }
+      } else {
+        for (int c = 0; c < 4; ++c) {
+          const int gc0 = tj * 128 + c * 32;
+          uint32_t up[32];
+          tmem_ld32(lane_base + CH_P + c * 32, up);  // warp-collective: every lane, row_ok or not
+          tmem_wait_ld();
+          if (row_ok) {
+            for (int j = 0; j < 32; ++j) {
+              const int gc = gc0 + j;
+              if (gc >= p.h || (ti == tj && gc < gr)) continue;
+              const double rv = static_cast<double>(__uint_as_float(up[j])) - (gc == gr ? d : 0.0);
+              __nv_bfloat16 hi, lo;
+              split_bf16(static_cast<float>(rv * s_scale[1]), hi, lo);
+              const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
+              const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
+              p.phi[o] = hi;
+              p.plo[o] = lo;
+              p.phi[om] = hi;
+              p.plo[om] = lo;
+            }
           }
         }
       }
+      if (tid == 0) CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 3);
     }
   }
   __syncthreads();
