@@ -103,6 +103,25 @@ __device__ __forceinline__ bool chain_truncate_before(const ChainParams& p, int 
   return static_cast<double>(p.tail_abs[k]) * (static_cast<double>(sum) / CHAIN_FIX) <= p.trunc_tau;
 }
 
+// Sum of the launch-wide per-tile (x, y) partials of matrix `lb` by the 128 epilogue threads after the
+// grid barrier: strided loads, fixed shuffle tree per warp, warps summed in order -- the same bits
+// on every CTA of the matrix.  Result in red[0][0] / red[1][0] after the trailing barrier.
+__device__ __forceinline__ void sum_tile_partials(const double* buf, int first, int n, int tid, double (*red)[4]) {
+  double a = 0.0, c = 0.0;
+  for (int q = tid; q < n; q += 128) {
+    a += __ldcg(&buf[(first + q) * 2 + 0]);
+    c += __ldcg(&buf[(first + q) * 2 + 1]);
+  }
+  a = warp_sum(a);
+  c = warp_sum(c);
+  named_bar_sync(1, 128);  // red[] free (its previous contents were consumed before the grid barrier)
+  if ((tid & 31) == 0) {
+    red[0][tid >> 5] = a;
+    red[1][tid >> 5] = c;
+  }
+  named_bar_sync(1, 128);
+}
+
 constexpr int CH_STAGES = 3;
 constexpr int CH_TILE = 128 * 64 * 2;          // 16 KB operand tile
 constexpr int CH_STAGE_BYTES = 4 * CH_TILE;    // A hi, A lo, B hi, B lo
@@ -286,12 +305,13 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       grid_arrive(p.gbar, 0);
       grid_wait(p.gbar, 0);
       CHAIN_TRACE(0, 2);
-      double s0 = 0.0, s1 = 0.0;
-      const int first = lb * p.tiles_per_mat;
-      for (int q = 0; q < p.tiles_per_mat; ++q) {  // fixed order -> deterministic
-        s0 += __ldcg(&p.normbuf[(first + q) * 2 + 0]);
-        s1 += __ldcg(&p.normbuf[(first + q) * 2 + 1]);
-      }
+    }
+    named_bar_sync(1, 128);  // every epilogue thread is past the grid barrier
+    sum_tile_partials(p.normbuf, lb * p.tiles_per_mat, p.tiles_per_mat, tid, red);
+    if (tid == 0) {
+      const double s0 = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+      const double s1 = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+      CHAIN_TRACE(0, 4);
       double s2 = p.scal_mode == SM_PLAIN ? s0 : sqrt(s1);
       if (p.scal_mode == SM_NONE) s2 = 1.0;
       const double inv_s = 1.0 / sqrt(s2);
@@ -472,12 +492,12 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         grid_arrive(p.gbar, round);
         grid_wait(p.gbar, round);
         CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 2);
-        double tp = 0.0, s2p = 0.0;
-        const int first = lb * p.tiles_per_mat;
-        for (int q = 0; q < p.tiles_per_mat; ++q) {
-          tp += __ldcg(&p.pstat[(first + q) * 2 + 0]);
-          s2p += __ldcg(&p.pstat[(first + q) * 2 + 1]);
-        }
+      }
+      named_bar_sync(1, 128);
+      sum_tile_partials(p.pstat, lb * p.tiles_per_mat, p.tiles_per_mat, tid, red);
+      if (tid == 0) {
+        const double tp = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+        const double s2p = red[1][0] + red[1][1] + red[1][2] + red[1][3];
         const double d = tp / p.h;
         const double r2 = fmax(s2p - tp * tp / p.h, 0.0);
         // ||X (R_hat - R)||_F <= ||X||_2 2^-9 ||R||_F with ||X||_2 <= 1 (gram/plain scaling), and

@@ -35,6 +35,6 @@ for c in range(3):
     a, f = t[c, 0], t[c, 63]
     if a[0] and f[0]:
         print(f"CTA slot {c}: phase A: partials+norms {(a[1]-a[0])/1e3:.2f} us, norm barrier {(a[2]-a[1])/1e3:.2f}, "
-              f"C_1/P init {(a[3]-a[2])/1e3:.2f}; step 1 data after C_1 {(t[c,1,1]-a[3])/1e3:.2f}; "
+              f"C_1/P init {(a[3]-a[2])/1e3:.2f} (of which the norm sum {(a[4]-a[2])/1e3:.2f}); step 1 data after C_1 {(t[c,1,1]-a[3])/1e3:.2f}; "
               f"final: stats {(f[1]-f[0])/1e3:.2f}, barrier {(f[2]-f[1])/1e3:.2f}, P split+mirror {(f[3]-f[2])/1e3:.2f}; "
               f"kernel span {(f[3]-a[0])/1e3:.2f} us")
