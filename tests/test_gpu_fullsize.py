@@ -36,9 +36,13 @@ def spectrum_svd(z: torch.Tensor) -> np.ndarray:
 def check_map(x, y, spec, precision, spectrum=spectrum_gram, label=""):
     sx = spectrum(x)
     sy = spectrum(y)
-    if spec.effective_scaling is U.Scaling.FROBENIUS_GRAM:
+    sc = spec.effective_scaling
+    if sc is U.Scaling.FROBENIUS_GRAM:       # ||A A^T||_F^(1/2)
         scale = float((sx ** 4).sum()) ** 0.25
-    else:
+    elif sc is U.Scaling.GELFAND:            # ||(A A^T)^k||_F^(1/(2k))
+        k = spec.gelfand_power
+        scale = float((sx ** (4 * k)).sum()) ** (1.0 / (4 * k))
+    else:                                    # ||A||_F
         scale = float(np.sqrt((sx ** 2).sum()))
     want = np.sort(U.scalar_map(spec)(sx / scale))[::-1]
     got = np.sort(sy)[::-1]
@@ -74,6 +78,11 @@ def pareto_spectrum_matrix(rows, cols, seed):
 SPECS = {
     "unso": lambda: U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()),
     "muon5": lambda: U.MethodSpec(U.MethodKind.MUON_NS, iterations=5),
+    "unso_plain": lambda: U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), scaling="plain"),
+    "unso_gelfand": lambda: U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), scaling="gelfand"),
+    "original8": lambda: U.MethodSpec(U.MethodKind.ORIGINAL_NS, iterations=8),
+    "cesista": lambda: U.MethodSpec(U.MethodKind.CESISTA_NS,
+                                    step_params=U.CesistaStepParams(U.default_cesista_triples())),
 }
 
 
@@ -107,3 +116,22 @@ def test_cfg5_full_bf16_and_fp32(method):
     res = U.orthogonalize(x, spec, precision="fp32")
     # fp32 bar: tiny singular values (1e-6) need the SVD, not the Gram's eigenvalues
     check_map(x, res.y, spec, "fp32", spectrum=spectrum_svd, label=f"cfg5 {method}")
+
+
+@pytest.mark.parametrize("method", ["unso_plain", "unso_gelfand", "original8", "cesista"])
+def test_other_methods_and_scalings_full_size(method):
+    """The remaining method kinds and scalings of the boundary (ortho.py:54-65, 140-168, 208-256)
+    at configs[3]'s shape in bf16 mode and at configs[1]'s matrix shape (log-uniform spectrum) in fp32 mode."""
+    spec = SPECS[method]()
+    x = gaussian(262144, 2048, 1.0, 99, torch.bfloat16)
+    res = U.orthogonalize(x, spec, precision="bf16")
+    check_map(x, res.y, spec, "bf16", label=f"cfg4-shape {method}")
+    del x, res
+    rng = np.random.default_rng(7)
+    g = torch.Generator(device=DEV).manual_seed(7)
+    s = torch.from_numpy(np.exp(rng.uniform(np.log(1e-4), 0.0, 512))).to(DEV)
+    q1, r1 = torch.linalg.qr(torch.randn(2048, 512, generator=g, device=DEV, dtype=torch.float64))
+    q2, r2 = torch.linalg.qr(torch.randn(512, 512, generator=g, device=DEV, dtype=torch.float64))
+    xf = ((q1 * torch.sign(torch.diagonal(r1))) * s[None, :] @ (q2 * torch.sign(torch.diagonal(r2))).T).float()
+    res = U.orthogonalize(xf, spec, precision="fp32")
+    check_map(xf, res.y, spec, "fp32", spectrum=spectrum_svd, label=f"cfg2-shape {method}")
