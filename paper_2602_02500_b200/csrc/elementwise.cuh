@@ -7,7 +7,7 @@
 
 namespace unso {
 
-constexpr int NORM_BLOCKS = 64;  // per-matrix partial-reduction blocks (fixed -> deterministic)
+constexpr int NORM_BLOCKS = 256;  // per-matrix partial-reduction blocks (fixed -> deterministic)
 
 // scal[b * SCAL_STRIDE + ...]
 // S_SHIFT: d/s, the identity shift removed from P before the bf16 split (added back as d/s * X in the
@@ -163,6 +163,78 @@ __global__ void sumsq_kernel(const void* __restrict__ x, int dt, int64_t rows, i
     o[1] = 0.0;
     o[2] = 0.0;
   }
+}
+
+// ||A||_F^2 partials for the plain scaling (ortho.py:153-154) on 16-byte chunks: a power-of-two
+// group of threads walks each row (no per-element index arithmetic), every element squared in
+// fp64.  Requires 16-byte aligned rows whose length is a multiple of the chunk; launch_sumsq falls
+// back to sumsq_kernel otherwise.  Fixed grid and assignment -> deterministic partials.
+template <int DT>
+__device__ __forceinline__ double sumsq_chunk(const uint4 v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  double s = 0.0;
+  if constexpr (DT == DT_BF16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double a = bf16_lo_to_f32(w[i]), c = bf16_hi_to_f32(w[i]);
+      s = fma(a, a, fma(c, c, s));
+    }
+  } else if constexpr (DT == DT_F32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double a = __uint_as_float(w[i]);
+      s = fma(a, a, s);
+    }
+  } else {
+    const double a = __hiloint2double(static_cast<int>(w[1]), static_cast<int>(w[0]));
+    const double c = __hiloint2double(static_cast<int>(w[3]), static_cast<int>(w[2]));
+    s = fma(a, a, c * c);
+  }
+  return s;
+}
+
+template <int DT>
+__global__ void sumsq_vec_kernel(const void* __restrict__ x, int64_t rows, int64_t cpr, int64_t ld, int64_t bs,
+                                 int tpr, double* __restrict__ blk) {
+  __shared__ double scratch[32];
+  constexpr int E = DT == DT_F64 ? 8 : (DT == DT_F32 ? 4 : 2);
+  const int b = blockIdx.y;
+  const char* base = static_cast<const char*>(x) + static_cast<int64_t>(b) * bs * E;
+  const int rpi = blockDim.x / tpr, sub = threadIdx.x / tpr, li = threadIdx.x % tpr;
+  double s = 0.0;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * rpi + sub; r < rows; r += static_cast<int64_t>(gridDim.x) * rpi) {
+    const uint4* row = reinterpret_cast<const uint4*>(base + r * ld * E);
+    for (int64_t c = li; c < cpr; c += tpr) s += sumsq_chunk<DT>(__ldcs(row + c));
+  }
+  s = block_sum(s, scratch);
+  if (threadIdx.x == 0) {
+    double* o = blk + (static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * 3;
+    o[0] = s;
+    o[1] = 0.0;
+    o[2] = 0.0;
+  }
+}
+
+// Plain-scaling partials (NORM_BLOCKS per matrix into blk), vectorized when the layout allows.
+inline void launch_sumsq(const void* x, int dt, int64_t rows, int64_t cols, int64_t ld, int64_t bs, int64_t batch,
+                         double* blk, cudaStream_t st) {
+  const int e = dt == DT_F64 ? 8 : (dt == DT_F32 ? 4 : 2), v = 16 / e;
+  const bool vec = (cols % v) == 0 && ((ld * e) & 15) == 0 && ((bs * e) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const dim3 grid(NORM_BLOCKS, static_cast<unsigned>(batch));
+  if (!vec) {
+    sumsq_kernel<<<grid, 256, 0, st>>>(x, dt, rows, cols, ld, bs, blk);
+    return;
+  }
+  const int64_t cpr = cols / v;
+  int tpr = 1;
+  while (tpr < cpr && tpr < 256) tpr <<= 1;
+  if (dt == DT_BF16)
+    sumsq_vec_kernel<DT_BF16><<<grid, 256, 0, st>>>(x, rows, cpr, ld, bs, tpr, blk);
+  else if (dt == DT_F32)
+    sumsq_vec_kernel<DT_F32><<<grid, 256, 0, st>>>(x, rows, cpr, ld, bs, tpr, blk);
+  else
+    sumsq_vec_kernel<DT_F64><<<grid, 256, 0, st>>>(x, rows, cpr, ld, bs, tpr, blk);
 }
 
 enum ScalarsMode : int { SM_GRAM = 0, SM_PLAIN = 1, SM_GELFAND = 2, SM_ERROR = 3, SM_NONE = 4 };

@@ -27,6 +27,81 @@ __global__ void ns_init_state_kernel(const void* __restrict__ src, int sdt, int6
   }
 }
 
+// Same state initialisation on 8-element chunks (16-byte aligned rows, cols % 8 == 0): a
+// power-of-two group of threads per row, no per-element index arithmetic; identical rounding
+// (double scale -> float -> bf16 RNE).
+template <int SDT>
+__global__ void ns_init_state_vec_kernel(const void* __restrict__ src, int64_t sld, int64_t sbs,
+                                         const double* __restrict__ scal, float* __restrict__ xf,
+                                         __nv_bfloat16* __restrict__ xb, int64_t xld, int64_t rows, int64_t cols,
+                                         int batch, int tpr) {
+  constexpr int E = SDT == DT_F64 ? 8 : (SDT == DT_F32 ? 4 : 2);
+  const int64_t cpr = cols / 8, nrows = rows * batch;
+  const int rpi = blockDim.x / tpr, sub = threadIdx.x / tpr, li = threadIdx.x % tpr;
+  for (int64_t R = static_cast<int64_t>(blockIdx.x) * rpi + sub; R < nrows; R += static_cast<int64_t>(gridDim.x) * rpi) {
+    const int64_t b = R / rows, r = R - b * rows;
+    const double sc = scal ? scal[b * SCAL_STRIDE + S_INV_S] : 1.0;
+    const char* srow = static_cast<const char*>(src) + (b * sbs + r * sld) * E;
+    float* frow = xf + (b * rows + r) * cols;
+    __nv_bfloat16* brow = xb + (b * rows + r) * xld;
+    for (int64_t c = li; c < cpr; c += tpr) {
+      float f[8];
+      if constexpr (SDT == DT_BF16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(srow + c * 16);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          f[2 * i] = static_cast<float>(static_cast<double>(bf16_lo_to_f32(w[i])) * sc);
+          f[2 * i + 1] = static_cast<float>(static_cast<double>(bf16_hi_to_f32(w[i])) * sc);
+        }
+      } else if constexpr (SDT == DT_F32) {
+        const float4 a = *reinterpret_cast<const float4*>(srow + c * 32);
+        const float4 d = *reinterpret_cast<const float4*>(srow + c * 32 + 16);
+        const float in[8] = {a.x, a.y, a.z, a.w, d.x, d.y, d.z, d.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = static_cast<float>(static_cast<double>(in[i]) * sc);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = static_cast<float>(reinterpret_cast<const double*>(srow)[c * 8 + i] * sc);
+      }
+      *reinterpret_cast<float4*>(frow + c * 8) = make_float4(f[0], f[1], f[2], f[3]);
+      *reinterpret_cast<float4*>(frow + c * 8 + 4) = make_float4(f[4], f[5], f[6], f[7]);
+      uint4 o;
+      o.x = pack_bf16x2(f[0], f[1]);
+      o.y = pack_bf16x2(f[2], f[3]);
+      o.z = pack_bf16x2(f[4], f[5]);
+      o.w = pack_bf16x2(f[6], f[7]);
+      *reinterpret_cast<uint4*>(brow + c * 8) = o;
+    }
+  }
+}
+
+inline void launch_ns_init_state(const void* src, int sdt, int64_t sld, int64_t sbs, const double* scal, float* xf,
+                                 __nv_bfloat16* xb, int64_t xld, int64_t rows, int64_t cols, int batch,
+                                 cudaStream_t st) {
+  const int e = sdt == DT_F64 ? 8 : (sdt == DT_F32 ? 4 : 2);
+  const bool vec = (cols % 8) == 0 && ((sld * e) & 15) == 0 && ((sbs * e) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (xld % 8) == 0 &&
+                   (reinterpret_cast<uintptr_t>(xb) & 15) == 0 && (reinterpret_cast<uintptr_t>(xf) & 15) == 0;
+  if (!vec) {
+    const int64_t total = rows * cols * batch;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    ns_init_state_kernel<<<blocks, 256, 0, st>>>(src, sdt, sld, sbs, scal, xf, xb, xld, rows, cols, batch);
+    return;
+  }
+  const int64_t cpr = cols / 8;
+  int tpr = 1;
+  while (tpr < cpr && tpr < 256) tpr <<= 1;
+  const int64_t nrows = rows * batch;
+  const int blocks = static_cast<int>(std::min<int64_t>((nrows + 256 / tpr - 1) / (256 / tpr), 148 * 16));
+  if (sdt == DT_BF16)
+    ns_init_state_vec_kernel<DT_BF16><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr);
+  else if (sdt == DT_F32)
+    ns_init_state_vec_kernel<DT_F32><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr);
+  else
+    ns_init_state_vec_kernel<DT_F64><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr);
+}
+
 // out_hi/lo = split(factor * G), full h x h (the cubic step operator B = -0.5 G).
 __global__ void split_scaled_kernel(const float* __restrict__ G, int h, int64_t ld, float factor,
                                     __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {

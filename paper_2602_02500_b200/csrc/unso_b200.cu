@@ -1354,8 +1354,7 @@ static int32_t ns_fp32(const Problem& p, const Plan& pl, void* ws, const void* x
   if (p.scaling == UNSO_SCALING_NONE) {
     xscale = nullptr;
   } else if (p.scaling == UNSO_SCALING_PLAIN) {
-    dim3 grid(NORM_BLOCKS, static_cast<unsigned>(B));
-    sumsq_kernel<<<grid, 256, 0, st>>>(x, p.dt, p.rows, p.cols, p.ld, p.bs, at<double>(ws, pl.blk));
+    launch_sumsq(x, p.dt, p.rows, p.cols, p.ld, p.bs, B, at<double>(ws, pl.blk), st);
     UNSO_CHECK_LAUNCH();
     scalars_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, SM_PLAIN, p.gpow,
                                                             at<double>(ws, pl.scal), status);
@@ -1433,15 +1432,14 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
   if (p.scaling == UNSO_SCALING_NONE) {
     xscale = nullptr;
   } else if (p.scaling == UNSO_SCALING_PLAIN) {
-    dim3 grid(NORM_BLOCKS, static_cast<unsigned>(B));
-    sumsq_kernel<<<grid, 256, 0, st>>>(x, p.dt, p.rows, p.cols, p.ld, p.bs, at<double>(ws, pl.blk));
+    launch_sumsq(x, p.dt, p.rows, p.cols, p.ld, p.bs, B, at<double>(ws, pl.blk), st);
     UNSO_CHECK_LAUNCH();
     scalars_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, SM_PLAIN, p.gpow,
                                                             scal, status);
     UNSO_CHECK_LAUNCH();
   } else {  // gram / gelfand: Gram of the unscaled bf16 input on the tensor cores
-    ns_init_state_kernel<<<grid_for(B * xsz), 256, 0, st>>>(x, p.dt, p.ld, p.bs, nullptr, at<float>(ws, pl.Xs[0]), xb,
-                                                           ldx, p.rows, p.cols, static_cast<int>(B));
+    launch_ns_init_state(x, p.dt, p.ld, p.bs, nullptr, at<float>(ws, pl.Xs[0]), xb, ldx, p.rows, p.cols,
+                         static_cast<int>(B), st);
     UNSO_CHECK_LAUNCH();
     UNSO_TRY(gram_bf16(p, pl, ws, xb, ldx, bsx, st));
     UNSO_TRY(finalize_gram<float>(p, pl, ws, pl.splits, at<float>(ws, pl.G), st));
@@ -1449,8 +1447,8 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
     if (p.scaling == UNSO_SCALING_GELFAND)
       UNSO_TRY(gelfand_scale<float>(p, pl, ws, at<float>(ws, pl.G), DT_F32, status, st));
   }
-  ns_init_state_kernel<<<grid_for(B * xsz), 256, 0, st>>>(x, p.dt, p.ld, p.bs, xscale, at<float>(ws, pl.Xs[0]), xb,
-                                                         ldx, p.rows, p.cols, static_cast<int>(B));
+  launch_ns_init_state(x, p.dt, p.ld, p.bs, xscale, at<float>(ws, pl.Xs[0]), xb, ldx, p.rows, p.cols,
+                       static_cast<int>(B), st);
   UNSO_CHECK_LAUNCH();
   const dim3 egrid(grid_for(static_cast<int64_t>(h) * h, 256, 1024), static_cast<unsigned>(B));
   int cur = 0;
@@ -1828,8 +1826,7 @@ int32_t unso_scale_denominator(const unso_matrix_desc* x, const void* x_ptr, con
   }
   UNSO_TRY(check_ws(plg, workspace, workspace_bytes));
   if (p.scaling == UNSO_SCALING_PLAIN) {
-    dim3 grid(NORM_BLOCKS, static_cast<unsigned>(p.batch));
-    sumsq_kernel<<<grid, 256, 0, st>>>(x_ptr, p.dt, p.rows, p.cols, p.ld, p.bs, at<double>(workspace, pl.blk));
+    launch_sumsq(x_ptr, p.dt, p.rows, p.cols, p.ld, p.bs, p.batch, at<double>(workspace, pl.blk), st);
     UNSO_CHECK_LAUNCH();
     scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(workspace, pl.blk), NORM_BLOCKS,
                                                                     SM_PLAIN, 1, at<double>(workspace, pl.scal),
