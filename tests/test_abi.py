@@ -112,3 +112,32 @@ def test_gram_peer_buffer_sizes():
     assert lib.unso_gram_peer_bytes(2048, 2, 0, 0) == 0
     from paper_2602_02500_b200.distributed import gram_push_splits
     assert gram_push_splits(2048, 32768) == 2 and gram_push_splits(128, 64) == 1
+
+
+def test_header_constants_match_the_binding():
+    """Every enum value and #define of include/unso_b200.h equals the ctypes binding's constant
+    (guards the ABI against drift between the header and _native.py)."""
+    import re
+    from paper_2602_02500_b200 import _native as N
+    text = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                             "unso_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    consts = {m.group(1): int(m.group(2), 0) for m in re.finditer(r"\b(UNSO_[A-Z0-9_]+)\s*=\s*(0x[0-9a-fA-F]+|\d+)", text)}
+    consts.update({m.group(1): int(m.group(2), 0)
+                   for m in re.finditer(r"#define\s+(UNSO_[A-Z0-9_]+)\s+(0x[0-9a-fA-F]+|\d+)", text)})
+    expect = {
+        "UNSO_OK": N.OK, "UNSO_ERR_SHAPE": N.ERR_SHAPE, "UNSO_ERR_DEGENERATE": N.ERR_DEGENERATE,
+        "UNSO_ERR_VALUE": N.ERR_VALUE, "UNSO_ERR_CUDA": N.ERR_CUDA, "UNSO_ERR_UNSUPPORTED": N.ERR_UNSUPPORTED,
+        "UNSO_ERR_WORKSPACE": N.ERR_WORKSPACE,
+        "UNSO_DTYPE_F32": N.DTYPE_F32, "UNSO_DTYPE_BF16": N.DTYPE_BF16, "UNSO_DTYPE_F64": N.DTYPE_F64,
+        "UNSO_PREC_FP32": N.PREC_FP32, "UNSO_PREC_BF16": N.PREC_BF16,
+        "UNSO_SCALING_GRAM": N.SCALING_GRAM, "UNSO_SCALING_PLAIN": N.SCALING_PLAIN,
+        "UNSO_SCALING_GELFAND": N.SCALING_GELFAND, "UNSO_SCALING_NONE": N.SCALING_NONE,
+        "UNSO_METHOD_UNSO": N.METHOD_UNSO, "UNSO_METHOD_ORIGINAL_NS": N.METHOD_ORIGINAL_NS,
+        "UNSO_METHOD_QUINTIC": N.METHOD_QUINTIC,
+        "UNSO_FLAG_SINGLE_TERM_APPLY": N.FLAG_SINGLE_TERM_APPLY, "UNSO_FLAG_TWO_TERM_APPLY": N.FLAG_TWO_TERM_APPLY,
+        "UNSO_FLAG_CHAIN_BF16X3": N.FLAG_CHAIN_BF16X3, "UNSO_FLAG_NO_TRUNCATION": N.FLAG_NO_TRUNCATION,
+        "UNSO_MAX_PEERS": N.MAX_PEERS, "UNSO_SCALARS": N.SCALARS, "UNSO_PROFILE_STAGES": len(N.PROFILE_STAGES),
+    }
+    for name, value in expect.items():
+        assert consts.get(name) == value, (name, consts.get(name), value)
