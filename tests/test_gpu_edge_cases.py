@@ -144,3 +144,15 @@ def test_scale_invariance():
     a = U.orthogonalize(x, UNSO, precision="fp32").y
     b = U.orthogonalize(x * 1e3, UNSO, precision="fp32").y
     assert rel(b.cpu().numpy(), a.cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float64])
+def test_ns_layouts_vectorized_and_fallback(precision, dtype):
+    """The NS comparison path (plain-scaling norm + state initialisation) on layouts that take the
+    16-byte-chunk kernels (contiguous, cols % 8 == 0) and ones that fall back to the element kernels
+    (cols % 8 != 0, unaligned row stride), tall and wide, single and batched."""
+    cases = [gaussian((640, 96), 61, dtype), gaussian((96, 640), 62, dtype), gaussian((3, 300, 52), 63, dtype),
+             gaussian((250, 37), 64, dtype), gaussian((400, 133), 65, dtype)[:, :130]]
+    for x in cases:
+        check(x, MUON, "muon", precision)
