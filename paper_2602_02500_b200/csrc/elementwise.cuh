@@ -145,7 +145,7 @@ __global__ void gram_norms_kernel(const T* __restrict__ G, int h, int64_t ld, do
 
 // sum of squares of a rows x cols input (plain scaling, ortho.py:153-154) -> slot 0
 __global__ void sumsq_kernel(const void* __restrict__ x, int dt, int64_t rows, int64_t cols, int64_t ld, int64_t bs,
-                             double* __restrict__ blk) {
+                             double* __restrict__ blk, int round_in = 0) {
   __shared__ double scratch[32];
   const int b = blockIdx.y;
   const int64_t total = rows * cols;
@@ -153,7 +153,8 @@ __global__ void sumsq_kernel(const void* __restrict__ x, int dt, int64_t rows, i
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = i / cols, c = i - r * cols;
-    const double v = load_as_f64(x, b * bs + r * ld + c, dt);
+    double v = load_as_f64(x, b * bs + r * ld + c, dt);
+    if (round_in) v = static_cast<double>(__bfloat162float(__float2bfloat16_rn(static_cast<float>(v))));
     s += v * v;
   }
   s = block_sum(s, scratch);
@@ -169,7 +170,10 @@ __global__ void sumsq_kernel(const void* __restrict__ x, int dt, int64_t rows, i
 // group of threads walks each row (no per-element index arithmetic), every element squared in
 // fp64.  Requires 16-byte aligned rows whose length is a multiple of the chunk; launch_sumsq falls
 // back to sumsq_kernel otherwise.  Fixed grid and assignment -> deterministic partials.
-template <int DT>
+__device__ __forceinline__ double round_bf16_d(double a) {
+  return static_cast<double>(__bfloat162float(__float2bfloat16_rn(static_cast<float>(a))));
+}
+template <int DT, bool ROUND>
 __device__ __forceinline__ double sumsq_chunk(const uint4 v) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
   double s = 0.0;
@@ -182,18 +186,23 @@ __device__ __forceinline__ double sumsq_chunk(const uint4 v) {
   } else if constexpr (DT == DT_F32) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const double a = __uint_as_float(w[i]);
+      double a = __uint_as_float(w[i]);
+      if (ROUND) a = round_bf16_d(a);
       s = fma(a, a, s);
     }
   } else {
-    const double a = __hiloint2double(static_cast<int>(w[1]), static_cast<int>(w[0]));
-    const double c = __hiloint2double(static_cast<int>(w[3]), static_cast<int>(w[2]));
+    double a = __hiloint2double(static_cast<int>(w[1]), static_cast<int>(w[0]));
+    double c = __hiloint2double(static_cast<int>(w[3]), static_cast<int>(w[2]));
+    if (ROUND) {
+      a = round_bf16_d(a);
+      c = round_bf16_d(c);
+    }
     s = fma(a, a, c * c);
   }
   return s;
 }
 
-template <int DT>
+template <int DT, bool ROUND>
 __global__ void sumsq_vec_kernel(const void* __restrict__ x, int64_t rows, int64_t cpr, int64_t ld, int64_t bs,
                                  int tpr, double* __restrict__ blk) {
   __shared__ double scratch[32];
@@ -204,7 +213,7 @@ __global__ void sumsq_vec_kernel(const void* __restrict__ x, int64_t rows, int64
   double s = 0.0;
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * rpi + sub; r < rows; r += static_cast<int64_t>(gridDim.x) * rpi) {
     const uint4* row = reinterpret_cast<const uint4*>(base + r * ld * E);
-    for (int64_t c = li; c < cpr; c += tpr) s += sumsq_chunk<DT>(__ldcs(row + c));
+    for (int64_t c = li; c < cpr; c += tpr) s += sumsq_chunk<DT, ROUND>(__ldcs(row + c));
   }
   s = block_sum(s, scratch);
   if (threadIdx.x == 0) {
@@ -216,25 +225,28 @@ __global__ void sumsq_vec_kernel(const void* __restrict__ x, int64_t rows, int64
 }
 
 // Plain-scaling partials (NORM_BLOCKS per matrix into blk), vectorized when the layout allows.
+// round_in: square the bf16-rounded values (bf16-mode NS path, see launch_ns_init_state).
 inline void launch_sumsq(const void* x, int dt, int64_t rows, int64_t cols, int64_t ld, int64_t bs, int64_t batch,
-                         double* blk, cudaStream_t st) {
+                         double* blk, cudaStream_t st, bool round_in = false) {
   const int e = dt == DT_F64 ? 8 : (dt == DT_F32 ? 4 : 2), v = 16 / e;
   const bool vec = (cols % v) == 0 && ((ld * e) & 15) == 0 && ((bs * e) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   const dim3 grid(NORM_BLOCKS, static_cast<unsigned>(batch));
   if (!vec) {
-    sumsq_kernel<<<grid, 256, 0, st>>>(x, dt, rows, cols, ld, bs, blk);
+    sumsq_kernel<<<grid, 256, 0, st>>>(x, dt, rows, cols, ld, bs, blk, round_in ? 1 : 0);
     return;
   }
   const int64_t cpr = cols / v;
   int tpr = 1;
   while (tpr < cpr && tpr < 256) tpr <<= 1;
   if (dt == DT_BF16)
-    sumsq_vec_kernel<DT_BF16><<<grid, 256, 0, st>>>(x, rows, cpr, ld, bs, tpr, blk);
+    sumsq_vec_kernel<DT_BF16, false><<<grid, 256, 0, st>>>(x, rows, cpr, ld, bs, tpr, blk);
   else if (dt == DT_F32)
-    sumsq_vec_kernel<DT_F32><<<grid, 256, 0, st>>>(x, rows, cpr, ld, bs, tpr, blk);
+    (round_in ? sumsq_vec_kernel<DT_F32, true> : sumsq_vec_kernel<DT_F32, false>)<<<grid, 256, 0, st>>>(
+        x, rows, cpr, ld, bs, tpr, blk);
   else
-    sumsq_vec_kernel<DT_F64><<<grid, 256, 0, st>>>(x, rows, cpr, ld, bs, tpr, blk);
+    (round_in ? sumsq_vec_kernel<DT_F64, true> : sumsq_vec_kernel<DT_F64, false>)<<<grid, 256, 0, st>>>(
+        x, rows, cpr, ld, bs, tpr, blk);
 }
 
 enum ScalarsMode : int { SM_GRAM = 0, SM_PLAIN = 1, SM_GELFAND = 2, SM_ERROR = 3, SM_NONE = 4 };

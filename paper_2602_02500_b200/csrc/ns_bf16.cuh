@@ -14,12 +14,13 @@ namespace unso {
 __global__ void ns_init_state_kernel(const void* __restrict__ src, int sdt, int64_t sld, int64_t sbs,
                                      const double* __restrict__ scal, float* __restrict__ xf,
                                      __nv_bfloat16* __restrict__ xb, int64_t xld, int64_t rows, int64_t cols,
-                                     int batch) {
+                                     int batch, int round_in) {
   const int64_t per = rows * cols, total = per * batch;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t b = i / per, rc = i - b * per, r = rc / cols, c = rc - r * cols;
     double v = load_as_f64(src, b * sbs + r * sld + c, sdt);
+    if (round_in) v = static_cast<double>(__bfloat162float(__float2bfloat16_rn(static_cast<float>(v))));
     if (scal) v *= scal[b * SCAL_STRIDE + S_INV_S];
     const float f = static_cast<float>(v);
     xf[b * per + r * cols + c] = f;
@@ -34,7 +35,7 @@ template <int SDT>
 __global__ void ns_init_state_vec_kernel(const void* __restrict__ src, int64_t sld, int64_t sbs,
                                          const double* __restrict__ scal, float* __restrict__ xf,
                                          __nv_bfloat16* __restrict__ xb, int64_t xld, int64_t rows, int64_t cols,
-                                         int batch, int tpr) {
+                                         int batch, int tpr, int round_in) {
   constexpr int E = SDT == DT_F64 ? 8 : (SDT == DT_F32 ? 4 : 2);
   const int64_t cpr = cols / 8, nrows = rows * batch;
   const int rpi = blockDim.x / tpr, sub = threadIdx.x / tpr, li = threadIdx.x % tpr;
@@ -59,10 +60,17 @@ __global__ void ns_init_state_vec_kernel(const void* __restrict__ src, int64_t s
         const float4 d = *reinterpret_cast<const float4*>(srow + c * 32 + 16);
         const float in[8] = {a.x, a.y, a.z, a.w, d.x, d.y, d.z, d.w};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) f[i] = static_cast<float>(static_cast<double>(in[i]) * sc);
+        for (int i = 0; i < 8; ++i) {
+          const float vi = round_in ? __bfloat162float(__float2bfloat16_rn(in[i])) : in[i];
+          f[i] = static_cast<float>(static_cast<double>(vi) * sc);
+        }
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) f[i] = static_cast<float>(reinterpret_cast<const double*>(srow)[c * 8 + i] * sc);
+        for (int i = 0; i < 8; ++i) {
+          double vi = reinterpret_cast<const double*>(srow)[c * 8 + i];
+          if (round_in) vi = static_cast<double>(__bfloat162float(__float2bfloat16_rn(static_cast<float>(vi))));
+          f[i] = static_cast<float>(vi * sc);
+        }
       }
       *reinterpret_cast<float4*>(frow + c * 8) = make_float4(f[0], f[1], f[2], f[3]);
       *reinterpret_cast<float4*>(frow + c * 8 + 4) = make_float4(f[4], f[5], f[6], f[7]);
@@ -76,9 +84,11 @@ __global__ void ns_init_state_vec_kernel(const void* __restrict__ src, int64_t s
   }
 }
 
+// round_in: round every input value to bf16 first (bf16 mode: the path computes on the bf16-rounded
+// input, the same values the UNSO path and the parity oracle see).
 inline void launch_ns_init_state(const void* src, int sdt, int64_t sld, int64_t sbs, const double* scal, float* xf,
                                  __nv_bfloat16* xb, int64_t xld, int64_t rows, int64_t cols, int batch,
-                                 cudaStream_t st) {
+                                 int round_in, cudaStream_t st) {
   const int e = sdt == DT_F64 ? 8 : (sdt == DT_F32 ? 4 : 2);
   const bool vec = (cols % 8) == 0 && ((sld * e) & 15) == 0 && ((sbs * e) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (xld % 8) == 0 &&
@@ -86,7 +96,7 @@ inline void launch_ns_init_state(const void* src, int sdt, int64_t sld, int64_t 
   if (!vec) {
     const int64_t total = rows * cols * batch;
     const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
-    ns_init_state_kernel<<<blocks, 256, 0, st>>>(src, sdt, sld, sbs, scal, xf, xb, xld, rows, cols, batch);
+    ns_init_state_kernel<<<blocks, 256, 0, st>>>(src, sdt, sld, sbs, scal, xf, xb, xld, rows, cols, batch, round_in);
     return;
   }
   const int64_t cpr = cols / 8;
@@ -95,11 +105,11 @@ inline void launch_ns_init_state(const void* src, int sdt, int64_t sld, int64_t 
   const int64_t nrows = rows * batch;
   const int blocks = static_cast<int>(std::min<int64_t>((nrows + 256 / tpr - 1) / (256 / tpr), 148 * 16));
   if (sdt == DT_BF16)
-    ns_init_state_vec_kernel<DT_BF16><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr);
+    ns_init_state_vec_kernel<DT_BF16><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr, round_in);
   else if (sdt == DT_F32)
-    ns_init_state_vec_kernel<DT_F32><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr);
+    ns_init_state_vec_kernel<DT_F32><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr, round_in);
   else
-    ns_init_state_vec_kernel<DT_F64><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr);
+    ns_init_state_vec_kernel<DT_F64><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr, round_in);
 }
 
 // out_hi/lo = split(factor * G), full h x h (the cubic step operator B = -0.5 G).

@@ -1432,14 +1432,14 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
   if (p.scaling == UNSO_SCALING_NONE) {
     xscale = nullptr;
   } else if (p.scaling == UNSO_SCALING_PLAIN) {
-    launch_sumsq(x, p.dt, p.rows, p.cols, p.ld, p.bs, B, at<double>(ws, pl.blk), st);
+    launch_sumsq(x, p.dt, p.rows, p.cols, p.ld, p.bs, B, at<double>(ws, pl.blk), st, /*round_in=*/true);
     UNSO_CHECK_LAUNCH();
     scalars_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, SM_PLAIN, p.gpow,
                                                             scal, status);
     UNSO_CHECK_LAUNCH();
   } else {  // gram / gelfand: Gram of the unscaled bf16 input on the tensor cores
     launch_ns_init_state(x, p.dt, p.ld, p.bs, nullptr, at<float>(ws, pl.Xs[0]), xb, ldx, p.rows, p.cols,
-                         static_cast<int>(B), st);
+                         static_cast<int>(B), /*round_in=*/1, st);
     UNSO_CHECK_LAUNCH();
     UNSO_TRY(gram_bf16(p, pl, ws, xb, ldx, bsx, st));
     UNSO_TRY(finalize_gram<float>(p, pl, ws, pl.splits, at<float>(ws, pl.G), st));
@@ -1448,7 +1448,7 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
       UNSO_TRY(gelfand_scale<float>(p, pl, ws, at<float>(ws, pl.G), DT_F32, status, st));
   }
   launch_ns_init_state(x, p.dt, p.ld, p.bs, xscale, at<float>(ws, pl.Xs[0]), xb, ldx, p.rows, p.cols,
-                       static_cast<int>(B), st);
+                       static_cast<int>(B), /*round_in=*/1, st);
   UNSO_CHECK_LAUNCH();
   const dim3 egrid(grid_for(static_cast<int64_t>(h) * h, 256, 1024), static_cast<unsigned>(B));
   int cur = 0;

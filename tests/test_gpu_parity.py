@@ -199,20 +199,25 @@ def test_preprocess_and_bare_kernels_match_oracle():
 
 
 # ------------------------------------------------------------------ larger / BASELINE-shaped cases
-def test_cfg2_full_fp32_mode():
-    """configs[1]: 16 x 2048x512 controlled spectrum s ~ logU[1e-4, 1], fp32 mode <= 1e-5."""
+@pytest.mark.parametrize("method", ["unso", "muon5"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_cfg2_full(precision, method):
+    """configs[1]: 16 x 2048x512 controlled spectrum s ~ logU[1e-4, 1] against the oracle on the same
+    (mode-rounded) input, UNSO and the Muon-5 comparison path: fp32 <= 1e-5, bf16 <= 2e-2."""
     rng = np.random.default_rng(2)
     ms = np.stack([O.controlled_spectrum_matrix(2048, 512, np.exp(rng.uniform(np.log(1e-4), 0, 512)), 100 + i)
                    for i in range(16)]).astype(np.float32)
-    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients())
-    res = U.orthogonalize(torch.from_numpy(ms).to(DEV), spec, precision="fp32")
+    spec = (U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()) if method == "unso"
+            else U.MethodSpec(U.MethodKind.MUON_NS, iterations=5))
+    res = U.orthogonalize(torch.from_numpy(ms).to(DEV), spec, precision=precision)
     y = res.y.double().cpu().numpy()
     worst = 0.0
     for i in range(16):
-        ref = O.run(ms[i].astype(np.float64), "unso")["y"]
+        inp = ms[i].astype(np.float64) if precision == "fp32" else bf16_round(ms[i])
+        ref = O.run(inp, "unso")["y"] if method == "unso" else O.run(inp, "muon", iterations=5)["y"]
         worst = max(worst, rel(y[i], ref))
-    print(f"cfg2 fp32 worst rel err {worst:.2e}")
-    assert worst <= TOL["fp32"]
+    print(f"cfg2 {method} {precision} worst rel err {worst:.2e}")
+    assert worst <= TOL[precision]
 
 
 @pytest.mark.parametrize("method", ["unso", "muon5"])
