@@ -156,3 +156,34 @@ def test_ns_layouts_vectorized_and_fallback(precision, dtype):
              gaussian((250, 37), 64, dtype), gaussian((400, 133), 65, dtype)[:, :130]]
     for x in cases:
         check(x, MUON, "muon", precision)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float64])
+def test_method_mode_dtype_matrix(mode, dtype):
+    """Every method kind and scaling x precision mode x input dtype, tall and wide, on an
+    ill-conditioned (log-uniform, 1e-4) spectrum, against the oracle on the values the mode computes
+    on (profiles/round1_parity_sweep_methods_modes_dtypes.txt has the wider sweep)."""
+    ces = U.CesistaStepParams(U.default_cesista_triples())
+    methods = [
+        (U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()), dict(method="unso")),
+        (U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), scaling="plain"),
+         dict(method="unso", scaling="plain")),
+        (U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), scaling="gelfand"),
+         dict(method="unso", scaling="gelfand")),
+        (MUON, dict(method="muon", iterations=5)),
+        (U.MethodSpec(U.MethodKind.ORIGINAL_NS, iterations=8), dict(method="original", iterations=8)),
+        (U.MethodSpec(U.MethodKind.CESISTA_NS, step_params=ces),
+         dict(method="cesista", rows=O.cesista_rows(O.CESISTA_DEFAULT_TRIPLES))),
+    ]
+    rng = np.random.default_rng(3)
+    for shape in ((1024, 256), (256, 1024)):
+        m = O.controlled_spectrum_matrix(*shape, np.exp(rng.uniform(np.log(1e-4), 0.0, 256)), 70 + shape[0])
+        x = torch.from_numpy(m).to(DEV, dtype)
+        vals = (x if mode == "fp32" else x.to(torch.bfloat16)).double().cpu().numpy()
+        tol = TOL[mode] + (2.0 ** -9 if dtype == torch.bfloat16 else 0.0)
+        for spec, kw in methods:
+            y = U.orthogonalize(x, spec, precision=mode).y
+            assert y.dtype == dtype
+            r = rel(y.double().cpu().numpy(), O.run(vals, **kw)["y"])
+            assert r <= tol, (shape, mode, dtype, kw, r)
