@@ -7,7 +7,14 @@
 
 namespace unso {
 
-constexpr int NORM_BLOCKS = 256;  // per-matrix partial-reduction blocks (fixed -> deterministic)
+constexpr int NORM_BLOCKS = 1024;  // max per-matrix partial-reduction blocks (workspace slots)
+// Partial-reduction blocks for a matrix of `elems` elements: ~16K elements per block, at most
+// NORM_BLOCKS; a pure function of the shape, so the partials (and their fixed-order sum) are
+// deterministic.  The producing kernel's grid.x and the scalars_kernel's nblk must both use it.
+inline int norm_blocks(int64_t elems) {
+  const int64_t n = (elems + 16383) / 16384;
+  return static_cast<int>(n < 1 ? 1 : (n > NORM_BLOCKS ? NORM_BLOCKS : n));
+}
 
 // scal[b * SCAL_STRIDE + ...]
 // S_SHIFT: d/s, the identity shift removed from P before the bf16 split (added back as d/s * X in the
@@ -213,7 +220,14 @@ __global__ void sumsq_vec_kernel(const void* __restrict__ x, int64_t rows, int64
   double s = 0.0;
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * rpi + sub; r < rows; r += static_cast<int64_t>(gridDim.x) * rpi) {
     const uint4* row = reinterpret_cast<const uint4*>(base + r * ld * E);
-    for (int64_t c = li; c < cpr; c += tpr) s += sumsq_chunk<DT, ROUND>(__ldcs(row + c));
+    int64_t c = li;
+    for (; c + 3 * tpr < cpr; c += 4 * tpr) {  // four independent 16-byte loads in flight per thread
+      const uint4 v0 = __ldcs(row + c), v1 = __ldcs(row + c + tpr), v2 = __ldcs(row + c + 2 * tpr),
+                  v3 = __ldcs(row + c + 3 * tpr);
+      s += (sumsq_chunk<DT, ROUND>(v0) + sumsq_chunk<DT, ROUND>(v1)) +
+           (sumsq_chunk<DT, ROUND>(v2) + sumsq_chunk<DT, ROUND>(v3));
+    }
+    for (; c < cpr; c += tpr) s += sumsq_chunk<DT, ROUND>(__ldcs(row + c));
   }
   s = block_sum(s, scratch);
   if (threadIdx.x == 0) {
@@ -224,14 +238,14 @@ __global__ void sumsq_vec_kernel(const void* __restrict__ x, int64_t rows, int64
   }
 }
 
-// Plain-scaling partials (NORM_BLOCKS per matrix into blk), vectorized when the layout allows.
+// Plain-scaling partials (norm_blocks(rows * cols) per matrix into blk), vectorized when the layout allows.
 // round_in: square the bf16-rounded values (bf16-mode NS path, see launch_ns_init_state).
 inline void launch_sumsq(const void* x, int dt, int64_t rows, int64_t cols, int64_t ld, int64_t bs, int64_t batch,
                          double* blk, cudaStream_t st, bool round_in = false) {
   const int e = dt == DT_F64 ? 8 : (dt == DT_F32 ? 4 : 2), v = 16 / e;
   const bool vec = (cols % v) == 0 && ((ld * e) & 15) == 0 && ((bs * e) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-  const dim3 grid(NORM_BLOCKS, static_cast<unsigned>(batch));
+  const dim3 grid(norm_blocks(rows * cols), static_cast<unsigned>(batch));
   if (!vec) {
     sumsq_kernel<<<grid, 256, 0, st>>>(x, dt, rows, cols, ld, bs, blk, round_in ? 1 : 0);
     return;

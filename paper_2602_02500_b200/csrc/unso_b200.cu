@@ -650,10 +650,11 @@ static int32_t finalize_gram(const Problem& p, const Plan& pl, void* ws, int spl
 template <typename T>
 static int32_t norms_and_scalars(const Problem& p, const Plan& pl, void* ws, const T* G, int mode, int32_t* status,
                                  cudaStream_t st) {
-  dim3 grid(NORM_BLOCKS, static_cast<unsigned>(p.batch));
+  const int nb = norm_blocks(p.h * p.h);
+  dim3 grid(nb, static_cast<unsigned>(p.batch));
   gram_norms_kernel<T><<<grid, 256, 0, st>>>(G, static_cast<int>(p.h), pl.ldc, at<double>(ws, pl.blk));
   UNSO_CHECK_LAUNCH();
-  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, mode, p.gpow,
+  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(ws, pl.blk), nb, mode, p.gpow,
                                                                   at<double>(ws, pl.scal), status);
   UNSO_CHECK_LAUNCH();
   return UNSO_OK;
@@ -679,10 +680,11 @@ static int32_t gelfand_scale(const Problem& p, const Plan& pl, void* ws, const T
     prev_dt = DT_F64;
     cur ^= 1;
   }
-  dim3 grid(NORM_BLOCKS, static_cast<unsigned>(p.batch));
+  const int nb = norm_blocks(p.h * p.h);
+  dim3 grid(nb, static_cast<unsigned>(p.batch));
   gram_norms_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(prev), h, pl.ldc, at<double>(ws, pl.blk));
   UNSO_CHECK_LAUNCH();
-  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, SM_GELFAND,
+  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(ws, pl.blk), nb, SM_GELFAND,
                                                                   p.gpow, at<double>(ws, pl.scal), status);
   UNSO_CHECK_LAUNCH();
   return UNSO_OK;
@@ -1356,7 +1358,7 @@ static int32_t ns_fp32(const Problem& p, const Plan& pl, void* ws, const void* x
   } else if (p.scaling == UNSO_SCALING_PLAIN) {
     launch_sumsq(x, p.dt, p.rows, p.cols, p.ld, p.bs, B, at<double>(ws, pl.blk), st);
     UNSO_CHECK_LAUNCH();
-    scalars_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, SM_PLAIN, p.gpow,
+    scalars_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(at<double>(ws, pl.blk), norm_blocks(p.rows * p.cols), SM_PLAIN, p.gpow,
                                                             at<double>(ws, pl.scal), status);
     UNSO_CHECK_LAUNCH();
   } else {
@@ -1434,7 +1436,7 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
   } else if (p.scaling == UNSO_SCALING_PLAIN) {
     launch_sumsq(x, p.dt, p.rows, p.cols, p.ld, p.bs, B, at<double>(ws, pl.blk), st, /*round_in=*/true);
     UNSO_CHECK_LAUNCH();
-    scalars_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(at<double>(ws, pl.blk), NORM_BLOCKS, SM_PLAIN, p.gpow,
+    scalars_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(at<double>(ws, pl.blk), norm_blocks(p.rows * p.cols), SM_PLAIN, p.gpow,
                                                             scal, status);
     UNSO_CHECK_LAUNCH();
   } else {  // gram / gelfand: Gram of the unscaled bf16 input on the tensor cores
@@ -1828,7 +1830,7 @@ int32_t unso_scale_denominator(const unso_matrix_desc* x, const void* x_ptr, con
   if (p.scaling == UNSO_SCALING_PLAIN) {
     launch_sumsq(x_ptr, p.dt, p.rows, p.cols, p.ld, p.bs, p.batch, at<double>(workspace, pl.blk), st);
     UNSO_CHECK_LAUNCH();
-    scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(workspace, pl.blk), NORM_BLOCKS,
+    scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(workspace, pl.blk), norm_blocks(p.rows * p.cols),
                                                                     SM_PLAIN, 1, at<double>(workspace, pl.scal),
                                                                     d_status);
     UNSO_CHECK_LAUNCH();
@@ -1860,11 +1862,12 @@ int32_t unso_ortho_error(const unso_matrix_desc* y, const void* y_ptr, double* d
   UNSO_TRY(check_ws(pl, workspace, workspace_bytes));
   UNSO_TRY(gram_simt(p, y_ptr, p.dt, p.ld, p.bs, pl, workspace, pl.splits, st));
   UNSO_TRY(finalize_gram<double>(p, pl, workspace, pl.splits, at<double>(workspace, pl.G), st));
-  dim3 grid(NORM_BLOCKS, static_cast<unsigned>(p.batch));
+  const int nb = norm_blocks(p.h * p.h);
+  dim3 grid(nb, static_cast<unsigned>(p.batch));
   gram_norms_kernel<double><<<grid, 256, 0, st>>>(at<double>(workspace, pl.G), static_cast<int>(p.h), pl.ldc,
                                                   at<double>(workspace, pl.blk));
   UNSO_CHECK_LAUNCH();
-  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(workspace, pl.blk), NORM_BLOCKS, SM_ERROR,
+  scalars_kernel<<<static_cast<unsigned>(p.batch), 256, 0, st>>>(at<double>(workspace, pl.blk), nb, SM_ERROR,
                                                                   1, at<double>(workspace, pl.scal), nullptr);
   UNSO_CHECK_LAUNCH();
   copy_err_kernel<<<static_cast<unsigned>((p.batch + 127) / 128), 128, 0, st>>>(at<double>(workspace, pl.scal),
