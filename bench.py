@@ -50,7 +50,8 @@ def parse_args():
                     help="bf16 apply split: default adaptive per matrix (device-side bound)")
     ap.add_argument("--e2e-steps", type=int, default=30,
                     help="pipelined e2e steps (fill and drain of the three-stream pipeline amortised over them)")
-    ap.add_argument("--cpu-sample-rows", type=int, default=32768)
+    ap.add_argument("--cpu-sample-rows", type=int, default=65536,
+                    help="rows of the cpu_baseline sample (~10 s of OpenBLAS fp64 on the GPU box host)")
     ap.add_argument("--ref-sample-rows", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
