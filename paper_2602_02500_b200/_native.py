@@ -41,6 +41,7 @@ SCALAR_NAMES = ("trace", "fro2", "dev2", "s2", "inv_s", "ortho_error", "shift", 
 FLAG_TWO_TERM_APPLY = 0x2
 FLAG_NO_TRUNCATION = 0x8
 FLAG_CHAIN_BF16X3 = 0x4
+FLAG_NS_SINGLE_STATE = 0x10
 PROFILE_STAGES = ("convert", "gram", "scale_prep", "chain", "finalize_p", "apply")
 
 

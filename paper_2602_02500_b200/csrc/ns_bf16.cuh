@@ -14,7 +14,7 @@ namespace unso {
 __global__ void ns_init_state_kernel(const void* __restrict__ src, int sdt, int64_t sld, int64_t sbs,
                                      const double* __restrict__ scal, float* __restrict__ xf,
                                      __nv_bfloat16* __restrict__ xb, int64_t xld, int64_t rows, int64_t cols,
-                                     int batch, int round_in) {
+                                     int batch, int round_in, __nv_bfloat16* __restrict__ xlo) {
   const int64_t per = rows * cols, total = per * batch;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -24,7 +24,9 @@ __global__ void ns_init_state_kernel(const void* __restrict__ src, int sdt, int6
     if (scal) v *= scal[b * SCAL_STRIDE + S_INV_S];
     const float f = static_cast<float>(v);
     xf[b * per + r * cols + c] = f;
-    xb[b * rows * xld + r * xld + c] = __float2bfloat16_rn(f);
+    const __nv_bfloat16 hb = __float2bfloat16_rn(f);
+    xb[b * rows * xld + r * xld + c] = hb;
+    if (xlo) xlo[b * rows * xld + r * xld + c] = __float2bfloat16_rn(f - __bfloat162float(hb));
   }
 }
 
@@ -35,7 +37,7 @@ template <int SDT>
 __global__ void ns_init_state_vec_kernel(const void* __restrict__ src, int64_t sld, int64_t sbs,
                                          const double* __restrict__ scal, float* __restrict__ xf,
                                          __nv_bfloat16* __restrict__ xb, int64_t xld, int64_t rows, int64_t cols,
-                                         int batch, int tpr, int round_in) {
+                                         int batch, int tpr, int round_in, __nv_bfloat16* __restrict__ xlo) {
   constexpr int E = SDT == DT_F64 ? 8 : (SDT == DT_F32 ? 4 : 2);
   const int64_t cpr = cols / 8, nrows = rows * batch;
   const int rpi = blockDim.x / tpr, sub = threadIdx.x / tpr, li = threadIdx.x % tpr;
@@ -74,12 +76,14 @@ __global__ void ns_init_state_vec_kernel(const void* __restrict__ src, int64_t s
       }
       *reinterpret_cast<float4*>(frow + c * 8) = make_float4(f[0], f[1], f[2], f[3]);
       *reinterpret_cast<float4*>(frow + c * 8 + 4) = make_float4(f[4], f[5], f[6], f[7]);
-      uint4 o;
-      o.x = pack_bf16x2(f[0], f[1]);
-      o.y = pack_bf16x2(f[2], f[3]);
-      o.z = pack_bf16x2(f[4], f[5]);
-      o.w = pack_bf16x2(f[6], f[7]);
-      *reinterpret_cast<uint4*>(brow + c * 8) = o;
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        hw[e] = pack_bf16x2(f[2 * e], f[2 * e + 1]);
+        lw[e] = pack_bf16x2(f[2 * e] - bf16_lo_to_f32(hw[e]), f[2 * e + 1] - bf16_hi_to_f32(hw[e]));
+      }
+      *reinterpret_cast<uint4*>(brow + c * 8) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      if (xlo) *reinterpret_cast<uint4*>(xlo + (b * rows + r) * xld + c * 8) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
   }
 }
@@ -88,15 +92,16 @@ __global__ void ns_init_state_vec_kernel(const void* __restrict__ src, int64_t s
 // input, the same values the UNSO path and the parity oracle see).
 inline void launch_ns_init_state(const void* src, int sdt, int64_t sld, int64_t sbs, const double* scal, float* xf,
                                  __nv_bfloat16* xb, int64_t xld, int64_t rows, int64_t cols, int batch,
-                                 int round_in, cudaStream_t st) {
+                                 int round_in, cudaStream_t st, __nv_bfloat16* xlo = nullptr) {
   const int e = sdt == DT_F64 ? 8 : (sdt == DT_F32 ? 4 : 2);
   const bool vec = (cols % 8) == 0 && ((sld * e) & 15) == 0 && ((sbs * e) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (xld % 8) == 0 &&
-                   (reinterpret_cast<uintptr_t>(xb) & 15) == 0 && (reinterpret_cast<uintptr_t>(xf) & 15) == 0;
+                   (reinterpret_cast<uintptr_t>(xb) & 15) == 0 && (reinterpret_cast<uintptr_t>(xf) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(xlo) & 15) == 0;
   if (!vec) {
     const int64_t total = rows * cols * batch;
     const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
-    ns_init_state_kernel<<<blocks, 256, 0, st>>>(src, sdt, sld, sbs, scal, xf, xb, xld, rows, cols, batch, round_in);
+    ns_init_state_kernel<<<blocks, 256, 0, st>>>(src, sdt, sld, sbs, scal, xf, xb, xld, rows, cols, batch, round_in, xlo);
     return;
   }
   const int64_t cpr = cols / 8;
@@ -105,11 +110,11 @@ inline void launch_ns_init_state(const void* src, int sdt, int64_t sld, int64_t 
   const int64_t nrows = rows * batch;
   const int blocks = static_cast<int>(std::min<int64_t>((nrows + 256 / tpr - 1) / (256 / tpr), 148 * 16));
   if (sdt == DT_BF16)
-    ns_init_state_vec_kernel<DT_BF16><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr, round_in);
+    ns_init_state_vec_kernel<DT_BF16><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr, round_in, xlo);
   else if (sdt == DT_F32)
-    ns_init_state_vec_kernel<DT_F32><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr, round_in);
+    ns_init_state_vec_kernel<DT_F32><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr, round_in, xlo);
   else
-    ns_init_state_vec_kernel<DT_F64><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr, round_in);
+    ns_init_state_vec_kernel<DT_F64><<<blocks, 256, 0, st>>>(src, sld, sbs, scal, xf, xb, xld, rows, cols, batch, tpr, round_in, xlo);
 }
 
 // out_hi/lo = split(factor * G), full h x h (the cubic step operator B = -0.5 G).
@@ -161,6 +166,7 @@ struct EpiNSUpdate {
   int64_t rows, cols;     // state is rows x cols, ld = cols
   int M, N;               // output tile bounds (= rows, cols in the matrix's own layout)
   float alpha;
+  __nv_bfloat16* xlo = nullptr;  // optional bf16 lo part of the new state (hi/lo products)
   __device__ __forceinline__ void operator()(int b, int, int row, int col0, const float (&v)[32]) const {
     if (row >= M) return;
     const int64_t o = static_cast<int64_t>(b) * rows * cols + static_cast<int64_t>(row) * cols + col0;
@@ -178,17 +184,25 @@ struct EpiNSUpdate {
         *reinterpret_cast<float4*>(xnew + o + 4 * j) = make_float4(xn[4 * j], xn[4 * j + 1], xn[4 * j + 2], xn[4 * j + 3]);
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        *reinterpret_cast<uint4*>(xb + ob + 8 * j) =
-            make_uint4(pack_bf16x2(xn[8 * j], xn[8 * j + 1]), pack_bf16x2(xn[8 * j + 2], xn[8 * j + 3]),
-                       pack_bf16x2(xn[8 * j + 4], xn[8 * j + 5]), pack_bf16x2(xn[8 * j + 6], xn[8 * j + 7]));
+      for (int j = 0; j < 4; ++j) {
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          hw[e] = pack_bf16x2(xn[8 * j + 2 * e], xn[8 * j + 2 * e + 1]);
+          lw[e] = pack_bf16x2(xn[8 * j + 2 * e] - bf16_lo_to_f32(hw[e]), xn[8 * j + 2 * e + 1] - bf16_hi_to_f32(hw[e]));
+        }
+        *reinterpret_cast<uint4*>(xb + ob + 8 * j) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        if (xlo) *reinterpret_cast<uint4*>(xlo + ob + 8 * j) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         if (col0 + j < N) {
           const float x = fmaf(alpha, xold[o + j], v[j]);
           xnew[o + j] = x;
-          xb[ob + j] = __float2bfloat16_rn(x);
+          const __nv_bfloat16 hb = __float2bfloat16_rn(x);
+          xb[ob + j] = hb;
+          if (xlo) xlo[ob + j] = __float2bfloat16_rn(x - __bfloat162float(hb));
         }
       }
     }

@@ -486,6 +486,7 @@ struct Plan {
   size_t normbuf = 0, pstat = 0, gbar = 0;        // persistent chain: per-tile norms / P stats, grid barrier
   size_t Xs[2] = {0, 0};                          // NS state (f64 in FP32 mode, f32 in BF16 mode)
   size_t xb2 = 0;                                 // NS BF16: second bf16 operand buffer (ping-pong)
+  size_t xl[2] = {0, 0};                          // NS BF16: bf16 lo parts of the state (hi/lo products)
   size_t mnorm = 0, mpstat = 0;                   // multi-launch pipeline: norm / final-P partials
   size_t C8h[2] = {0, 0}, C8l[2] = {0, 0};        // e4m3 operand planes of C_k (2^8 hi, 2^16 lo)
   size_t C8i[2] = {0, 0};                         // e4m3 interleaved [hi8 | lo8] per 64-column block
@@ -593,6 +594,10 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       pl.xb = take(pl, static_cast<size_t>(B * p.rows * pl.ldx) * 2);
     }
     pl.xb2 = take(pl, static_cast<size_t>(B * p.rows * pl.ldx) * 2);
+    if ((p.flags & UNSO_FLAG_NS_SINGLE_STATE) == 0) {
+      pl.xl[0] = take(pl, static_cast<size_t>(B * p.rows * pl.ldx) * 2);
+      pl.xl[1] = take(pl, static_cast<size_t>(B * p.rows * pl.ldx) * 2);
+    }
     pl.Xs[0] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 4);
     pl.Xs[1] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 4);
     pl.Chi[0] = take(pl, static_cast<size_t>(B * pl.hh) * 2);
@@ -1416,6 +1421,36 @@ static int32_t ns_fp32(const Problem& p, const Plan& pl, void* ws, const void* x
 // ---------------------------------------------------------------- NS baselines (BF16 precision, tcgen05)
 using Cfg2NSTall = Umma2Cfg<256, 1, 2, 2, TERM(0, 0, 0) | TERM(1, 0, 1), false, false, 4>;
 using Cfg2NSWide = Umma2Cfg<256, 2, 1, 2, TERM(0, 0, 0) | TERM(1, 1, 0), false, true, 4>;
+// hi/lo state (default): X = X_hi + X_lo in every long-side product, bf16x3 (hi*hi + hi*lo + lo*hi)
+constexpr int TERMS_X3 = TERM(0, 0, 0) | TERM(1, 0, 1) | TERM(2, 1, 0);
+using Cfg2GramMN3 = Umma2Cfg<256, 2, 2, 3, TERMS_X3, true, true, 3>;
+using Cfg2GramK3 = Umma2Cfg<256, 2, 2, 3, TERMS_X3, false, false, 3>;
+using Cfg2NSTall3 = Umma2Cfg<256, 2, 2, 3, TERMS_X3, false, false, 3>;
+using Cfg2NSWide3 = Umma2Cfg<256, 2, 2, 3, TERMS_X3, false, true, 3>;
+
+// Gram of the NS state from its bf16 hi/lo parts (split-K partials, like gram_bf16).
+static int32_t gram_bf16_x3(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xh,
+                            const __nv_bfloat16* xl, int64_t ldx, int64_t bsx, cudaStream_t st) {
+  CUtensorMap mh, ml;
+  UEpiPartialF32 epi{at<float>(ws, pl.part), pl.hh, pl.ldc, static_cast<int>(p.batch), static_cast<int>(p.h)};
+  const UmmaWork w2 = umma2_make_work(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 256,
+                                      static_cast<int>(p.batch), true, pl.splits);
+  cudaError_t e;
+  if (p.tall) {
+    if (!umma_make_mnmajor_map(&mh, xh, p.rows, p.cols, ldx, p.batch, bsx) ||
+        !umma_make_mnmajor_map(&ml, xl, p.rows, p.cols, ldx, p.batch, bsx))
+      return UNSO_ERR_CUDA;
+    e = launch_umma2<Cfg2GramMN3>(mh, ml, mh, ml, w2, epi, st);
+  } else {
+    if (!umma_make_kmajor_map(&mh, xh, p.rows, p.cols, ldx, p.batch, bsx, 128) ||
+        !umma_make_kmajor_map(&ml, xl, p.rows, p.cols, ldx, p.batch, bsx, 128))
+      return UNSO_ERR_CUDA;
+    e = launch_umma2<Cfg2GramK3>(mh, ml, mh, ml, w2, epi, st);
+  }
+  if (e != cudaSuccess) return UNSO_ERR_CUDA;
+  ++g_launches;
+  return UNSO_OK;
+}
 
 static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x, void* y, int32_t* status,
                        cudaStream_t st) {
@@ -1424,6 +1459,11 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
   const int64_t xsz = p.rows * p.cols;
   __nv_bfloat16* xbs[2] = {at<__nv_bfloat16>(ws, pl.xb), at<__nv_bfloat16>(ws, pl.xb2)};
   __nv_bfloat16* xb = xbs[0];
+  // hi/lo state: every long-side product (Gram of X_k, X_k B) uses X_k = hi + lo in bf16x3, so the
+  // fp32 state enters the tensor cores at ~2^-17 instead of bf16 rounding (Muon-5: ~1e-2 -> ~1e-4
+  // from the fp64 result, at 3 + 3 instead of 1 + 2 bf16 products per step).
+  const bool x3 = (p.flags & UNSO_FLAG_NS_SINGLE_STATE) == 0 && use_pair_engine();
+  __nv_bfloat16* xls[2] = {x3 ? at<__nv_bfloat16>(ws, pl.xl[0]) : nullptr, x3 ? at<__nv_bfloat16>(ws, pl.xl[1]) : nullptr};
   const int64_t ldx = pl.ldx, bsx = p.rows * pl.ldx;
   double* scal = at<double>(ws, pl.scal);
   double* unit = at<double>(ws, pl.normbuf);
@@ -1450,13 +1490,16 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
       UNSO_TRY(gelfand_scale<float>(p, pl, ws, at<float>(ws, pl.G), DT_F32, status, st));
   }
   launch_ns_init_state(x, p.dt, p.ld, p.bs, xscale, at<float>(ws, pl.Xs[0]), xb, ldx, p.rows, p.cols,
-                       static_cast<int>(B), /*round_in=*/1, st);
+                       static_cast<int>(B), /*round_in=*/1, st, xls[0]);
   UNSO_CHECK_LAUNCH();
   const dim3 egrid(grid_for(static_cast<int64_t>(h) * h, 256, 1024), static_cast<unsigned>(B));
   int cur = 0;
   for (int it = 0; it < p.steps; ++it) {
     xb = xbs[cur];  // read this step's operand, write the next one into the other buffer
-    UNSO_TRY(gram_bf16(p, pl, ws, xb, ldx, bsx, st));
+    if (x3)
+      UNSO_TRY(gram_bf16_x3(p, pl, ws, xb, xls[cur], ldx, bsx, st));
+    else
+      UNSO_TRY(gram_bf16(p, pl, ws, xb, ldx, bsx, st));
     UNSO_TRY(finalize_gram<float>(p, pl, ws, pl.splits, at<float>(ws, pl.G), st));
     const float* G = at<float>(ws, pl.G);
     float a_c;
@@ -1492,16 +1535,27 @@ static int32_t ns_bf16(const Problem& p, const Plan& pl, void* ws, const void* x
     const float* xo = at<float>(ws, pl.Xs[cur]);
     float* xn = at<float>(ws, pl.Xs[cur ^ 1]);
     cudaError_t e;
+    CUtensorMap mxl;
     if (p.tall) {
       if (!umma_make_kmajor_map(&mx, xb, p.rows, p.cols, ldx, B, bsx, 128)) return UNSO_ERR_CUDA;
-      EpiNSUpdate epi{xo, xn, xbs[cur ^ 1], ldx, p.rows, p.cols, static_cast<int>(p.rows), h, a_c};
+      EpiNSUpdate epi{xo, xn, xbs[cur ^ 1], ldx, p.rows, p.cols, static_cast<int>(p.rows), h, a_c, xls[cur ^ 1]};
       const UmmaWork wa = umma2_make_work(static_cast<int>(p.rows), h, h, 256, static_cast<int>(B), false, 1);
-      e = launch_umma2<Cfg2NSTall>(mx, mx, mph, mpl, wa, epi, st);
+      if (x3) {
+        if (!umma_make_kmajor_map(&mxl, xls[cur], p.rows, p.cols, ldx, B, bsx, 128)) return UNSO_ERR_CUDA;
+        e = launch_umma2<Cfg2NSTall3>(mx, mxl, mph, mpl, wa, epi, st);
+      } else {
+        e = launch_umma2<Cfg2NSTall>(mx, mx, mph, mpl, wa, epi, st);
+      }
     } else {
       if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, B, bsx)) return UNSO_ERR_CUDA;
-      EpiNSUpdate epi{xo, xn, xbs[cur ^ 1], ldx, p.rows, p.cols, h, static_cast<int>(p.cols), a_c};
+      EpiNSUpdate epi{xo, xn, xbs[cur ^ 1], ldx, p.rows, p.cols, h, static_cast<int>(p.cols), a_c, xls[cur ^ 1]};
       const UmmaWork wa = umma2_make_work(h, static_cast<int>(p.cols), h, 256, static_cast<int>(B), false, 1);
-      e = launch_umma2<Cfg2NSWide>(mph, mpl, mx, mx, wa, epi, st);
+      if (x3) {
+        if (!umma_make_mnmajor_map(&mxl, xls[cur], p.rows, p.cols, ldx, B, bsx)) return UNSO_ERR_CUDA;
+        e = launch_umma2<Cfg2NSWide3>(mph, mpl, mx, mxl, wa, epi, st);
+      } else {
+        e = launch_umma2<Cfg2NSWide>(mph, mpl, mx, mx, wa, epi, st);
+      }
     }
     if (e != cudaSuccess) return UNSO_ERR_CUDA;
     ++g_launches;

@@ -77,6 +77,8 @@ class MethodSpec:
     apply_terms: int | None = None   # bf16 mode: None = adaptive per matrix, 1 = P_hi only, 2 = P_hi + P_lo
     chain: str | None = None         # bf16 mode, large h: None = bf16 hi*hi + e4m3 cross terms, "bf16x3"
     truncate: bool = True            # bf16 mode, persistent chain: stop once ||I - C_k||_F bounds the rest
+    ns_products: str | None = None   # bf16 mode, NS kinds: None / "bf16x3" = hi/lo state in the long-side
+                                     # products (~1e-4 from fp64), "bf16" = one bf16 term (faster, ~1e-2)
 
     def __post_init__(self):
         object.__setattr__(self, "_cache", {})  # per-spec memo of the native method descriptor / FLOP model
@@ -92,6 +94,8 @@ class MethodSpec:
             raise ValueError("apply_terms must be None (adaptive), 1 or 2")
         if self.chain not in (None, "bf16x3"):
             raise ValueError("chain must be None (bf16 + e4m3 cross terms) or 'bf16x3'")
+        if self.ns_products not in (None, "bf16x3", "bf16"):
+            raise ValueError("ns_products must be None / 'bf16x3' (hi/lo state) or 'bf16'")
         if kind is MethodKind.UNSO:
             if self.coeffs is None:
                 raise ValueError("unso requires a CoefficientSet")
@@ -329,6 +333,8 @@ def _build_method_desc(spec: MethodSpec, precision: Precision, scaling_code: int
         method, order, steps = N.METHOD_QUINTIC, 0, rows.shape[0]
     co = np.ascontiguousarray(co, dtype=np.float64)
     flags = {None: 0, 1: N.FLAG_SINGLE_TERM_APPLY, 2: N.FLAG_TWO_TERM_APPLY}[spec.apply_terms]
+    if spec.ns_products == "bf16":
+        flags |= N.FLAG_NS_SINGLE_STATE
     if spec.chain == "bf16x3":
         flags |= N.FLAG_CHAIN_BF16X3
     if not spec.truncate:

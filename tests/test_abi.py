@@ -137,6 +137,7 @@ def test_header_constants_match_the_binding():
         "UNSO_METHOD_QUINTIC": N.METHOD_QUINTIC,
         "UNSO_FLAG_SINGLE_TERM_APPLY": N.FLAG_SINGLE_TERM_APPLY, "UNSO_FLAG_TWO_TERM_APPLY": N.FLAG_TWO_TERM_APPLY,
         "UNSO_FLAG_CHAIN_BF16X3": N.FLAG_CHAIN_BF16X3, "UNSO_FLAG_NO_TRUNCATION": N.FLAG_NO_TRUNCATION,
+        "UNSO_FLAG_NS_SINGLE_STATE": N.FLAG_NS_SINGLE_STATE,
         "UNSO_MAX_PEERS": N.MAX_PEERS, "UNSO_SCALARS": N.SCALARS, "UNSO_PROFILE_STAGES": len(N.PROFILE_STAGES),
     }
     for name, value in expect.items():

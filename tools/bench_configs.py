@@ -150,6 +150,9 @@ def main():
         results.append(run("cfg4 262144x2048 unso", x, unso, "bf16", 1, 2048, 262144, reps=10))
         # the comparison path on the same input: 5 Muon-coefficient NS steps (reference-model FLOPs)
         results.append(run("cfg4 262144x2048 muon5", x, muon, "bf16", 1, 2048, 262144, reps=3))
+        muon_fast = U.MethodSpec(U.MethodKind.MUON_NS, iterations=5, ns_products="bf16")
+        results.append(run("cfg4 262144x2048 muon5 (single-bf16 state products)", x, muon_fast, "bf16", 1, 2048,
+                           262144, reps=3))
         del x
     if "cfg5" in only:
         u = torch.rand(4, 8192, generator=g, device=DEV, dtype=torch.float64)
