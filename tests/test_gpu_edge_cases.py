@@ -187,3 +187,18 @@ def test_method_mode_dtype_matrix(mode, dtype):
             assert y.dtype == dtype
             r = rel(y.double().cpu().numpy(), O.run(vals, **kw)["y"])
             assert r <= tol, (shape, mode, dtype, kw, r)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_ns_batched_tall_and_wide(precision):
+    """Batched NS (Muon-5, cubic) calls equal the oracle per matrix, tall and wide, with a matrix of a
+    different scale in the batch (per-matrix plain scaling)."""
+    for shape in ((4, 600, 200), (4, 200, 600)):
+        x = gaussian(shape, 90 + shape[1])
+        x[2] *= 1e-3
+        check(x, MUON, "muon", precision)
+        orig = U.MethodSpec(U.MethodKind.ORIGINAL_NS, iterations=6)
+        res = U.orthogonalize(x, orig, precision=precision)
+        vals = (x if precision == "fp32" else x.to(torch.bfloat16)).double().cpu().numpy()
+        ref = np.stack([O.run(m, "original", iterations=6)["y"] for m in vals])
+        assert rel(res.y.double().cpu().numpy(), ref) <= TOL[precision]
