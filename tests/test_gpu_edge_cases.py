@@ -202,3 +202,18 @@ def test_ns_batched_tall_and_wide(precision):
         vals = (x if precision == "fp32" else x.to(torch.bfloat16)).double().cpu().numpy()
         ref = np.stack([O.run(m, "original", iterations=6)["y"] for m in vals])
         assert rel(res.y.double().cpu().numpy(), ref) <= TOL[precision]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("power", [1, 3])
+def test_gelfand_powers(precision, power):
+    """Gelfand scaling ||(A A^T)^k||_F^(1/(2k)) for k != 2 (ortho.py:158-163), UNSO and Muon-5."""
+    x = gaussian((700, 180), 120 + power)
+    vals = (x if precision == "fp32" else x.to(torch.bfloat16)).double().cpu().numpy()
+    for spec, kw in ((U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), scaling="gelfand",
+                                   gelfand_power=power), dict(method="unso")),
+                     (U.MethodSpec(U.MethodKind.MUON_NS, iterations=5, scaling="gelfand", gelfand_power=power),
+                      dict(method="muon", iterations=5))):
+        y = U.orthogonalize(x, spec, precision=precision).y.double().cpu().numpy()
+        ref = O.run(vals, scaling="gelfand", gelfand_power=power, **kw)["y"]
+        assert rel(y, ref) <= TOL[precision], (power, precision, kw, rel(y, ref))
