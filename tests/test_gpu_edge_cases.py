@@ -217,3 +217,30 @@ def test_gelfand_powers(precision, power):
         y = U.orthogonalize(x, spec, precision=precision).y.double().cpu().numpy()
         ref = O.run(vals, scaling="gelfand", gelfand_power=power, **kw)["y"]
         assert rel(y, ref) <= TOL[precision], (power, precision, kw, rel(y, ref))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("order,rule", [(2, "exact"), (6, "approx-sum"), (20, "approx-abs"), (20, "exact")])
+def test_other_polynomial_orders_and_rules(precision, order, rule):
+    """CoefficientSets of other orders N and b-rules (scalarpoly.py:39-61, 117-127) on the small
+    (h <= 128), persistent (h <= 2048) and multi-launch routes, against the oracle."""
+    rng = np.random.default_rng(order)
+    a = rng.uniform(-1.0, 2.0, order - 1)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.CoefficientSet(order, a, rule))
+    for shape in ((600, 96), (1200, 384)):
+        x = gaussian(shape, 130 + order + shape[1])
+        vals = (x if precision == "fp32" else x.to(torch.bfloat16)).double().cpu().numpy()
+        y = U.orthogonalize(x, spec, precision=precision).y.double().cpu().numpy()
+        ref = O.run(vals, "unso", order=order, a=a, rule=rule)["y"]
+        assert rel(y, ref) <= TOL[precision], (order, rule, shape, precision, rel(y, ref))
+
+
+def test_other_order_on_the_multi_launch_route():
+    """h = 2304 (> the persistent chain's co-residency): the CTA-pair squaring launches with N = 8."""
+    rng = np.random.default_rng(8)
+    a = rng.uniform(-1.0, 2.0, 7)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.CoefficientSet(8, a, "exact"))
+    x = gaussian((4608, 2304), 140)
+    y = U.orthogonalize(x, spec, precision="bf16").y.double().cpu().numpy()
+    ref = O.run(x.to(torch.bfloat16).double().cpu().numpy(), "unso", order=8, a=a, rule="exact")["y"]
+    assert rel(y, ref) <= TOL["bf16"], rel(y, ref)
