@@ -244,3 +244,16 @@ def test_other_order_on_the_multi_launch_route():
     y = U.orthogonalize(x, spec, precision="bf16").y.double().cpu().numpy()
     ref = O.run(x.to(torch.bfloat16).double().cpu().numpy(), "unso", order=8, a=a, rule="exact")["y"]
     assert rel(y, ref) <= TOL["bf16"], rel(y, ref)
+
+
+def test_extreme_scales():
+    """fp32 mode (fp64 accumulation) handles the input's full range like the reference; bf16 mode
+    accumulates the Gram in fp32, so inputs whose Gram leaves the fp32 range are reported loudly as
+    degenerate instead of returning garbage."""
+    x = gaussian((400, 100), 150, torch.float32)
+    base = U.orthogonalize(x, UNSO, precision="fp32").y
+    for c in (1e-25, 1e18):
+        y = U.orthogonalize(x * c, UNSO, precision="fp32").y
+        assert rel(y.double().cpu().numpy(), base.double().cpu().numpy()) <= 1e-6, c
+        with pytest.raises(U.DegenerateInputError):
+            U.orthogonalize(x * c, UNSO, precision="bf16")
