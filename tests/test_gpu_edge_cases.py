@@ -257,3 +257,15 @@ def test_extreme_scales():
         assert rel(y.double().cpu().numpy(), base.double().cpu().numpy()) <= 1e-6, c
         with pytest.raises(U.DegenerateInputError):
             U.orthogonalize(x * c, UNSO, precision="bf16")
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("bad", [float("nan"), float("inf")])
+def test_non_finite_input_is_degenerate(precision, bad):
+    """A NaN / Inf entry makes the scaling denominator non-finite: DegenerateInputError, as the
+    reference's preprocess raises (ortho.py:164-165), for UNSO and the NS kinds."""
+    x = gaussian((300, 80), 160)
+    x[5, 7] = bad
+    for spec in (UNSO, MUON):
+        with pytest.raises(U.DegenerateInputError):
+            U.orthogonalize(x, spec, precision=precision)
