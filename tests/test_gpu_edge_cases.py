@@ -269,3 +269,12 @@ def test_non_finite_input_is_degenerate(precision, bad):
     for spec in (UNSO, MUON):
         with pytest.raises(U.DegenerateInputError):
             U.orthogonalize(x, spec, precision=precision)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_wide_large_h(precision):
+    """Wide input (rows < cols) with h = 2304 > the persistent chain's co-residency: the multi-launch
+    chain and the MN-major apply, UNSO and Muon-5 (hi/lo state on the wide path)."""
+    x = gaussian((2304, 4608), 170)
+    check(x, UNSO, "unso", precision)
+    check(x, MUON, "muon", precision)
