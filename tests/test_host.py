@@ -108,6 +108,17 @@ def test_method_spec_validation():
         U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), precision="fp8")
     with pytest.raises(ValueError):
         U.CoefficientSet(3, np.array([1.0, np.inf]))
+    # recipe knobs of this implementation (not in the reference): validated the same way
+    with pytest.raises(ValueError):
+        U.MethodSpec(U.MethodKind.MUON_NS, iterations=5, ns_products="fp8")
+    with pytest.raises(ValueError):
+        U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), chain="fp8")
+    from paper_2602_02500_b200 import _native as N
+    from paper_2602_02500_b200.ortho import Precision, _build_method_desc
+    md, _ = _build_method_desc(U.MethodSpec(U.MethodKind.MUON_NS, iterations=5, ns_products="bf16"), Precision.BF16, 1)
+    assert md.flags & N.FLAG_NS_SINGLE_STATE
+    md, _ = _build_method_desc(U.MethodSpec(U.MethodKind.MUON_NS, iterations=5), Precision.BF16, 1)
+    assert not md.flags & N.FLAG_NS_SINGLE_STATE
 
 
 def test_expand_cesista_rows():
