@@ -1,3 +1,5 @@
+// Reference: the squaring loop of unso() (ortho.py:197-204) in fp64 via the C-form restatement,
+// with preprocess's Frobenius-gram scale (ortho.py:153-157) folded into phase A.
 // Persistent fp64 squaring chain for the FP32 (fp64-grade) mode, h <= 256: every squaring of
 // every matrix of a co-resident batch chunk in ONE cooperative launch (replacing N-1 launches of
 // the DMMA engine, each of which is latency-bound at these sizes).

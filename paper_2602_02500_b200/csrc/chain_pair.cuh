@@ -1,3 +1,5 @@
+// Reference: one iteration of unso()'s loop (ortho.py:201-203: P += a_k B_k; B <- B B) in the
+// C-form C = I - B (identical in exact arithmetic), for every matrix of the batch.
 // One C-form squaring step for large h (tiles > co-resident CTAs), on CTA pairs:
 //   C_{k+1} = 2 C_k - C_k^2 (upper 256 x 256 pair tiles only), P -= c_{k+1} C_{k+1}
 // with the bf16x3 split product hi*hi + hi*lo + lo*hi accumulated in TMEM.

@@ -1,3 +1,5 @@
+// Reference: preprocess's gram scale (ortho.py:153-157) + unso() (ortho.py:197-204) for h <= 128,
+// with the Gram of the tall input (ortho.py:156/198) optionally fused.
 // Single-CTA "scale + squaring chain" for h <= 128 (BF16 precision): one CTA per matrix, the
 // whole C_k resident on chip for all N-1 squarings.
 //

@@ -1,3 +1,4 @@
+// Reference: ortho.py:153-157 (scale), 197-204 (squarings, P) for large h.
 // Glue-free multi-launch pipeline for large h (tiles > co-resident CTAs):
 //   K1 gram epilogue -> G as bf16 hi/lo (upper pair tiles) + per-warp norm partials
 //   scalars          -> s^2, 1/s, status               (fixed-order reduction, deterministic)

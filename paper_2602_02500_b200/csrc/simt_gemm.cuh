@@ -1,3 +1,4 @@
+// Reference: densemat.matmul (densemat.py:74-82, numpy/OpenBLAS dgemm) at fp64 accumulation.
 // fp64-accumulating GEMM/SYRK engine on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64):
 // the "fp32 mode" of the orthogonalizer (parity <= 1e-5 needs fp64-grade Gram and squaring
 // chain on ill-conditioned inputs), the Gelfand scaling products and the

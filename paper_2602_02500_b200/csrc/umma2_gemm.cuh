@@ -1,3 +1,5 @@
+// Reference contractions: the Gram densemat.matmul(a, transpose(a)) (ortho.py:156, 198) as a SYRK,
+// the apply P.X (ortho.py:205) in the tall form Y = X P, and the NS products (ortho.py:215-230).
 // CTA-pair (cta_group::2) tcgen05 engine: a cluster of 2 CTAs on one TPC computes a
 // 256 x BN tile with M=256 MMAs issued by the leader CTA.  Each CTA stages its own
 // 128 A-rows and BN/2 B-rows per k-block (TMA .cta_group::2, completion on the

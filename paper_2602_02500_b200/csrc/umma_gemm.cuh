@@ -1,3 +1,4 @@
+// Reference contractions: as umma2_gemm.cuh (ortho.py:156, 198, 205, 215-230), 1-CTA tiles.
 // tcgen05 / TMEM / TMA GEMM-SYRK engine for sm_100a (bf16 operands, f32 accumulate).
 //
 //   D[b](m, n) = sum_t sum_k A_{a(t)}[b](m, k) * B_{b(t)}[b](n, k)
