@@ -4,8 +4,8 @@
 Workload (BASELINE.json configs[3], the config its 1/2/4/8-GPU metric and the
 north_star's scaling target are quoted on): one tall bf16 matrix 262144 x 2048,
 i.i.d. N(0,1) (seeded synthetic), orthogonalized with the shipped order-14 UNSO
-polynomial in bf16 mode (tcgen05 bf16 tensor cores; bf16x3 C-form chain; bf16x2
-apply).  With --gpus N > 1 (torchrun) the rows are sharded along the long side:
+polynomial in bf16 mode (tcgen05 bf16 tensor cores; SYRK Gram; bf16x3 C-form chain
+with data-dependent truncation; adaptive single-term / bf16x2 apply of the shifted P).  With --gpus N > 1 (torchrun) the rows are sharded along the long side:
 local Gram -> one NCCL all-reduce of the 2048 x 2048 Gram -> redundant P(A) ->
 local apply (strong scaling: total work fixed).
 
