@@ -278,3 +278,26 @@ def test_wide_large_h(precision):
     x = gaussian((2304, 4608), 170)
     check(x, UNSO, "unso", precision)
     check(x, MUON, "muon", precision)
+
+
+def test_side_streams_run_concurrently_and_match():
+    """Calls on two side streams at once (per-stream workspaces, stream-ordered ABI) equal the
+    default-stream results bit for bit."""
+    xa = gaussian((4, 1024, 256), 180, torch.bfloat16)
+    xb = gaussian((2048, 512), 181)
+    ref_a = U.orthogonalize(xa, UNSO).y
+    ref_b = U.orthogonalize(xb, MUON, precision="bf16").y
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            ya = U.orthogonalize(xa, UNSO, check=False).y
+        with torch.cuda.stream(s2):
+            yb = U.orthogonalize(xb, MUON, precision="bf16", check=False).y
+        outs.append((ya, yb))
+    torch.cuda.synchronize()
+    for ya, yb in outs:
+        assert torch.equal(ya, ref_a)
+        assert torch.equal(yb, ref_b)
