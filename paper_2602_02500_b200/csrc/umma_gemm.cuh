@@ -34,13 +34,30 @@ struct UmmaWork {
   int mode_want = -1;
 };
 
+// Non-SYRK tile order: groups of UMMA_GROUP_M row blocks, row block fastest within a group, so the
+// ~74 tiles in flight touch UMMA_GROUP_M A row blocks and ~74 / UMMA_GROUP_M B column blocks (an
+// L2-sized working set when A and B are both large, e.g. the apply of configs[4]: P is then read
+// from DRAM once per group instead of once per row block).
+constexpr int UMMA_GROUP_M = 8;
+__device__ __forceinline__ void umma_grouped_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
+  const int per_group = UMMA_GROUP_M * tiles_n;
+  const int g = t / per_group;
+  const int r = t - g * per_group;
+  const int rows = min(UMMA_GROUP_M, tiles_m - g * UMMA_GROUP_M);
+  tn = r / rows;
+  tm = g * UMMA_GROUP_M + (r - tn * rows);
+}
+
 __device__ __forceinline__ void umma_decode(const UmmaWork& w, int idx, int& b, int& split, int& tm, int& tn,
                                             int& kt0, int& kt1) {
   const int t = idx % w.tiles_valid;
   const int r = idx / w.tiles_valid;
   split = r % w.splits;
   b = r / w.splits;
-  simt_tile_coords(t, w.tiles_m, w.tiles_n, w.syrk, tm, tn);
+  if (!w.syrk)
+    umma_grouped_coords(t, w.tiles_m, w.tiles_n, tm, tn);
+  else
+    simt_tile_coords(t, w.tiles_m, w.tiles_n, 1, tm, tn);
   kt0 = static_cast<int>(static_cast<int64_t>(split) * w.k_tiles / w.splits);
   kt1 = static_cast<int>(static_cast<int64_t>(split + 1) * w.k_tiles / w.splits);
 }
