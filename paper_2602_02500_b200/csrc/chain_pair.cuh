@@ -90,11 +90,11 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * SC_STAGE_BYTES;
           const uint32_t lbar = lbar0 + stage * 8;
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * SC_STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], work.no_cross ? SC_STAGE_BYTES : 2 * SC_STAGE_BYTES);
           sc_load(&maps.hiK, &maps.hiMN, lbar, st, tm, arow, kt, b);
-          sc_load(&maps.loK, &maps.loMN, lbar, st + SC_TILE, tm, arow, kt, b);
+          if (!work.no_cross) sc_load(&maps.loK, &maps.loMN, lbar, st + SC_TILE, tm, arow, kt, b);
           sc_load(&maps.hiK, &maps.hiMN, lbar, st + 2 * SC_TILE, tn, brow, kt, b);
-          sc_load(&maps.loK, &maps.loMN, lbar, st + 3 * SC_TILE, tn, brow, kt, b);
+          if (!work.no_cross) sc_load(&maps.loK, &maps.loMN, lbar, st + 3 * SC_TILE, tn, brow, kt, b);
           if (++stage == SC_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -128,8 +128,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
             const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * SC_TILE, ks)
                                      : operand_desc<false>(st + 3 * SC_TILE, ks);
             umma_bf16_pair(d_tmem, ah, bh, idesc, (kt > kt0 || ks > 0) ? 1u : 0u);
-            umma_bf16_pair(d_tmem, ah, bl, idesc, 1u);
-            umma_bf16_pair(d_tmem, al, bh, idesc, 1u);
+            if (!work.no_cross) {
+              umma_bf16_pair(d_tmem, ah, bl, idesc, 1u);
+              umma_bf16_pair(d_tmem, al, bh, idesc, 1u);
+            }
           }
           umma_commit_pair(&empty[stage], 0x3);
           if (++stage == SC_STAGES) {
@@ -331,11 +333,13 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * F8_STAGE_BYTES;
           const uint32_t lbar = lbar0 + stage * 8;
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * F8_STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], work.no_cross ? 4 * SC_TILE : 2 * F8_STAGE_BYTES);
           sc_load(&maps.hiK, &maps.hiMN, lbar, st, tm, arow, kt, b);
           sc_load(&maps.hiK, &maps.hiMN, lbar, st + OFF_BH, tn, brow, kt, b);
-          f8_load(maps, lbar, st + OFF_A8, tm, arow, kt, b);
-          f8_load(maps, lbar, st + OFF_B8, tn, brow, kt, b);
+          if (!work.no_cross) {
+            f8_load(maps, lbar, st + OFF_A8, tm, arow, kt, b);
+            f8_load(maps, lbar, st + OFF_B8, tn, brow, kt, b);
+          }
           if (++stage == F8_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -369,6 +373,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
           }
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
+            if (work.no_cross) break;
             umma_f8_pair(d_tmem, f8_desc(st + OFF_A8, a_mn, 0, ks), f8_desc(st + OFF_B8, b_mn, 1, ks), id8, 1u);
             umma_f8_pair(d_tmem, f8_desc(st + OFF_A8, a_mn, 1, ks), f8_desc(st + OFF_B8, b_mn, 0, ks), id8, 1u);
           }

@@ -32,6 +32,9 @@ struct UmmaWork {
   // (mode_flag[b * opt_stride] != 0) == (mode_want == 1) are processed by this launch.
   const double* mode_flag = nullptr;
   int mode_want = -1;
+  // Squaring-chain kernels (chain_pair.cuh): 1 = accumulate the hi*hi product only (no lo / e4m3
+  // cross terms, their operand tiles are not loaded) -- the first squarings of the chain.
+  int no_cross = 0;
 };
 
 // Non-SYRK tile order: groups of UMMA_GROUP_M row blocks, row block fastest within a group, so the

@@ -919,6 +919,10 @@ static int32_t gram_bf16_split(const Problem& p, const Plan& pl, void* ws, const
   return UNSO_OK;
 }
 
+constexpr int CHAIN_HI_ONLY_STEPS = 2;
+// developer override (A/B timing and precision): cross terms in every squaring
+static const bool g_dev_cross_all = std::getenv("UNSO_CHAIN_CROSS_ALL") != nullptr;
+
 // Multi-launch pipeline for large h (multi_chain.cuh): scalars from the norm partials, N-1 CTA-pair
 // squaring steps (the first folds C_1 = G/s^2 and initialises P, the last emits P statistics),
 // the adaptive-apply decision and the shifted symmetric P.  Requires C hi/lo[0] = split(G) and
@@ -937,6 +941,12 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
   for (double v : p.co) alpha += v;
   const UmmaWork wc2 = umma2_make_work(h, h, h, 256, static_cast<int>(p.batch), true, 1);
   const bool f8 = (p.flags & UNSO_FLAG_CHAIN_BF16X3) == 0;
+  // The first CHAIN_HI_ONLY_STEPS squarings of the default (bf16 + e4m3) recipe take the hi*hi
+  // product alone (shipped-order chains only): an error there is damped by the later squarings,
+  // whereas the last squarings (largest coefficients) need the cross terms
+  // (tools/chain_precision_emulation.py: 2.6-2.7e-3 -> 2.7-3.3e-3 on the cfg2/3/5-like spectra;
+  // dropping them in the LAST step instead gives 2-7e-2).
+  const int hi_only_steps = (f8 && N >= 12 && !g_dev_cross_all) ? CHAIN_HI_ONLY_STEPS : 0;
   int cur = 0;
   bool p_pending = false;
   for (int k = 1; k < N; ++k) {
@@ -955,11 +965,13 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
                      k == 1 ? 1 : 0, static_cast<float>(p.co[0]), alpha, at<double>(ws, pl.scal),
                      last ? at<double>(ws, pl.mpstat) : nullptr};
     if (f8 && !last) {  // produce the e4m3 operand copies (and the 2^12-scaled bf16 hi) of C_{k+1}
-      epi.n8hi = at<uint8_t>(ws, pl.C8h[cur ^ 1]);
-      epi.n8lo = at<uint8_t>(ws, pl.C8l[cur ^ 1]);
       epi.out_hi_scale = 4096.f;
-      epi.n8i = at<uint8_t>(ws, pl.C8i[cur ^ 1]);
-      epi.ld8i = 2 * pl.ldc;
+      if (k + 1 > hi_only_steps) {  // step k + 1 reads them
+        epi.n8hi = at<uint8_t>(ws, pl.C8h[cur ^ 1]);
+        epi.n8lo = at<uint8_t>(ws, pl.C8l[cur ^ 1]);
+        epi.n8i = at<uint8_t>(ws, pl.C8i[cur ^ 1]);
+        epi.ld8i = 2 * pl.ldc;
+      }
     }
     if (f8 && k > 1) epi.in_hi_scale = 1.f / 4096.f;
     // P is updated every other step (a_k C_k + a_{k+1} C_{k+1} in one read-modify-write)
@@ -967,6 +979,8 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
     epi.coefk = p_pending ? static_cast<float>(p.co[k - 1]) : 0.f;
     p_pending = epi.write_p == 0;
     cudaError_t le;
+    UmmaWork wk = wc2;
+    wk.no_cross = k <= hi_only_steps ? 1 : 0;
     if (f8 && k > 1) {  // C_k is scaled (|C| <= 1): hi*hi in bf16 + e4m3 cross terms
       SymMapsF8 m8;
       m8.hiK = maps.hiK;
@@ -978,9 +992,9 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
           !make_map_u8(&m8.h8MN, h8, h, h, p.batch, pl.ldc, pl.hh, 128, 64) ||
           !make_map_u8(&m8.l8MN, l8, h, h, p.batch, pl.ldc, pl.hh, 128, 64))
         return UNSO_ERR_CUDA;
-      le = launch_chain_pair_f8(m8, wc2, epi, st);
+      le = launch_chain_pair_f8(m8, wk, epi, st);
     } else {
-      le = launch_chain_pair(maps, wc2, epi, st);
+      le = launch_chain_pair(maps, wk, epi, st);
     }
     if (le != cudaSuccess) return UNSO_ERR_CUDA;
     ++g_launches;

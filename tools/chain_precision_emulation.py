@@ -91,3 +91,39 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "fp8":
                 P = P - co[k] * C
             y = (P / np.sqrt(s2)) @ x
             print(name, f"S=({S_hi},{S_lo})", f"{np.linalg.norm(y - ref) / np.linalg.norm(ref):.2e}", flush=True)
+
+
+def unso_first_steps_hi_only(m, first, bf16x3=False):
+    """The large-h recipe (bf16 hi*hi + e4m3 cross terms; C_k stored as bf16 hi + bf16 lo) with the
+    cross terms dropped in the first `first` squarings (bf16x3=True: the bf16x3 recipe instead)."""
+    x = np.asarray(m, np.float64)
+    if x.shape[0] > x.shape[1]: x = x.T
+    g = x @ x.T; s2 = np.sqrt(np.sum(g * g)); C = (g / s2).astype(np.float32).astype(np.float64)
+    a = np.array(O.DEFAULT_A); c = O.final_coefficient(14, a, "exact"); co = list(a) + [c]
+    P = (1 + sum(co)) * np.eye(C.shape[0]) - co[0] * C
+    for k in range(1, 14):
+        h = bf16(C)
+        if bf16x3:
+            l = bf16(C - h)
+            sq = h @ h if k <= first else h @ h + h @ l + l @ h
+            n = 2 * C - sq
+        else:
+            l = C - h
+            if k <= first:
+                sq = h @ h
+            else:
+                h8 = e4m3_real(h * 256.0) / 256.0; l8 = e4m3_real(l * 65536.0) / 65536.0
+                sq = h @ h + h8 @ l8 + l8 @ h8
+            n = 2 * (h + bf16(l)) - sq
+        C = n.astype(np.float32).astype(np.float64)
+        P = P - co[k] * C
+    return (P / np.sqrt(s2)) @ x
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "--first-steps":
+    # cross terms dropped in the first j squarings (what the large-h chain ships with j = 2)
+    for name, m in cases.items():
+        ref = O.run(m, "unso")["y"]; ref = ref if ref.shape[0] <= ref.shape[1] else ref.T
+        r = {f"first{j}": np.linalg.norm(unso_first_steps_hi_only(m, j) - ref) / np.linalg.norm(ref)
+             for j in (0, 1, 2, 3, 4)}
+        print(name, " ".join(f"{k}={v:.2e}" for k, v in r.items()), flush=True)
