@@ -919,9 +919,10 @@ static int32_t gram_bf16_split(const Problem& p, const Plan& pl, void* ws, const
   return UNSO_OK;
 }
 
-constexpr int CHAIN_HI_ONLY_STEPS = 2;
-// developer override (A/B timing and precision): cross terms in every squaring
+constexpr int CHAIN_HI_ONLY_STEPS = 3;
+// developer overrides (A/B timing and precision): cross terms in every squaring; another count
 static const bool g_dev_cross_all = std::getenv("UNSO_CHAIN_CROSS_ALL") != nullptr;
+static const int g_dev_hi_only = std::getenv("UNSO_CHAIN_HI_ONLY_STEPS") ? std::atoi(std::getenv("UNSO_CHAIN_HI_ONLY_STEPS")) : -1;
 
 // Multi-launch pipeline for large h (multi_chain.cuh): scalars from the norm partials, N-1 CTA-pair
 // squaring steps (the first folds C_1 = G/s^2 and initialises P, the last emits P statistics),
@@ -946,7 +947,8 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
   // whereas the last squarings (largest coefficients) need the cross terms
   // (tools/chain_precision_emulation.py: 2.6-2.7e-3 -> 2.7-3.3e-3 on the cfg2/3/5-like spectra;
   // dropping them in the LAST step instead gives 2-7e-2).
-  const int hi_only_steps = (f8 && N >= 12 && !g_dev_cross_all) ? CHAIN_HI_ONLY_STEPS : 0;
+  const int hi_only_steps =
+      (f8 && N >= 12 && !g_dev_cross_all) ? (g_dev_hi_only >= 0 ? g_dev_hi_only : CHAIN_HI_ONLY_STEPS) : 0;
   int cur = 0;
   bool p_pending = false;
   for (int k = 1; k < N; ++k) {
