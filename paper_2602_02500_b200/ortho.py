@@ -75,7 +75,7 @@ class MethodSpec:
     gelfand_power: int = 2
     precision: Precision | None = None
     apply_terms: int | None = None   # bf16 mode: None = adaptive per matrix, 1 = P_hi only, 2 = P_hi + P_lo
-    chain: str | None = None         # bf16 mode, large h: None = bf16 hi*hi + e4m3 cross terms, "bf16x3"
+    chain: str | None = None         # bf16 mode, large h: None = bf16 hi*hi (first 3 squarings alone) + e4m3 cross terms, "bf16x3"
     truncate: bool = True            # bf16 mode, persistent chain: stop once ||I - C_k||_F bounds the rest
     ns_products: str | None = None   # bf16 mode, NS kinds: None / "bf16x3" = hi/lo state in the long-side
                                      # products (~1e-4 from fp64), "bf16" = one bf16 term (faster, ~1e-2)

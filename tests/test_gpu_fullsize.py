@@ -135,3 +135,19 @@ def test_other_methods_and_scalings_full_size(method):
     xf = ((q1 * torch.sign(torch.diagonal(r1))) * s[None, :] @ (q2 * torch.sign(torch.diagonal(r2))).T).float()
     res = U.orthogonalize(xf, spec, precision="fp32")
     check_map(xf, res.y, spec, "fp32", spectrum=spectrum_svd, label=f"cfg2-shape {method}")
+
+
+@pytest.mark.parametrize("chain", [None, "bf16x3"])
+def test_large_h_chain_recipe_against_fp32_mode(chain):
+    """The large-h chain recipes (multi-launch CTA-pair route, h = 4096) at full size: the default
+    (hi*hi alone in the first three squarings, e4m3 cross terms after) and bf16x3 in every step,
+    against the fp32 mode (fp64-grade Gram and chain) on the same bf16 input.  Measured 2.8e-3 and
+    1.7e-3; the bars leave room above those, far inside 2e-2."""
+    x = gaussian(4096, 4096, 0.02, 11, torch.bfloat16)
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), chain=chain)
+    yb = U.orthogonalize(x, spec, precision="bf16").y.double()
+    yf = U.orthogonalize(x.float(), U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients()),
+                         precision="fp32").y.double()
+    err = float(torch.linalg.norm(yb - yf) / torch.linalg.norm(yf))
+    print(f"chain={chain}: {err:.2e}")
+    assert err <= (5e-3 if chain is None else 2.5e-3), err
