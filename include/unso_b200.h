@@ -179,6 +179,19 @@ int32_t unso_ortho_error(const unso_matrix_desc* y, const void* y_ptr, double* d
 int32_t unso_query_scalars(const unso_matrix_desc* x, const unso_method_desc* method, const void* workspace,
                            double* d_out, void* stream);
 
+/* Elementwise passes of a Muon optimizer step around the orthogonalizer (no
+ * reference interface: the reference lists the optimizer as out of scope).  One shape
+ * group of n matrices, `numel` elements each, all of `dtype` (F32 or BF16); d_grads / d_bufs /
+ * d_params are DEVICE arrays of n pointers, every pointer 16-byte aligned, numel a multiple of 8.
+ *   prepare: M_i <- mu M_i + G_i; U_i = G_i + mu M_i (nesterov) or M_i written to stacked + i*numel;
+ *            d_maxabs[i] = max |U_i| (n floats, zeroed by the call).
+ *   update:  P_i <- decay P_i + alpha O_i, O = ortho + i*numel, skipped (P_i <- decay P_i) when
+ *            d_maxabs[i] == 0 (a zero update is a zero step). */
+int32_t unso_muon_prepare(int32_t n, const void* d_grads, const void* d_bufs, void* stacked, int64_t numel,
+                          int32_t dtype, float mu, int32_t nesterov, float* d_maxabs, void* stream);
+int32_t unso_muon_update(int32_t n, const void* d_params, const void* ortho, int64_t numel, int32_t dtype,
+                         const float* d_maxabs, float decay, float alpha, void* stream);
+
 /* Number of CUDA kernels launched by the last successful call on this thread. */
 int32_t unso_last_launch_count(void);
 

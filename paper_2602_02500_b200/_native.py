@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "unso_gram_dtype", "unso_orthogonalize_from_gram", "unso_scale_denominator", "unso_ortho_error",
     "unso_last_launch_count", "unso_profile_begin", "unso_profile_read", "unso_profile_end",
     "unso_query_scalars", "unso_gram_peer_bytes", "unso_gram_push", "unso_gram_reduce", "unso_gram_wait",
+    "unso_muon_prepare", "unso_muon_update",
 )
 SCALARS = 16
 SCALAR_NAMES = ("trace", "fro2", "dev2", "s2", "inv_s", "ortho_error", "shift", "apply_single", "apply_bound",
@@ -111,6 +112,12 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.unso_gram_reduce.restype = ctypes.c_int32
     lib.unso_gram_reduce.argtypes = [ctypes.c_int64, GP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                      ctypes.c_uint32, P, ctypes.c_size_t, P]
+    lib.unso_muon_prepare.restype = ctypes.c_int32
+    lib.unso_muon_prepare.argtypes = [ctypes.c_int32, P, P, P, ctypes.c_int64, ctypes.c_int32, ctypes.c_float,
+                                      ctypes.c_int32, P, P]
+    lib.unso_muon_update.restype = ctypes.c_int32
+    lib.unso_muon_update.argtypes = [ctypes.c_int32, P, P, ctypes.c_int64, ctypes.c_int32, P, ctypes.c_float,
+                                     ctypes.c_float, P]
     lib.unso_gram_wait.restype = ctypes.c_int32
     lib.unso_gram_wait.argtypes = [ctypes.c_int64, GP, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P]
 

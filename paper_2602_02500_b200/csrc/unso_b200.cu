@@ -33,6 +33,7 @@
 #include "chain_pair.cuh"
 #include "ns_bf16.cuh"
 #include "multi_chain.cuh"
+#include "muon_update.cuh"
 #include <cstdlib>
 
 #define UNSO_VERSION_STRING "unso_b200 0.1.0 (sm_100a: tcgen05/TMEM/TMA bf16 path + fp64 DFMA parity path)"
@@ -1946,6 +1947,55 @@ int32_t unso_ortho_error(const unso_matrix_desc* y, const void* y_ptr, double* d
   UNSO_CHECK_LAUNCH();
   copy_err_kernel<<<static_cast<unsigned>((p.batch + 127) / 128), 128, 0, st>>>(at<double>(workspace, pl.scal),
                                                                                 static_cast<int>(p.batch), d_err);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+// ---------------------------------------------------------------- Muon optimizer passes
+static int64_t muon_per_block(int64_t numel) {
+  const int64_t per = 16384;
+  return numel < per ? ((numel + 7) / 8) * 8 : per;
+}
+
+int32_t unso_muon_prepare(int32_t n, const void* d_grads, const void* d_bufs, void* stacked, int64_t numel,
+                          int32_t dtype, float mu, int32_t nesterov, float* d_maxabs, void* stream) {
+  if (n < 0 || numel < 0 || (n > 0 && (!d_grads || !d_bufs || !stacked || !d_maxabs))) return UNSO_ERR_VALUE;
+  if (dtype != UNSO_DTYPE_F32 && dtype != UNSO_DTYPE_BF16) return UNSO_ERR_UNSUPPORTED;
+  g_launches = 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n == 0) return UNSO_OK;
+  if (cudaMemsetAsync(d_maxabs, 0, sizeof(float) * n, st) != cudaSuccess) return UNSO_ERR_CUDA;
+  if (numel == 0) return UNSO_OK;
+  const int64_t per = muon_per_block(numel);
+  dim3 grid(static_cast<unsigned>((numel + per - 1) / per), static_cast<unsigned>(n));
+  const uint64_t* g = static_cast<const uint64_t*>(d_grads);
+  const uint64_t* m = static_cast<const uint64_t*>(d_bufs);
+  if (dtype == UNSO_DTYPE_BF16)
+    muon_prepare_kernel<__nv_bfloat16><<<grid, MUON_THREADS, 0, st>>>(g, m, static_cast<__nv_bfloat16*>(stacked),
+                                                                     numel, per, mu, nesterov, d_maxabs);
+  else
+    muon_prepare_kernel<float><<<grid, MUON_THREADS, 0, st>>>(g, m, static_cast<float*>(stacked), numel, per, mu,
+                                                             nesterov, d_maxabs);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+int32_t unso_muon_update(int32_t n, const void* d_params, const void* ortho, int64_t numel, int32_t dtype,
+                         const float* d_maxabs, float decay, float alpha, void* stream) {
+  if (n < 0 || numel < 0 || (n > 0 && (!d_params || !ortho || !d_maxabs))) return UNSO_ERR_VALUE;
+  if (dtype != UNSO_DTYPE_F32 && dtype != UNSO_DTYPE_BF16) return UNSO_ERR_UNSUPPORTED;
+  g_launches = 0;
+  if (n == 0 || numel == 0) return UNSO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t per = muon_per_block(numel);
+  dim3 grid(static_cast<unsigned>((numel + per - 1) / per), static_cast<unsigned>(n));
+  const uint64_t* pp = static_cast<const uint64_t*>(d_params);
+  if (dtype == UNSO_DTYPE_BF16)
+    muon_update_kernel<__nv_bfloat16><<<grid, MUON_THREADS, 0, st>>>(
+        pp, static_cast<const __nv_bfloat16*>(ortho), numel, per, d_maxabs, decay, alpha);
+  else
+    muon_update_kernel<float><<<grid, MUON_THREADS, 0, st>>>(pp, static_cast<const float*>(ortho), numel, per,
+                                                            d_maxabs, decay, alpha);
   UNSO_CHECK_LAUNCH();
   return UNSO_OK;
 }

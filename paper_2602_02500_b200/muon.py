@@ -110,19 +110,24 @@ class Muon(torch.optim.Optimizer):
                 buf = state.get("momentum_buffer")
                 if buf is None:
                     buf = state["momentum_buffer"] = torch.zeros_like(g)
-                torch.add(g, buf, alpha=mu, out=buf)  # M <- mu M + G, one pass
-                if p.dim() == 2:
+                if p.dim() == 2:  # momentum in the group pass (fused on CUDA)
                     buckets[(tuple(p.shape), g.dtype, g.device)].append(p)
                 else:
+                    torch.add(g, buf, alpha=mu, out=buf)  # M <- mu M + G
                     if wd:
                         p.mul_(1.0 - lr * wd)
                     p.add_(g.add(buf, alpha=mu) if nesterov else buf, alpha=-lr)
             for (shape, dtype, device), items in buckets.items():
                 rows, cols = shape
+                scale = math.sqrt(max(1.0, rows / cols))
+                if _fused_ok(items, self.state):
+                    self._fused_group(items, rows, cols, mu, nesterov, 1.0 - lr * wd, -lr * scale)
+                    continue
                 # the update of every matrix of the group is written straight into the stacked batch
                 stacked = torch.empty((len(items), rows, cols), dtype=dtype, device=device)
                 for i, p in enumerate(items):
                     buf = self.state[p]["momentum_buffer"]
+                    torch.add(p.grad, buf, alpha=mu, out=buf)  # M <- mu M + G
                     if nesterov:
                         torch.add(p.grad, buf, alpha=mu, out=stacked[i])
                     else:
@@ -131,11 +136,45 @@ class Muon(torch.optim.Optimizer):
                 ortho = self._orthogonalize_group(stacked)
                 if bool(zero.any()):  # zero update -> zero step (not a degenerate input)
                     ortho = torch.where(zero[:, None, None], torch.zeros_like(ortho), ortho)
-                scale = math.sqrt(max(1.0, rows / cols))
                 if wd:
                     torch._foreach_mul_(items, 1.0 - lr * wd)
                 torch._foreach_add_(items, [o.to(items[0].dtype) for o in ortho.unbind(0)], alpha=-lr * scale)
         return loss
+
+    def _fused_group(self, items, rows, cols, mu, nesterov, decay, alpha):
+        """CUDA bf16/fp32 groups: momentum, Nesterov stacking and the zero check in one multi-tensor
+        kernel, the decayed update in another (csrc/muon_update.cuh), no host synchronisation."""
+        from . import _native as N
+        p0 = items[0]
+        dev, n, numel = p0.device, len(items), rows * cols
+        dt = N.DTYPE_BF16 if p0.dtype == torch.bfloat16 else N.DTYPE_F32
+        ptrs = torch.tensor([[p.grad.data_ptr() for p in items], [self.state[p]["momentum_buffer"].data_ptr()
+                             for p in items], [p.data_ptr() for p in items]], dtype=torch.int64).to(dev, non_blocking=True)
+        stacked = torch.empty((n, rows, cols), dtype=p0.dtype, device=dev)
+        maxabs = torch.empty(n, dtype=torch.float32, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        lib = N.lib()
+        N.check(lib.unso_muon_prepare(n, ptrs[0].data_ptr(), ptrs[1].data_ptr(), stacked.data_ptr(), numel, dt,
+                                      float(mu), 1 if nesterov else 0, maxabs.data_ptr(), stream), "unso_muon_prepare")
+        ortho = self._orthogonalize_group(stacked).contiguous()
+        N.check(lib.unso_muon_update(n, ptrs[2].data_ptr(), ortho.data_ptr(), numel, dt, maxabs.data_ptr(),
+                                     float(decay), float(alpha), stream), "unso_muon_update")
+
+
+#: use the fused CUDA passes where _fused_ok allows (tests switch it off to compare with the torch ops)
+FUSED_PASSES = True
+
+
+def _fused_ok(items, state) -> bool:
+    """Every tensor of the group on one CUDA device, contiguous, bf16 or fp32, 16-byte aligned."""
+    p0 = items[0]
+    if not FUSED_PASSES or not p0.is_cuda or p0.dtype not in (torch.bfloat16, torch.float32) or p0.numel() % 8:
+        return False
+    for p in items:
+        for t in (p, p.grad, state[p]["momentum_buffer"]):
+            if t.dtype != p0.dtype or t.device != p0.device or not t.is_contiguous() or t.data_ptr() % 16:
+                return False
+    return True
 
 
 __all__ = ["Muon", "default_spec"]
