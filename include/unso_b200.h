@@ -182,7 +182,7 @@ int32_t unso_query_scalars(const unso_matrix_desc* x, const unso_method_desc* me
 /* Elementwise passes of a Muon optimizer step around the orthogonalizer (no
  * reference interface: the reference lists the optimizer as out of scope).  One shape
  * group of n matrices, `numel` elements each, all of `dtype` (F32 or BF16); d_grads / d_bufs /
- * d_params are DEVICE arrays of n pointers, every pointer 16-byte aligned, numel a multiple of 8.
+ * d_params are DEVICE arrays of n <= 65535 pointers, every pointer 16-byte aligned, numel a multiple of 8.
  *   prepare: M_i <- mu M_i + G_i; U_i = G_i + mu M_i (nesterov) or M_i written to stacked + i*numel;
  *            d_maxabs[i] = max |U_i| (n floats, zeroed by the call).
  *   update:  P_i <- decay P_i + alpha O_i, O = ortho + i*numel, skipped (P_i <- decay P_i) when

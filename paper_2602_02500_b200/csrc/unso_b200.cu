@@ -1959,7 +1959,8 @@ static int64_t muon_per_block(int64_t numel) {
 
 int32_t unso_muon_prepare(int32_t n, const void* d_grads, const void* d_bufs, void* stacked, int64_t numel,
                           int32_t dtype, float mu, int32_t nesterov, float* d_maxabs, void* stream) {
-  if (n < 0 || numel < 0 || (n > 0 && (!d_grads || !d_bufs || !stacked || !d_maxabs))) return UNSO_ERR_VALUE;
+  if (n < 0 || n > 65535 || numel < 0 || (n > 0 && (!d_grads || !d_bufs || !stacked || !d_maxabs)))
+    return UNSO_ERR_VALUE;
   if (dtype != UNSO_DTYPE_F32 && dtype != UNSO_DTYPE_BF16) return UNSO_ERR_UNSUPPORTED;
   g_launches = 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1982,7 +1983,7 @@ int32_t unso_muon_prepare(int32_t n, const void* d_grads, const void* d_bufs, vo
 
 int32_t unso_muon_update(int32_t n, const void* d_params, const void* ortho, int64_t numel, int32_t dtype,
                          const float* d_maxabs, float decay, float alpha, void* stream) {
-  if (n < 0 || numel < 0 || (n > 0 && (!d_params || !ortho || !d_maxabs))) return UNSO_ERR_VALUE;
+  if (n < 0 || n > 65535 || numel < 0 || (n > 0 && (!d_params || !ortho || !d_maxabs))) return UNSO_ERR_VALUE;
   if (dtype != UNSO_DTYPE_F32 && dtype != UNSO_DTYPE_BF16) return UNSO_ERR_UNSUPPORTED;
   g_launches = 0;
   if (n == 0 || numel == 0) return UNSO_OK;

@@ -168,7 +168,8 @@ FUSED_PASSES = True
 def _fused_ok(items, state) -> bool:
     """Every tensor of the group on one CUDA device, contiguous, bf16 or fp32, 16-byte aligned."""
     p0 = items[0]
-    if not FUSED_PASSES or not p0.is_cuda or p0.dtype not in (torch.bfloat16, torch.float32) or p0.numel() % 8:
+    if (not FUSED_PASSES or not p0.is_cuda or p0.dtype not in (torch.bfloat16, torch.float32) or p0.numel() % 8
+            or len(items) > 65535):
         return False
     for p in items:
         for t in (p, p.grad, state[p]["momentum_buffer"]):
