@@ -148,8 +148,14 @@ class Muon(torch.optim.Optimizer):
         p0 = items[0]
         dev, n, numel = p0.device, len(items), rows * cols
         dt = N.DTYPE_BF16 if p0.dtype == torch.bfloat16 else N.DTYPE_F32
-        ptrs = torch.tensor([[p.grad.data_ptr() for p in items], [self.state[p]["momentum_buffer"].data_ptr()
-                             for p in items], [p.data_ptr() for p in items]], dtype=torch.int64).to(dev, non_blocking=True)
+        key = tuple((p.grad.data_ptr(), self.state[p]["momentum_buffer"].data_ptr(), p.data_ptr()) for p in items)
+        cache = self.__dict__.setdefault("_ptr_lists", {})
+        ptrs = cache.get(key)
+        if ptrs is None:  # device pointer lists, rebuilt only when a tensor moved (e.g. grads set to None)
+            ptrs = torch.tensor(list(zip(*key)), dtype=torch.int64).to(dev)
+            if len(cache) > 64:
+                cache.clear()
+            cache[key] = ptrs
         stacked = torch.empty((n, rows, cols), dtype=p0.dtype, device=dev)
         maxabs = torch.empty(n, dtype=torch.float32, device=dev)
         stream = torch.cuda.current_stream(dev).cuda_stream
