@@ -38,3 +38,16 @@ for c in range(3):
               f"C_1/P init {(a[3]-a[2])/1e3:.2f} (of which the norm sum {(a[4]-a[2])/1e3:.2f}); step 1 data after C_1 {(t[c,1,1]-a[3])/1e3:.2f}; "
               f"final: stats {(f[1]-f[0])/1e3:.2f}, barrier {(f[2]-f[1])/1e3:.2f}, P split+mirror {(f[3]-f[2])/1e3:.2f}; "
               f"kernel span {(f[3]-a[0])/1e3:.2f} us")
+
+# per-k-block arrival timeline of CTA 0, squaring 5 (full-stage seen by the MMA issuer, stage freed for
+# the producer), relative to the first arrival
+kb = (ctypes.c_ulonglong * 128)()
+if hasattr(N.lib(), "unso_debug_chain_kb") and N.lib().unso_debug_chain_kb(kb) == 0:
+    a = np.frombuffer(kb, dtype=np.uint64).reshape(2, 64).astype(np.float64)
+    full, free = a[0], a[1]
+    n = int((full > 0).sum())
+    t0 = full[0]
+    print("squaring 5, CTA 0: k-block  full_at(us)  gap(us)  producer_free_at(us)")
+    for kt in range(n):
+        gap = (full[kt] - full[kt - 1]) / 1e3 if kt else 0.0
+        print(f"   {kt:3d}  {(full[kt]-t0)/1e3:8.2f}  {gap:6.2f}  {(free[kt]-t0)/1e3 if free[kt] else float('nan'):8.2f}")
