@@ -40,7 +40,17 @@ __device__ __forceinline__ void chain_trace(int k, int ev) {
   g_chain_trace[c][k][ev] = t;
 }
 #define CHAIN_TRACE(k, ev) chain_trace(k, ev)
+// per-k-block timestamps of CTA 0, squaring 5: [0] MMA issuer saw the stage full, [1] producer found it empty
+__device__ unsigned long long g_chain_kb[2][64];
+__device__ __forceinline__ void chain_kb(int k, int which, int kt) {
+  if (blockIdx.x != 0 || k != 5 || kt >= 64) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_chain_kb[which][kt] = t;
+}
+#define CHAIN_KB(k, which, kt) chain_kb(k, which, kt)
 #else
+#define CHAIN_KB(k, which, kt)
 #define CHAIN_TRACE(k, ev)
 #endif
 
@@ -191,6 +201,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         const int buf = (k - 1) & 1;
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&empty[stage], phase ^ 1);
+          CHAIN_KB(k, 1, kt);
           uint8_t* st = smem + stage * CH_STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], CH_STAGE_BYTES);
           ch_load_block(maps, buf, 0, &full[stage], st, ti, kt, b);
@@ -216,6 +227,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         tc_fence_after();
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&full[stage], phase);
+          CHAIN_KB(k, 0, kt);
           if (kt == 0) CHAIN_TRACE(k, 1);
           tc_fence_after();
           const int kb = kt >> 1;
