@@ -128,3 +128,16 @@ def test_fused_passes_match_torch_ops(dtype):
         assert float(torch.linalg.norm(a - b)) <= tol * float(torch.linalg.norm(b)) + 1e-12
     # the zero-gradient matrix only decayed: p = base * (1 - lr wd)^2
     assert torch.allclose(out[0][1], base[1].double() * (1 - 0.05 * 0.1) ** 2, rtol=1e-2 if dtype == torch.bfloat16 else 1e-6)
+
+
+def test_fused_passes_only_for_cuda_bf16_fp32_groups():
+    """The fused optimizer kernels take CUDA bf16/fp32 groups only; CPU tensors (and other dtypes)
+    run the torch ops, so this CPU step must not touch the native library."""
+    import paper_2602_02500_b200.muon as M
+    p = torch.nn.Parameter(torch.randn(16, 8))
+    p.grad = torch.randn(16, 8)
+    state = {p: {"momentum_buffer": torch.zeros(16, 8)}}
+    assert not M._fused_ok([p], state)
+    q = torch.nn.Parameter(torch.randn(16, 8, dtype=torch.float64))
+    q.grad = torch.randn(16, 8, dtype=torch.float64)
+    assert not M._fused_ok([q], {q: {"momentum_buffer": torch.zeros_like(q)}})
