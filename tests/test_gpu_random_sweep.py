@@ -65,3 +65,4 @@ def test_random_case(case):
         err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         print(f"case {case}: {rows}x{cols} b{batch} {precision} {str(dtype)[6:]} {kind}/{scaling}: {err:.2e}")
         assert err <= BAR[precision], (case, rows, cols, batch, precision, str(dtype), kind, scaling, err)
+
