@@ -198,10 +198,18 @@ struct EpiChainStep {
     const double w = ((row >> 8) == (col0 >> 8)) ? 1.0 : 2.0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float c0v = fmaf(bf16_lo_to_f32(hw[j]), in_hi_scale, bf16_lo_to_f32(lw[j])) * cs;
-      const float c1v = fmaf(bf16_hi_to_f32(hw[j]), in_hi_scale, bf16_hi_to_f32(lw[j])) * cs;
-      const float n0 = 2.0f * c0v - v[2 * j] * as;
-      const float n1 = 2.0f * c1v - v[2 * j + 1] * as;
+      // Padding columns [h, ldc) hold bytes no epilogue owns (stale workspace): force them to zero
+      // so the stored state is exactly zero-padded -- the interleaved e4m3 operand map spans the
+      // padding (no TMA zero fill there) and stale NaN times a zero partner is still NaN.
+      const bool cok0 = col0 + 2 * j < h, cok1 = col0 + 2 * j + 1 < h;
+      const float c0v = cok0 ? fmaf(bf16_lo_to_f32(hw[j]), in_hi_scale, bf16_lo_to_f32(lw[j])) * cs : 0.f;
+      const float c1v = cok1 ? fmaf(bf16_hi_to_f32(hw[j]), in_hi_scale, bf16_hi_to_f32(lw[j])) * cs : 0.f;
+      const float n0 = cok0 ? 2.0f * c0v - v[2 * j] * as : 0.f;
+      const float n1 = cok1 ? 2.0f * c1v - v[2 * j + 1] * as : 0.f;
+      if (!first) {
+        if (!cok0) pv[2 * j] = 0.f;
+        if (!cok1) pv[2 * j + 1] = 0.f;
+      }
       if (first) {
         const int c = col0 + 2 * j;
         pv[2 * j] = static_cast<float>((c == row ? alpha : 0.0) - static_cast<double>(coef1) * c0v);
@@ -311,16 +319,20 @@ struct EpiChainStep {
       const uint2 hw = hwv[it];
       const uint2 lw = lwv[it];
       float pv[4] = {pvv[it].x, pvv[it].y, pvv[it].z, pvv[it].w};
-      const float cv[4] = {fmaf(bf16_lo_to_f32(hw.x), in_hi_scale, bf16_lo_to_f32(lw.x)) * cs,
-                           fmaf(bf16_hi_to_f32(hw.x), in_hi_scale, bf16_hi_to_f32(lw.x)) * cs,
-                           fmaf(bf16_lo_to_f32(hw.y), in_hi_scale, bf16_lo_to_f32(lw.y)) * cs,
-                           fmaf(bf16_hi_to_f32(hw.y), in_hi_scale, bf16_hi_to_f32(lw.y)) * cs};
+      float cv[4] = {fmaf(bf16_lo_to_f32(hw.x), in_hi_scale, bf16_lo_to_f32(lw.x)) * cs,
+                     fmaf(bf16_hi_to_f32(hw.x), in_hi_scale, bf16_hi_to_f32(lw.x)) * cs,
+                     fmaf(bf16_lo_to_f32(hw.y), in_hi_scale, bf16_lo_to_f32(lw.y)) * cs,
+                     fmaf(bf16_hi_to_f32(hw.y), in_hi_scale, bf16_hi_to_f32(lw.y)) * cs};
       const float av[4] = {acc.x, acc.y, acc.z, acc.w};
       float nv[4], hv[4];
       uint32_t nh[2], nl[2], q8h = 0u, q8l = 0u;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        nv[e] = 2.0f * cv[e] - av[e] * as;
+        if (c + e >= h) {  // zero padding columns (see operator())
+          cv[e] = 0.f;
+          pv[e] = 0.f;
+        }
+        nv[e] = c + e < h ? 2.0f * cv[e] - av[e] * as : 0.f;
         if (first) pv[e] = static_cast<float>((c + e == row ? alpha : 0.0) - static_cast<double>(coef1) * cv[e]);
         else pv[e] -= coefk * cv[e];
         pv[e] -= coef * nv[e];
