@@ -1,20 +1,35 @@
 #!/usr/bin/env python
 """UNSO orthogonalization benchmark on B200 (driver contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[3], the config its 1/2/4/8-GPU metric and the
-north_star's scaling target are quoted on): one tall bf16 matrix 262144 x 2048,
-i.i.d. N(0,1) (seeded synthetic), orthogonalized with the shipped order-14 UNSO
-polynomial in bf16 mode (tcgen05 bf16 tensor cores; SYRK Gram; bf16x3 C-form chain
-with data-dependent truncation; adaptive single-term / bf16x2 apply of the shifted P).  With --gpus N > 1 (torchrun) the rows are sharded along the long side:
-local Gram -> one NCCL all-reduce of the 2048 x 2048 Gram -> redundant P(A) ->
-local apply (strong scaling: total work fixed).
+Workloads (BASELINE.json configs, `--workload`, default cfg4):
 
-A step = one full orthogonalization (preprocess + chain + apply) of the matrix.
-value   = reference-model FLOPs (kernel_model_flops, ortho.py:313-335) per second, whole job.
-e2e     = the same metric through the public API with the input in pinned host memory
-          and the result copied back to pinned host memory inside the timed region.
---impl reference times the CPU oracle (numpy fp64 restatement of the reference) on a
-bounded row sample of the same workload on the host cores.
+  cfg4  configs[3]: one tall bf16 matrix 262144 x 2048, N(0,1).  The config the metric's 1/2/4/8-GPU
+        figure and the north_star's >= 60 % of peak / >= 80 % scaling targets are quoted on.  N > 1:
+        rows sharded along the long side, local Gram -> one all-reduce of the 2048 x 2048 Gram
+        (NCCL, or --collective nvlink: the peer-memory reduction) -> redundant P(A) -> local apply
+        (strong scaling).
+  cfg1  configs[0]: one 512 x 128 fp32 matrix, N(0,1), fp32 mode (fp64-grade, parity <= 1e-5).
+        Does not shard: N > 1 runs N replicas (weak scaling).
+  cfg2  configs[1]: 16 x 2048 x 512 fp32, X = U diag(s) V^T, Haar U/V, s log-uniform [1e-4, 1];
+        fp32 mode by default (--precision bf16 for the tensor-core mode).  N > 1: batch shares.
+  cfg3  configs[2]: one Muon optimizer step (paper_2602_02500_b200.Muon: momentum, Nesterov, grouped
+        orthogonalize, update) over 32 layers x {4 x 4096^2, 2 x 14336 x 4096, 4096 x 14336} bf16
+        parameters, gradients N(0, 0.02^2).  N > 1: Muon(distribute=True) shares every shape group
+        over the ranks and all-gathers the updates (strong scaling).
+  cfg5  configs[4]: 4 x 16384 x 8192 fp32, Haar U/V, s = 1 + Pareto(1.5) min-max rescaled to
+        [1e-6, 1]; bf16 mode by default, --precision fp32 for the fp64-grade mode.  N > 1: batch shares.
+
+A step = one pass of the hot path over the workload's batch (cfg3: one optimizer step).
+value    = reference-model FLOPs (kernel_model_flops, ortho.py:313-335) per second, whole job.
+executed = the FLOPs the device actually issues (SYRK upper tiles, truncated chain, split products;
+           e4m3 products counted at half a bf16 FLOP), and that rate as a fraction of the bf16 peak.
+e2e      = the same metric through the public API from pinned host buffers: every step copies its
+           input host -> device and its result device -> host inside the timed region.
+--impl reference times the CPU oracle (numpy fp64 restatement of the reference, OpenBLAS on all
+host threads) on a bounded sample of the workload; cpu_baseline in the ours arm times the SAME sample.
+
+--gpus N > 1 without torchrun's environment re-launches this script under torch.distributed.run
+with N ranks (one per GPU); under torchrun WORLD_SIZE must equal --gpus.
 """
 
 from __future__ import annotations
@@ -22,6 +37,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,40 +49,90 @@ sys.path.insert(0, REPO)
 
 METRIC = "UNSO orthogonalization TFLOP/s & matrices/s (% bf16 tensor peak), 1/2/4/8 B200"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+CPU_FULL_RECORD = os.path.join(REPO, "profiles", "cpu_full_workload.json")
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default per workload)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--rows", type=int, default=262144)
-    ap.add_argument("--cols", type=int, default=2048)
-    ap.add_argument("--precision", choices=["bf16", "fp32"], default="bf16")
+    ap.add_argument("--workload", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"], default="cfg4")
+    ap.add_argument("--rows", type=int, default=None, help="cfg4: rows of the tall matrix (default 262144)")
+    ap.add_argument("--cols", type=int, default=None, help="cfg4: columns (default 2048)")
+    ap.add_argument("--layers", type=int, default=32, help="cfg3: transformer layers")
+    ap.add_argument("--precision", choices=["bf16", "fp32"], default=None, help="default per workload")
     ap.add_argument("--collective", choices=["nccl", "nvlink"], default="nccl",
-                    help="N > 1: Gram all-reduce through NCCL, or the peer-memory reduction (unso_gram_push/...)")
+                    help="cfg4, N > 1: Gram all-reduce through NCCL, or the peer-memory reduction")
     ap.add_argument("--apply-terms", type=int, choices=[1, 2], default=None,
                     help="bf16 apply split: default adaptive per matrix (device-side bound)")
-    ap.add_argument("--e2e-steps", type=int, default=30,
-                    help="pipelined e2e steps (fill and drain of the three-stream pipeline amortised over them)")
-    ap.add_argument("--cpu-sample-rows", type=int, default=65536,
-                    help="rows of the cpu_baseline sample (~10 s of OpenBLAS fp64 on the GPU box host)")
-    ap.add_argument("--ref-sample-rows", type=int, default=8192)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--cpu-sample-rows", type=int, default=None,
+                    help="cfg4: rows of the CPU sample timed by cpu_baseline AND --impl reference (default 32768)")
+    ap.add_argument("--ref-sample-rows", type=int, default=None, help="alias of --cpu-sample-rows")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="also time the CPU oracle on the FULL workload once and record it in "
+                         "profiles/cpu_full_workload.json (minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-projection", action="store_true", help="cfg4: skip the per-rank shard projection")
     ap.add_argument("--sharded", action="store_true",
-                    help="run the row-sharded multi-rank path (process group, Gram reduction) even at world size 1; "
-                         "used to exercise the N > 1 code under torchrun on a single GPU")
-    return ap.parse_args()
+                    help="cfg4: run the row-sharded multi-rank path (process group, Gram reduction) even at world 1")
+    ap.add_argument("--probe-ranks", action="store_true", help=argparse.SUPPRESS)  # launcher self-test (CPU)
+    args = ap.parse_args(argv)
+    if args.ref_sample_rows and not args.cpu_sample_rows:
+        args.cpu_sample_rows = args.ref_sample_rows
+    return args
 
+
+# ----------------------------------------------------------------------------- launcher
+
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_command(argv, gpus: int, port: int | None = None) -> list[str]:
+    """The torch.distributed.run command that runs this script with `gpus` ranks on one node."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port or _free_port()),
+            os.path.abspath(__file__), *argv]
+
+
+def maybe_relaunch(args, argv) -> bool:
+    """--gpus N > 1 outside torchrun: re-run under torch.distributed.run (N ranks) and return True.
+    Under torchrun, WORLD_SIZE must match --gpus (a mismatch would silently report another N)."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None:
+        if args.gpus > 1:
+            rc = subprocess.call(launch_command(argv, args.gpus))
+            sys.exit(rc)
+        return False
+    if int(world_env) != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}; launch one rank per GPU")
+    return False
+
+
+def probe_ranks():
+    """Launcher self-test: every rank joins a gloo group and rank 0 prints the ranks it saw."""
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    seen = [None] * dist.get_world_size()
+    dist.all_gather_object(seen, {"rank": dist.get_rank(), "pid": os.getpid()})
+    if dist.get_rank() == 0:
+        print(json.dumps({"probe": True, "world": dist.get_world_size(), "ranks": seen}), flush=True)
+    dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- helpers
 
 def load_peaks():
     p = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as fh:
-            d = json.load(fh)
-        return d, "measured"
+            return json.load(fh), "measured"
     return dict(FALLBACK_PEAKS), "fallback"
 
 
@@ -101,7 +167,7 @@ class ClockSampler:
             if len(parts) < 7:
                 continue
             try:
-                self.samples.append((time.time(), float(parts[0]), float(parts[1]), parts[3:7]))
+                self.samples.append((time.time(), float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
             except ValueError:
                 continue
 
@@ -119,9 +185,9 @@ class ClockSampler:
         win = [s for s in self.samples if t0 - 0.05 <= s[0] <= t1 + 0.05] or self.samples
         if not win:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        reasons = sorted({n for s in win for n, v in zip(self.NAMES, s[3]) if v.lower().startswith("active")})
+        reasons = sorted({n for s in win for n, v in zip(self.NAMES, s[4]) if v.lower().startswith("active")})
         return {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": max(s[2] for s in win),
-                "reasons": reasons, "samples": len(win)}
+                "power_w_max": max(s[3] for s in win), "reasons": reasons, "samples": len(win)}
 
 
 def cpu_threads() -> int:
@@ -135,59 +201,508 @@ def cpu_threads() -> int:
     return os.cpu_count() or 1
 
 
-def cpu_oracle_sample(rows: int, cols: int, seed: int, bf16: bool = True):
-    """Time the CPU oracle (numpy fp64 port of the reference) on a rows x cols sample."""
+# ----------------------------------------------------------------------------- CPU samples (oracle)
+# The ONLY place (with --impl reference) where bench.py executes oracle/: the reported CPU baseline.
+
+def cpu_sample_spec(args) -> dict:
+    """The bounded CPU sample of each workload: the same one in cpu_baseline and --impl reference."""
+    wl = args.workload
+    if wl == "cfg4":
+        rows, cols = _cfg4_shape(args)
+        srows = min(args.cpu_sample_rows or 32768, rows)
+        return {"method": "unso", "shapes": [(srows, cols)], "bf16": (args.precision or "bf16") == "bf16",
+                "desc": f"one UNSO orthogonalization of a {srows}x{cols} row sample of the {rows}x{cols} workload "
+                        f"(= one rank's shard at {max(rows // srows, 1)} GPUs)"}
+    if wl == "cfg1":
+        return {"method": "unso", "shapes": [(512, 128)], "bf16": False, "desc": "the full configs[0] matrix"}
+    if wl == "cfg2":
+        return {"method": "unso", "shapes": [(2048, 512)] * 4, "bf16": (args.precision or "fp32") == "bf16",
+                "desc": "4 of the 16 configs[1] matrices (2048x512)"}
+    if wl == "cfg3":
+        return {"method": "unso", "shapes": [(4096, 4096)], "bf16": True,
+                "desc": "one 4096x4096 of the 224 configs[2] matrices (orthogonalization only)"}
+    return {"method": "unso", "shapes": [(16384, 4096)], "bf16": (args.precision or "bf16") == "bf16",
+            "desc": "one 16384x4096 matrix (h = 4096 instead of configs[4]'s 8192: one full 16384x8192 "
+                    "takes ~100 s on the host)"}
+
+
+def cpu_oracle_run(spec: dict, seed: int):
+    """Time the CPU oracle on the sample; returns (model FLOPs, seconds)."""
     import numpy as np
     import torch
     from oracle import unso_oracle as O
-    g = torch.Generator().manual_seed(seed)
-    m = torch.randn(rows, cols, generator=g)
-    if bf16:
-        m = m.to(torch.bfloat16)
-    m = m.double().numpy()
-    t0 = time.perf_counter()
-    O.run(m, "unso")
-    dt = time.perf_counter() - t0
-    h, w = min(rows, cols), max(rows, cols)
-    return O.model_flops("unso", h, w), dt
+    flops, secs = 0, 0.0
+    for i, (r, c) in enumerate(spec["shapes"]):
+        g = torch.Generator().manual_seed(seed + i)
+        m = torch.randn(r, c, generator=g)
+        if spec["bf16"]:
+            m = m.to(torch.bfloat16)
+        m = np.ascontiguousarray(m.double().numpy())
+        t0 = time.perf_counter()
+        O.run(m, spec["method"])
+        secs += time.perf_counter() - t0
+        flops += O.model_flops(spec["method"], min(r, c), max(r, c))
+    return flops, secs
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle on the host cores, rank 0 only."""
+    """--impl reference: the CPU oracle on the host cores, rank 0 only (other ranks exit 0)."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
-    rows = min(args.ref_sample_rows, args.rows)
-    cols = args.cols
-    f = None
-    for _ in range(args.warmup):
-        f, _ = cpu_oracle_sample(rows, cols, 7)
-    times = []
-    for i in range(args.steps):
-        f, dt = cpu_oracle_sample(rows, cols, 7 + i)
-        times.append(dt)
-    total = sum(times)
-    value = f * len(times) / total / 1e12
+    spec = cpu_sample_spec(args)
+    steps = args.steps if args.steps is not None else 10
+    for i in range(min(args.warmup, 1)):  # one untimed pass warms OpenBLAS' thread pool
+        cpu_oracle_run(spec, 7 + i)
+    fl, secs = 0, []
+    for i in range(steps):
+        f, dt = cpu_oracle_run(spec, 100 + i)
+        fl = f
+        secs.append(dt)
+    total = sum(secs)
+    value = fl * len(secs) / total / 1e12
     cores = cpu_threads()
-    sample = (f"{rows}x{cols} row sample of the {args.rows}x{cols} workload (bf16-rounded N(0,1), fp64 numpy/OpenBLAS "
-              f"oracle restating unso.ortho.orthogonalize), {args.steps} timed steps")
+    sample = f"{spec['desc']}; fp64 numpy/OpenBLAS oracle restating unso.ortho.orthogonalize; {steps} timed steps"
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": f"configs[3] UNSO {args.rows}x{cols} (CPU sample {rows}x{cols})",
-                   "global_batch": 1, "shape": [args.rows, cols], "parallelism": "host threads"},
+        "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(secs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_NAMES[args.workload] + f" (CPU sample: {spec['desc']})",
+                   "parallelism": f"{cores} host threads"},
+        "matrices_per_s": len(spec["shapes"]) * len(secs) / total,
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    rec = _cpu_full_record(args)
+    if rec:
+        line["cpu_baseline"]["full_workload_recorded"] = rec
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse_args()
-    if args.impl == "reference":
-        run_reference(args)
+def _cpu_full_record(args):
+    if not os.path.exists(CPU_FULL_RECORD):
+        return None
+    with open(CPU_FULL_RECORD) as fh:
+        return json.load(fh).get(args.workload)
+
+
+def cpu_full_measure(args):
+    """--cpu-full: the CPU oracle on the FULL cfg4 matrix once (~100 s); recorded for later lines."""
+    import numpy as np
+    import torch
+    from oracle import unso_oracle as O
+    rows, cols = _cfg4_shape(args)
+    g = torch.Generator().manual_seed(1234)
+    m = np.ascontiguousarray(torch.randn(rows, cols, generator=g).to(torch.bfloat16).double().numpy())
+    t0 = time.perf_counter()
+    O.run(m, "unso")
+    dt = time.perf_counter() - t0
+    f = O.model_flops("unso", min(rows, cols), max(rows, cols))
+    rec = {"value": f / dt / 1e12, "unit": "TFLOP/s", "seconds": dt, "cores": cpu_threads(), "kind": "port",
+           "sample": f"the full {rows}x{cols} matrix, one UNSO orthogonalization",
+           "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+    data = {}
+    if os.path.exists(CPU_FULL_RECORD):
+        with open(CPU_FULL_RECORD) as fh:
+            data = json.load(fh)
+    data[args.workload] = rec
+    with open(CPU_FULL_RECORD, "w") as fh:
+        json.dump(data, fh, indent=1)
+    return rec
+
+
+# ----------------------------------------------------------------------------- executed-FLOP model
+
+def _tiles(h: int, t: int) -> int:
+    n = -(-h // t)
+    return n * (n + 1) // 2
+
+
+def executed_flops_bf16_unso(h: int, w: int, order: int, chain_steps: float, apply_single: bool,
+                             route: str) -> dict:
+    """FLOPs the bf16-mode UNSO kernels issue for one h x w matrix (bf16-equivalent: an e4m3 product
+    costs half a bf16 product on tcgen05).  Mirrors the routes of csrc/unso_b200.cu:
+      gram     CTA-pair SYRK, 256 x 256 upper tiles over the long side;
+      chain    persistent (h <= 2048): 128 x 128 upper tiles, bf16x3 (3 products), chain_steps squarings
+               (device-side truncation); glue-free (h > 2048): 256 x 256 pair tiles, squarings 1-3
+               hi*hi (1 product), the rest hi*hi + two e4m3 cross terms (2 bf16-equivalents);
+      apply    X (R_hi [+ R_lo]): 1 or 2 products of the full h x h P."""
+    hp256 = -(-h // 256) * 256
+    gram = 2.0 * w * 256 * 256 * _tiles(h, 256)
+    if route == "persistent":
+        hp = -(-h // 128) * 128
+        chain = chain_steps * 3 * 2.0 * hp * 128 * 128 * _tiles(h, 128)
+    else:
+        per = 2.0 * hp256 * 256 * 256 * _tiles(h, 256)
+        hi_only = 3 if order >= 12 else 0
+        n = order - 1
+        chain = per * (min(hi_only, n) + 2 * max(n - hi_only, 0))
+    apply = 2.0 * w * h * h * (1 if apply_single else 2)
+    return {"gram": gram, "chain": chain, "apply": apply, "total": gram + chain + apply}
+
+
+# ----------------------------------------------------------------------------- workloads
+
+WORKLOAD_NAMES = {
+    "cfg1": "configs[0]: one 512x128 fp32 matrix N(0,1), UNSO order-14",
+    "cfg2": "configs[1]: 16 x 2048x512 fp32, Haar U/V, s log-uniform [1e-4,1], UNSO order-14",
+    "cfg3": "configs[2]: Muon optimizer step, 32 layers x {4x 4096x4096, 2x 14336x4096, 4096x14336} bf16",
+    "cfg4": "configs[3]: one 262144x2048 bf16 matrix N(0,1), UNSO order-14",
+    "cfg5": "configs[4]: 4 x 16384x8192 fp32, Haar U/V, Pareto(1.5) spectrum in [1e-6,1], UNSO order-14",
+}
+
+
+def _cfg4_shape(args):
+    return (args.rows or 262144), (args.cols or 2048)
+
+
+def _controlled(batch, rows, cols, seeds, dev, spectrum):
+    """X = U diag(s) V^T with Haar U (rows x k), V (cols x k) in fp64 on the device (seeded)."""
+    import numpy as np
+    import torch
+    k = min(rows, cols)
+    out = torch.empty(batch, rows, cols, dtype=torch.float32, device=dev)
+    for b in range(batch):
+        g = torch.Generator(device=dev).manual_seed(seeds[b])
+
+        def haar(n):
+            q, r = torch.linalg.qr(torch.randn(n, k, generator=g, device=dev, dtype=torch.float64))
+            return q * torch.sign(torch.diagonal(r))
+        s = torch.from_numpy(spectrum(np.random.default_rng(seeds[b]), k)).to(dev)
+        out[b] = ((haar(rows) * s[None, :]) @ haar(cols).T).float()
+        torch.cuda.synchronize(dev)
+    return out
+
+
+def _logu(rng, k):
+    import numpy as np
+    return np.exp(rng.uniform(np.log(1e-4), 0.0, k))
+
+
+def _pareto(rng, k):
+    s = 1.0 + rng.pareto(1.5, k)
+    return 1e-6 + (s - s.min()) / (s.max() - s.min()) * (1.0 - 1e-6)
+
+
+class MatrixWorkload:
+    """One orthogonalize call per step over this rank's matrices (a 2-D matrix or a 3-D batch)."""
+
+    def __init__(self, args, U, dev, rank, world):
+        import torch
+        self.args, self.U, self.dev, self.rank, self.world = args, U, dev, rank, world
+        wl = args.workload
+        self.sharded = False
+        self.precision = args.precision or {"cfg1": "fp32", "cfg2": "fp32", "cfg4": "bf16", "cfg5": "bf16"}[wl]
+        self.spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), precision=self.precision,
+                                 apply_terms=args.apply_terms)
+        if wl == "cfg4":
+            rows, cols = _cfg4_shape(args)
+            self.sharded = world > 1 or args.sharded
+            from paper_2602_02500_b200.distributed import row_shard_bounds
+            r0, r1 = row_shard_bounds(rows, world, rank) if self.sharded else (0, rows)
+            g = torch.Generator(device=dev).manual_seed(1234 + rank)
+            dt = torch.bfloat16 if self.precision == "bf16" else torch.float32
+            self.x = torch.randn(r1 - r0, cols, generator=g, device=dev, dtype=torch.float32).to(dt)
+            self.shape, self.total_batch, self.scaling = (rows, cols), 1, "strong"
+            self.data = "synthetic: i.i.d. N(0,1) from torch.Generator(seed 1234+rank), no dataset"
+        elif wl == "cfg1":
+            g = torch.Generator(device=dev).manual_seed(0)
+            self.x = torch.randn(512, 128, generator=g, device=dev, dtype=torch.float32)
+            if self.precision == "bf16":
+                self.x = self.x.to(torch.bfloat16)
+            self.shape, self.total_batch, self.scaling = (512, 128), world, "weak"
+            self.data = "synthetic: i.i.d. N(0,1) (torch.Generator seed 0); N > 1 = independent replicas"
+        else:
+            batch, rows, cols, spec_fn = ((16, 2048, 512, _logu) if wl == "cfg2" else (4, 16384, 8192, _pareto))
+            per = -(-batch // world)
+            mine = list(range(min(batch, rank * per), min(batch, (rank + 1) * per)))
+            self.x = _controlled(len(mine), rows, cols, [11 + i for i in mine], dev, spec_fn) if mine else None
+            if self.x is not None and self.precision == "bf16" and wl == "cfg2":
+                pass  # fp32 input, bf16 mode: the library rounds it once (ortho: bf16 operand copy)
+            self.shape, self.total_batch, self.scaling = (rows, cols), batch, "strong"
+            self.data = ("synthetic: Haar U/V (QR of seeded Gaussians, fp64 on the device) x "
+                         + ("log-uniform [1e-4,1]" if wl == "cfg2" else "Pareto(1.5) rescaled to [1e-6,1]")
+                         + f" spectrum; {len(mine)} of {batch} matrices on this rank")
+        rows, cols = self.shape
+        self.h, self.w = (cols, rows) if rows > cols else (rows, cols)
+        self.y = torch.empty_like(self.x) if self.x is not None else None
+        self.model_flops = self.U.kernel_model_flops(self.h, self.w, self.spec) * self.total_batch
+        self.launches = 0
+
+    # the timed step
+    def step(self, x=None, y=None):
+        x = self.x if x is None else x
+        y = self.y if y is None else y
+        if x is None:
+            return
+        if self.sharded:
+            from paper_2602_02500_b200.distributed import orthogonalize_row_sharded
+            orthogonalize_row_sharded(x, self.spec, out=y, check=False, collective=self.args.collective)
+        else:
+            self.U.orthogonalize(x, self.spec, out=y, check=False)
+
+    def gate(self):
+        """Untimed: status check, our orthogonality error, the reference's exact-arithmetic value."""
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        U, N = self.U, self.U._native
+        out = {"info": None}
+        if self.x is None:
+            return out
+        if not self.sharded:
+            res = U.orthogonalize(self.x, self.spec, out=self.y, check=True)
+            self.launches = res.launches
+            out["info"] = res.info
+        else:
+            from paper_2602_02500_b200 import distributed as D
+            D.orthogonalize_row_sharded(self.x, self.spec, out=self.y, check=True, collective=self.args.collective)
+            if self.args.collective == "nccl":
+                g = D.native_gram(self.x, self.spec, None)
+                self.launches = N.launch_count()
+            else:
+                red = D._nvlink_reducer(self.h, self.x.shape[0], None, self.dev)
+                red.push(self.x, self.spec, None)
+                self.launches = N.launch_count()
+                red.reduce()
+                self.launches += N.launch_count()
+                g = red.wait()
+                self.launches += N.launch_count()
+            D.native_finish(self.x, g, self.spec, None, self.y)
+            self.launches += N.launch_count()
+        torch.cuda.synchronize()
+        ys = self.y if self.y.dim() == 3 else self.y[None]
+        xs = self.x if self.x.dim() == 3 else self.x[None]
+        errs, refs = [], []
+        for b in range(ys.shape[0]):
+            yf, xf = ys[b].double(), xs[b].double()
+            tall = yf.shape[0] > yf.shape[1]
+            gy = yf.T @ yf if tall else yf @ yf.T
+            gx = xf.T @ xf if tall else xf @ xf.T
+            if self.sharded:
+                dist.all_reduce(gy)
+                dist.all_reduce(gx)
+            errs.append(float(torch.linalg.norm(gy - torch.eye(gy.shape[0], device=gy.device, dtype=gy.dtype))))
+            # the reference's result has singular values g(sigma(X)/s) (scalar_map, ortho.py:286-310)
+            sx = torch.sqrt(torch.linalg.eigvalsh(gx).clamp_min(0.0)).cpu().numpy()
+            sy = U.scalar_map(self.spec)(sx / float((sx ** 4).sum()) ** 0.25)
+            refs.append(float(np.sqrt(((sy ** 2 - 1.0) ** 2).sum())))
+        out["ortho_error"] = errs[0] if len(errs) == 1 else errs
+        out["ortho_error_reference"] = refs[0] if len(refs) == 1 else refs
+        return out
+
+    def executed(self, info):
+        """Executed bf16-equivalent FLOPs per step (whole job), bf16 mode only."""
+        if self.precision != "bf16" or not info:
+            return None
+        route = "persistent" if self.h <= 2048 else "glue-free"
+        tot = {"gram": 0.0, "chain": 0.0, "apply": 0.0, "total": 0.0}
+        for d in info:
+            e = executed_flops_bf16_unso(self.h, self.w, self.spec.coeffs.order, d["chain_steps"] or 13,
+                                         bool(d["apply_single"]), route)
+            for k in tot:
+                tot[k] += e[k] * (self.total_batch / len(info))
+        return tot
+
+    def stage_model(self):
+        """Algorithmic (model) FLOPs per call of each stage, this rank."""
+        b = 1 if self.x is None or self.x.dim() == 2 else self.x.shape[0]
+        h, w = self.h, (self.x.shape[-2] if self.sharded else self.w)
+        return {"gram": 2.0 * w * h * h * b, "apply": 2.0 * w * h * h * b,
+                "chain": 2.0 * (self.spec.coeffs.order - 1) * h ** 3 * b}
+
+    def hbm_bytes(self):
+        """Algorithmic HBM bytes of the stand-alone reduction/normalisation stages (per call):
+        finalize_p reads the fp32 P upper triangle and writes P/s - dI as bf16 hi + lo (both triangles)."""
+        b = 1 if self.x is None or self.x.dim() == 2 else self.x.shape[0]
+        return {"finalize_p": 6.0 * self.h * self.h * b}
+
+    def host_io(self):
+        return [self.x], [self.y]
+
+
+class MuonWorkload:
+    """configs[2]: one Muon optimizer step over the synthetic layer stack (bf16)."""
+
+    SHAPES = [(4096, 4096)] * 4 + [(14336, 4096)] * 2 + [(4096, 14336)]
+
+    def __init__(self, args, U, dev, rank, world):
+        import torch
+        self.args, self.U, self.dev, self.rank, self.world = args, U, dev, rank, world
+        self.precision = args.precision or "bf16"
+        self.sharded = world > 1
+        g = torch.Generator(device=dev).manual_seed(7)  # same on every rank: replicated (all-reduced) grads
+        self.params = []
+        for _ in range(args.layers):
+            for s in self.SHAPES:
+                p = torch.nn.Parameter(torch.zeros(s, dtype=torch.bfloat16, device=dev))
+                p.grad = (torch.randn(s, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+                self.params.append(p)
+        self.opt = U.Muon(self.params, lr=0.02, momentum=0.95, precision=self.precision, distribute=self.sharded)
+        self.spec = self.opt.spec
+        self.model_flops = sum(U.kernel_model_flops(min(p.shape), max(p.shape), self.spec) for p in self.params)
+        self.total_batch = len(self.params)
+        self.scaling = "strong"
+        self.shape = None
+        self.data = ("synthetic: bf16 parameters (zeros) with gradients i.i.d. N(0, 0.02^2) from "
+                     "torch.Generator(seed 7), identical on every rank (as after a data-parallel all-reduce)")
+        self.launches = 0
+
+    def step(self):
+        self.opt.step()
+
+    def gate(self):
+        """Untimed: orthogonality errors of one matrix of each shape group, and the call structure."""
+        import numpy as np
+        import torch
+        U, N = self.U, self.U._native
+        out = {"info": {}}
+        errs, refs = {}, {}
+        launches = 2 * 3  # the fused momentum/prepare and update passes of the 3 shape groups
+        for s in sorted(set(self.SHAPES)):
+            items = [p for p in self.params if tuple(p.shape) == s]
+            stacked = torch.stack([p.grad for p in items[: max(1, len(items) // self.world)]])
+            res = U.orthogonalize(stacked, self.spec, precision=self.precision, check=True)
+            launches += res.launches
+            out["info"][f"{s[0]}x{s[1]}"] = res.info
+            y, x = res.y[0].double(), stacked[0].double()
+            tall = y.shape[0] > y.shape[1]
+            gy = y.T @ y if tall else y @ y.T
+            gx = x.T @ x if tall else x @ x.T
+            errs[f"{s[0]}x{s[1]}"] = float(torch.linalg.norm(gy - torch.eye(gy.shape[0], device=gy.device,
+                                                                            dtype=gy.dtype)))
+            sx = torch.sqrt(torch.linalg.eigvalsh(gx).clamp_min(0.0)).cpu().numpy()
+            sy = U.scalar_map(self.spec)(sx / float((sx ** 4).sum()) ** 0.25)
+            refs[f"{s[0]}x{s[1]}"] = float(np.sqrt(((sy ** 2 - 1.0) ** 2).sum()))
+        self.launches = launches
+        self.opt.step()  # allocates the momentum buffers before timing
+        torch.cuda.synchronize()
+        out["ortho_error"] = errs
+        out["ortho_error_reference"] = refs
+        return out
+
+    def executed(self, info):
+        if self.precision != "bf16" or not info:
+            return None
+        tot = {"gram": 0.0, "chain": 0.0, "apply": 0.0, "total": 0.0}
+        for key, rows in info.items():
+            r, c = map(int, key.split("x"))
+            h, w = min(r, c), max(r, c)
+            n = sum(1 for p in self.params if tuple(p.shape) == (r, c))
+            for d in rows:
+                e = executed_flops_bf16_unso(h, w, self.spec.coeffs.order, d["chain_steps"] or 13,
+                                             bool(d["apply_single"]), "persistent" if h <= 2048 else "glue-free")
+                for k in tot:
+                    tot[k] += e[k] * n / len(rows)
+        return tot
+
+    def stage_model(self):
+        """Model FLOPs per step of each stage, summed over the groups (this rank's share)."""
+        tot = {"gram": 0.0, "apply": 0.0, "chain": 0.0}
+        for p in self.params:
+            h, w = min(p.shape), max(p.shape)
+            tot["gram"] += 2.0 * w * h * h / self.world
+            tot["apply"] += 2.0 * w * h * h / self.world
+            tot["chain"] += 2.0 * (self.spec.coeffs.order - 1) * h ** 3 / self.world
+        return tot
+
+    def hbm_bytes(self):
+        return {"finalize_p": sum(6.0 * min(p.shape) ** 2 for p in self.params) / self.world}
+
+
+# ----------------------------------------------------------------------------- e2e
+
+def run_e2e_matrix(work, steps, dev):
+    """Pinned host -> device copy of each step's input, the public API call, device -> pinned host
+    copy of the result; consecutive steps pipelined on three streams (double-buffered)."""
+    import torch
+    if work.x is None:
+        return None
+    x, y = work.x, work.y
+    x_host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    x_host.copy_(x)
+    y_host = [torch.empty(y.shape, dtype=y.dtype, pin_memory=True) for _ in range(2)]
+    xd = [torch.empty_like(x) for _ in range(2)]
+    yd = [torch.empty_like(y) for _ in range(2)]
+    s_h2d, s_cmp, s_d2h = (torch.cuda.Stream(device=dev) for _ in range(3))
+    ev_cmp = [torch.cuda.Event() for _ in range(2)]
+    ev_h2d = [torch.cuda.Event() for _ in range(2)]
+    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+    started = [False, False]
+
+    def e2e_step(i):
+        j = i % 2
+        with torch.cuda.stream(s_h2d):
+            if started[j]:
+                s_h2d.wait_event(ev_cmp[j])
+            xd[j].copy_(x_host, non_blocking=True)
+            ev_h2d[j].record(s_h2d)
+        with torch.cuda.stream(s_cmp):
+            s_cmp.wait_event(ev_h2d[j])
+            if started[j]:
+                s_cmp.wait_event(ev_d2h[j])
+            work.step(xd[j], yd[j])
+            ev_cmp[j].record(s_cmp)
+        with torch.cuda.stream(s_d2h):
+            s_d2h.wait_event(ev_cmp[j])
+            y_host[j].copy_(yd[j], non_blocking=True)
+            ev_d2h[j].record(s_d2h)
+        started[j] = True
+
+    for i in range(2):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s_h2d)
+    for i in range(steps):
+        e2e_step(i)
+    s_d2h.wait_stream(s_cmp)
+    e1.record(s_d2h)
+    torch.cuda.synchronize()
+    nbytes = x.numel() * x.element_size()
+    return e0.elapsed_time(e1) / steps, nbytes, y.numel() * y.element_size(), (
+        "pinned host -> device copy, orthogonalize (unso_orthogonalize), device -> pinned host copy; consecutive "
+        "steps pipelined on three streams (double-buffered)")
+
+
+def run_e2e_muon(work, steps, dev):
+    """Gradients copied in from pinned host memory, the optimizer step, the updated parameters copied
+    back to pinned host memory, every step, sequentially on one stream."""
+    import torch
+    grads_h = [torch.empty(p.shape, dtype=p.dtype, pin_memory=True) for p in work.params]
+    params_h = [torch.empty(p.shape, dtype=p.dtype, pin_memory=True) for p in work.params]
+    for gh, p in zip(grads_h, work.params):
+        gh.copy_(p.grad)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        for gh, p in zip(grads_h, work.params):
+            p.grad.copy_(gh, non_blocking=True)
+        work.step()
+        for ph, p in zip(params_h, work.params):
+            ph.copy_(p.detach(), non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    nbytes = sum(p.numel() * p.element_size() for p in work.params)
+    return e0.elapsed_time(e1) / steps, nbytes, nbytes, (
+        "gradients pinned host -> device, Muon.step (grouped orthogonalize), updated parameters device -> "
+        "pinned host, sequential on one stream")
+
+
+# ----------------------------------------------------------------------------- main
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
+    args = parse_args(argv)
+    if args.probe_ranks:
+        if not maybe_relaunch(args, argv):
+            probe_ranks()
         return
+    if args.impl == "reference":
+        if os.environ.get("WORLD_SIZE") is None or int(os.environ.get("RANK", "0")) == 0:
+            run_reference(args)
+        return
+    maybe_relaunch(args, argv)
 
     import numpy as np
     import torch
@@ -195,88 +710,30 @@ def main():
 
     import paper_2602_02500_b200 as U
     from paper_2602_02500_b200 import _native as N
-    from paper_2602_02500_b200.distributed import orthogonalize_row_sharded, row_shard_bounds
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    sharded = world > 1 or args.sharded
-    if sharded:
+    multi = world > 1 or args.sharded
+    if multi:
         dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
-        if sharded:
+        if multi:
             dist.barrier()
 
-    rows, cols = args.rows, args.cols
-    h, w = (cols, rows) if rows > cols else (rows, cols)
-    r0, r1 = row_shard_bounds(rows, world, rank)
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    x = torch.randn(r1 - r0, cols, generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16
-                                                                                      if args.precision == "bf16"
-                                                                                      else torch.float32)
-    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), precision=args.precision,
-                        apply_terms=args.apply_terms)
-    y = torch.empty_like(x)
-
-    def step():
-        if not sharded:
-            U.orthogonalize(x, spec, out=y, check=False)
-        else:
-            orthogonalize_row_sharded(x, spec, out=y, check=False, collective=args.collective)
-
-    # ---- correctness gate (untimed): status + orthogonality of the output
-    apply_info = None
-    if not sharded:
-        res = U.orthogonalize(x, spec, out=y, check=True)
-        launches_per_step = res.launches
-        apply_info = res.info[0] if res.info else None
-    else:
-        orthogonalize_row_sharded(x, spec, out=y, check=True, collective=args.collective)
-        launches_per_step = None
-    torch.cuda.synchronize()
-    if not sharded:
-        ortho_err = float(U.ortho_error_device(y)[0])
-    else:   # untimed check: ||Y^T Y - I||_F with the shard Grams summed over the group
-        yf = y.float()
-        gy = (yf.T @ yf) if rows > cols else (yf @ yf.T)
-        dist.all_reduce(gy)
-        gy -= torch.eye(gy.shape[0], device=dev)
-        ortho_err = float(torch.linalg.norm(gy))
-    # The reference's own orthogonality error on this input: Y_ref = X P(X^T X) has singular values
-    # g(sigma(X)) (the scalar map, ortho.py:286-310), so ||Y_ref^T Y_ref - I||_F follows from the
-    # spectrum of X (fp64 Gram, summed over the shards, eigenvalues on the device; untimed).
-    xg = x.double()
-    gx = (xg.T @ xg) if rows > cols else (xg @ xg.T)
-    del xg
-    if sharded:
-        dist.all_reduce(gx)
-    sx = torch.sqrt(torch.linalg.eigvalsh(gx).clamp_min(0.0)).cpu().numpy()
-    del gx
-    sy = U.scalar_map(spec)(sx / float((sx ** 4).sum()) ** 0.25)
-    ortho_ref = float(np.sqrt(((sy ** 2 - 1.0) ** 2).sum()))
-    if launches_per_step is None:
-        # our kernels per step, from the library's per-call counters: the Gram stage (or the
-        # push / reduce / wait kernels of the peer-memory reduction) plus the finish stage
-        if args.collective == "nccl":
-            g = U.distributed.native_gram(x, spec, None)
-            launches_per_step = N.launch_count()
-        else:
-            red = U.distributed._nvlink_reducer(cols, x.shape[0], None, dev)
-            red.push(x, spec, None)
-            launches_per_step = N.launch_count()
-            red.reduce()
-            launches_per_step += N.launch_count()
-            g = red.wait()
-            launches_per_step += N.launch_count()
-        U.distributed.native_finish(x, g, spec, None, y)
-        launches_per_step += N.launch_count()
-        torch.cuda.synchronize()
+    wl = args.workload
+    steps = args.steps if args.steps is not None else {"cfg1": 200, "cfg2": 50, "cfg3": 3, "cfg4": 50,
+                                                       "cfg5": 5}[wl]
+    if wl == "cfg3" and args.precision == "fp32":
+        sys.exit("bench.py: cfg3 runs in bf16 mode")
+    work = MuonWorkload(args, U, dev, rank, world) if wl == "cfg3" else MatrixWorkload(args, U, dev, rank, world)
+    gate = work.gate()
 
     for _ in range(max(args.warmup, 0)):
-        step()
+        work.step()
     torch.cuda.synchronize()
     barrier()
 
@@ -286,15 +743,16 @@ def main():
     time.sleep(0.2)
     stream = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    prof = N.StageProfiler(args.steps) if not sharded else None
+    calls_per_step = 3 if wl == "cfg3" else 1
+    prof = N.StageProfiler(steps * calls_per_step) if (world == 1 and not args.sharded) else None
     if prof:
         prof.__enter__()
     barrier()
     torch.cuda.synchronize()
     t_wall0 = time.time()
     ev0.record(stream)
-    for _ in range(args.steps):
-        step()
+    for _ in range(steps):
+        work.step()
     ev1.record(stream)
     torch.cuda.synchronize()
     t_wall1 = time.time()
@@ -306,141 +764,185 @@ def main():
     time.sleep(0.1)
     sampler.stop()
     ms_t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-    if sharded:
+    if multi:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_total = float(ms_t.item())
-    ms_step = ms_total / args.steps
+    ms_step = float(ms_t.item()) / steps
 
-    F = U.kernel_model_flops(h, w, spec)
+    F = work.model_flops
     value = F / (ms_step / 1e3) / 1e12
     peak = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
     peak_sus = peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"])
+    hbm_peak = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
 
-    # ---- e2e through the public API with pinned host buffers.  Every step copies its input
-    # host -> device and its result device -> host inside the timed region; consecutive steps are
-    # pipelined on three streams (H2D of step i+1 and D2H of step i-1 overlap the compute of step i,
-    # double-buffered device buffers), as a production caller streaming matrices would run it.
+    # ---- executed work (what the tensor cores actually issue)
+    execd = work.executed(gate.get("info"))
+    executed = None
+    if execd:
+        executed = {"flops_per_step": execd["total"], "tflops": execd["total"] / (ms_step / 1e3) / 1e12,
+                    "frac_of_peak": execd["total"] / (ms_step / 1e3) / 1e12 / peak,
+                    "by_stage": {k: execd[k] for k in ("gram", "chain", "apply")},
+                    "how": "bf16-equivalent FLOPs the kernels issue: SYRK upper tiles, truncated chain, "
+                           "split products (e4m3 at half a bf16 FLOP)"}
+
+    # ---- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        x_host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
-        x_host.copy_(x)
-        y_host = [torch.empty(y.shape, dtype=y.dtype, pin_memory=True) for _ in range(2)]
-        xd = [torch.empty_like(x) for _ in range(2)]
-        yd = [torch.empty_like(y) for _ in range(2)]
-        s_h2d, s_cmp, s_d2h = (torch.cuda.Stream(device=dev) for _ in range(3))
-        ev_h2d = [torch.cuda.Event() for _ in range(2)]
-        ev_cmp = [torch.cuda.Event() for _ in range(2)]
-        ev_d2h = [torch.cuda.Event() for _ in range(2)]
-        started = [False, False]
-
-        def e2e_step(i):
-            j = i % 2
-            with torch.cuda.stream(s_h2d):
-                if started[j]:
-                    s_h2d.wait_event(ev_cmp[j])      # step i-2 finished reading xd[j]
-                xd[j].copy_(x_host, non_blocking=True)
-                ev_h2d[j].record(s_h2d)
-            with torch.cuda.stream(s_cmp):
-                s_cmp.wait_event(ev_h2d[j])
-                if started[j]:
-                    s_cmp.wait_event(ev_d2h[j])      # step i-2's result left yd[j]
-                if not sharded:
-                    U.orthogonalize(xd[j], spec, out=yd[j], check=False)
-                else:
-                    orthogonalize_row_sharded(xd[j], spec, out=yd[j], check=False, collective=args.collective)
-                ev_cmp[j].record(s_cmp)
-            with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(ev_cmp[j])
-                y_host[j].copy_(yd[j], non_blocking=True)
-                ev_d2h[j].record(s_d2h)
-            started[j] = True
-
-        for i in range(2):
-            e2e_step(i)
-        torch.cuda.synchronize()
+        e_steps = args.e2e_steps or (1 if wl == "cfg3" else min(30, max(steps, 4)))
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s_h2d)
-        for i in range(args.e2e_steps):
-            e2e_step(i)
-        s_d2h.wait_stream(s_cmp)
-        e1.record(s_d2h)
-        torch.cuda.synchronize()
-        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if sharded:
+        r = run_e2e_muon(work, e_steps, dev) if wl == "cfg3" else run_e2e_matrix(work, e_steps, dev)
+        if r is not None:
+            e_ms, bi, bo, path = r
+        else:
+            e_ms, bi, bo, path = 0.0, 0, 0, "no matrices on this rank"
+        et = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        bt = torch.tensor([bi, bo], dtype=torch.float64, device=dev)
+        if multi:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_ms = float(et.item()) / args.e2e_steps
-        nbytes = x.numel() * x.element_size()
+            dist.all_reduce(bt)
+        e_ms = float(et.item())
         e2e = {"value": F / (e_ms / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
-               "path": "pinned host -> device copy, unso_orthogonalize, device -> pinned host copy; "
-                       "consecutive steps pipelined on three streams (double-buffered)"}
+               "h2d_bytes_per_step": int(bt[0].item()), "d2h_bytes_per_step": int(bt[1].item()), "path": path}
 
     # ---- roofline of the dominant kernel (stage times from CUDA events inside the timed region)
-    roofline = None
-    stages = None
+    roofline, stages, hbm = None, None, None
     if stage_ms is not None and len(stage_ms):
-        mean = stage_ms.mean(axis=0)
-        stages = {n: float(v) for n, v in zip(N.PROFILE_STAGES, mean)}
-        algo = {"gram": 2.0 * w * h * h, "apply": 2.0 * w * h * h,
-                "chain": 2.0 * (spec.coeffs.order - 1) * h ** 3}
+        per_step = stage_ms.reshape(steps, calls_per_step, -1).sum(axis=1).mean(axis=0)
+        stages = {n: float(v) for n, v in zip(N.PROFILE_STAGES, per_step)}
+        algo = work.stage_model()
         dom = max(algo, key=lambda k: stages[k])
         achieved = algo[dom] / (stages[dom] / 1e3) / 1e12
         traffic = None
         tp = os.path.join(REPO, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             with open(tp) as fh:
-                traffic = json.load(fh).get(f"{dom}:{rows}x{cols}:{args.precision}")
+                traffic = json.load(fh).get(f"{dom}:{wl}:{work.precision}")
         roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "frac_of_sustained": achieved / peak_sus, "traffic": traffic,
                     "peak_source": f"{peaks_src} bf16_tflops (burst)",
-                    "algorithmic_flops_per_launch": algo[dom], "avg_launch_ms": stages[dom]}
+                    "algorithmic_flops_per_step": algo[dom], "stage_ms_per_step": stages[dom]}
+        if execd and dom in execd:
+            roofline["executed_tflops"] = execd[dom] / (stages[dom] / 1e3) / 1e12
+            roofline["executed_frac"] = roofline["executed_tflops"] / peak
+        hb = work.hbm_bytes()
+        hbm = {}
+        for k, nbytes in hb.items():
+            if stages.get(k, 0.0) > 0.01:  # a stand-alone stage (fused into the chain kernel otherwise)
+                gbs = nbytes / (stages[k] / 1e3) / 1e9
+                hbm[k] = {"bytes_per_step": nbytes, "ms_per_step": stages[k], "GB/s": gbs, "frac": gbs / hbm_peak}
+            else:
+                hbm[k] = {"fused": "into the persistent chain kernel (no stand-alone launch)",
+                          "ms_per_step": stages.get(k)}
 
+    # ---- cfg4: per-rank critical path of an N-way row shard, measured on this GPU
+    projection = None
+    if wl == "cfg4" and world == 1 and not args.sharded and not args.no_projection:
+        projection = shard_projection(work, U, N, dev, ms_step)
+
+    # ---- CPU baseline: the same bounded sample as --impl reference, on this box's host cores
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        srows = min(args.cpu_sample_rows, rows)
-        f, dt = cpu_oracle_sample(srows, cols, 99, bf16=args.precision == "bf16")
+        spec = cpu_sample_spec(args)
+        f, dt = cpu_oracle_run(spec, 100)
         cpu_base = {"value": f / dt / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
-                    "sample": f"one UNSO orthogonalization of a {srows}x{cols} row sample (fp64 numpy oracle)",
+                    "sample": spec["desc"] + " (fp64 numpy oracle; same sample as --impl reference)",
                     "seconds": dt}
+        rec = cpu_full_measure(args) if (args.cpu_full and wl == "cfg4") else _cpu_full_record(args)
+        if rec:
+            cpu_base["full_workload_recorded"] = rec
 
     clocks = sampler.summary(t_wall0, t_wall1)
     if rank == 0:
+        shape = work.shape
+        cfg = {"workload": WORKLOAD_NAMES[wl] + ("" if args.rows is None and args.cols is None else
+                                                f" (shape overridden: {shape[0]}x{shape[1]})"),
+               "global_batch": work.total_batch,
+               "precision_mode": work.precision,
+               "parallelism": parallelism_name(wl, world, multi, args.collective),
+               "l2": "inputs larger than the 126 MB L2 (no flush needed)" if wl in ("cfg3", "cfg4", "cfg5") else
+                     "working set fits in L2: inputs stay L2-resident between steps (latency-bound config)"}
+        if shape:
+            cfg["shape"] = list(shape)
         line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
-            "data": "synthetic: i.i.d. N(0,1) from torch.Generator(seed 1234+rank), no dataset",
-            "config": {"workload": f"configs[3]: one {rows}x{cols} {args.precision} matrix, UNSO order-14 "
-                                   "shipped coefficients", "global_batch": 1, "shape": [rows, cols],
-                       "precision_recipe": ("bf16 Gram, bf16x3 C-form chain, "
-                                            + {None: "adaptive bf16/bf16x2 (shifted P)", 1: "bf16", 2: "bf16x2"}[
-                                                args.apply_terms] + " apply")
-                       if args.precision == "bf16" else "fp64-grade DFMA",
-                       "parallelism": (f"row-shard x{world} + " + ("NCCL all-reduce of G" if args.collective == "nccl" else
-                                 "NVLink peer-memory reduction of G")) if sharded else "1 GPU",
-                       "l2": "input 1 GiB > 126 MB L2 (no flush needed)"},
-            "matrices_per_s": 1e3 / ms_step,
-            "pct_bf16_peak": value / peak,
-            "pct_bf16_peak_sustained": value / peak_sus,
-            "flops_per_matrix": F,
+            "scaling": work.scaling, "vs_baseline": None, "dtype": work.precision,
+            "data": work.data, "config": cfg,
+            "matrices_per_s": work.total_batch / (ms_step / 1e3),
+            "model_flops_per_step": F,
+            "pct_bf16_peak_model_flops": value / peak,
+            "executed": executed,
             "roofline": roofline,
+            "hbm_stages": hbm,
             "stages_ms": stages,
             "cpu_baseline": cpu_base,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": work.launches * steps if work.launches else None,
             "clocks": clocks,
-            "ortho_error": ortho_err,
-            "ortho_error_reference": ortho_ref,
+            "ortho_error": gate.get("ortho_error"),
+            "ortho_error_reference": gate.get("ortho_error_reference"),
             "ortho_error_reference_how": "exact-arithmetic value of the reference polynomial on this input: "
                                          "sqrt(sum (g(sigma_i)^2 - 1)^2), sigma from the fp64 Gram of X",
-            "apply_decision": None if apply_info is None else {
-                "single_term": bool(apply_info["apply_single"]), "bound": apply_info["apply_bound"],
-                "shift": apply_info["shift"]},
         }
+        if projection:
+            line["shard_projection"] = projection
+        info = gate.get("info")
+        if isinstance(info, list) and info and wl == "cfg4":
+            d = info[0]
+            line["apply_decision"] = {"single_term": bool(d["apply_single"]), "bound": d["apply_bound"],
+                                      "shift": d["shift"], "chain_steps": d["chain_steps"]}
         print(json.dumps(line), flush=True)
-    if sharded:
+    if multi:
         dist.destroy_process_group()
+
+
+def parallelism_name(wl, world, multi, collective):
+    if not multi:
+        return "1 GPU"
+    if wl == "cfg4":
+        return f"row-shard x{world} + " + ("NCCL all-reduce of G" if collective == "nccl" else
+                                           "NVLink peer-memory reduction of G")
+    if wl == "cfg1":
+        return f"{world} independent replicas"
+    if wl == "cfg3":
+        return f"data-parallel Muon: shape-group shares x{world} + all-gather of the updates"
+    return f"batch shares x{world}, no communication"
+
+
+def shard_projection(work, U, N, dev, ms_full):
+    """Measured per-rank critical path of the row-sharded cfg4 at N = 2, 4, 8 on this one GPU: the
+    local stages of one rank (its w/N rows: Gram, chain + P, apply) timed with CUDA events, plus an
+    ASSUMED Gram all-reduce (not measurable on one GPU: 16.8 MB fp32, ring/NVLS bus bandwidth of
+    700 GB/s + 15 us latency).  Projected efficiency = T_1 / (N * T_N)."""
+    import torch
+    from paper_2602_02500_b200 import distributed as D
+    out = {}
+    rows = work.x.shape[0]
+    h = work.h
+    ar_bytes = 4.0 * h * h
+    for n in (2, 4, 8):
+        xs = work.x[: rows // n]
+        ys = torch.empty_like(xs)
+        for _ in range(3):
+            U.orthogonalize(xs, work.spec, out=ys, check=False)
+        torch.cuda.synchronize()
+        reps = 20
+        with N.StageProfiler(reps) as prof:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                U.orthogonalize(xs, work.spec, out=ys, check=False)
+            e1.record()
+            torch.cuda.synchronize()
+            st = prof.read().mean(axis=0)
+        t_local = e0.elapsed_time(e1) / reps
+        t_ar = 1e3 * (2.0 * (n - 1) / n * ar_bytes / 700e9) + 0.015
+        t_n = t_local + t_ar
+        out[str(n)] = {"rows_per_rank": rows // n, "local_ms": t_local,
+                       "stages_ms": {k: float(v) for k, v in zip(N.PROFILE_STAGES, st)},
+                       "allreduce_ms_assumed": t_ar, "critical_path_ms": t_n,
+                       "projected_efficiency": ms_full / (n * t_n)}
+    del D
+    return out
 
 
 if __name__ == "__main__":

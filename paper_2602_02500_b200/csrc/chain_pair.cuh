@@ -439,12 +439,13 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
 template <class Epi>
 inline cudaError_t launch_chain_pair_f8(const SymMapsF8& maps, const UmmaWork& w, const Epi& epi,
                                         cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceFlag configured;
+  const int cfg_dev = PerDeviceFlag::current();
+  if (!configured.test(cfg_dev)) {
     cudaError_t e =
         cudaFuncSetAttribute(chain_pair_f8_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, F8_SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.set(cfg_dev);
   }
   if (w.num_work <= 0) return cudaSuccess;
   const int pairs = device_sm_count() / 2;
@@ -466,11 +467,12 @@ inline cudaError_t launch_chain_pair_f8(const SymMapsF8& maps, const UmmaWork& w
 
 template <class Epi>
 inline cudaError_t launch_chain_pair(const SymMaps& maps, const UmmaWork& w, const Epi& epi, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceFlag configured;
+  const int cfg_dev = PerDeviceFlag::current();
+  if (!configured.test(cfg_dev)) {
     cudaError_t e = cudaFuncSetAttribute(chain_pair_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, SC_SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.set(cfg_dev);
   }
   if (w.num_work <= 0) return cudaSuccess;
   const int pairs = device_sm_count() / 2;

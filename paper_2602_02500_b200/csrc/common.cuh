@@ -1,10 +1,36 @@
 // Shared device helpers: element loads/stores by dtype, bf16 hi/lo split, reductions.
 #pragma once
+#include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace unso {
+
+// Kernel attributes (the dynamic shared-memory opt-in) and occupancy are per device: one flag bit
+// per device ordinal, so a process driving several GPUs configures every one of them.
+struct PerDeviceFlag {
+  std::atomic<unsigned long long> bits{0};
+  static int current() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+  }
+  bool test(int d) const { return (bits.load(std::memory_order_acquire) >> d) & 1ull; }
+  void set(int d) { bits.fetch_or(1ull << d, std::memory_order_acq_rel); }
+};
+
+// Developer A/B overrides (routes, recipes) are read from the environment only in builds with
+// -DUNSO_DEVELOPER_OVERRIDES; the shipped library ignores them.
+inline const char* dev_override(const char* name) {
+#ifdef UNSO_DEVELOPER_OVERRIDES
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 enum Dtype : int { DT_F32 = 0, DT_BF16 = 1, DT_F64 = 2 };
 

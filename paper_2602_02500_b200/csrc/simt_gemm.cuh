@@ -308,12 +308,13 @@ template <int DTA, int DTB, class Epi>
 inline cudaError_t launch_dmma(const SimtOperand& A, const SimtOperand& B, int M, int N, int K, int batch, bool syrk,
                                int splits, const Epi& epi, cudaStream_t stream, int tm, int tn, int tiles) {
   constexpr int smem = DMMA_STAGES * (DmmaLayout<DTA>::BYTES + DmmaLayout<DTB>::BYTES);
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceFlag configured;
+  const int cfg_dev = PerDeviceFlag::current();
+  if (!configured.test(cfg_dev)) {
     const cudaError_t e =
         cudaFuncSetAttribute(dmma_gemm_kernel<DTA, DTB, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.set(cfg_dev);
   }
   dim3 grid(tiles, splits, batch);
   dmma_gemm_kernel<DTA, DTB, Epi><<<grid, 128, smem, stream>>>(A, B, M, N, K, syrk ? 1 : 0, tm, tn, splits, epi);

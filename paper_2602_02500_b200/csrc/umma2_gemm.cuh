@@ -287,12 +287,13 @@ inline cudaError_t launch_umma2(const CUtensorMap& a0, const CUtensorMap& a1, co
                                 const CUtensorMap& b1, const UmmaWork& w, const Epi& epi, cudaStream_t stream) {
   constexpr int smem = Cfg::SMEM + (epi_has_rows4<Epi>::value ? Cfg::EPI_WARPS * 4096 : 0);
   static_assert(smem <= 227 * 1024, "smem budget with the epilogue staging blocks");
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceFlag configured;
+  const int cfg_dev = PerDeviceFlag::current();
+  if (!configured.test(cfg_dev)) {
     cudaError_t e = cudaFuncSetAttribute(umma2_gemm_kernel<Cfg, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.set(cfg_dev);
   }
   if (w.num_work <= 0) return cudaSuccess;
   const int pairs = device_sm_count() / 2;

@@ -274,12 +274,13 @@ inline UmmaWork umma_make_work(int M, int N, int K, int BN, int batch, bool syrk
 template <class Cfg, class Epi>
 inline cudaError_t launch_umma(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
                                const CUtensorMap& b1, const UmmaWork& w, const Epi& epi, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceFlag configured;
+  const int cfg_dev = PerDeviceFlag::current();
+  if (!configured.test(cfg_dev)) {
     cudaError_t e = cudaFuncSetAttribute(umma_gemm_kernel<Cfg, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.set(cfg_dev);
   }
   if (w.num_work <= 0) return cudaSuccess;
   const int sms = device_sm_count();

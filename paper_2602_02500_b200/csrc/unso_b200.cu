@@ -409,7 +409,7 @@ using Cfg2ApplyWide1 = Umma2Cfg<256, 1, 1, 1, TERM(0, 0, 0), false, true, 6>;
 static bool use_pair_engine() {
   static int v = -1;
   if (v < 0) {
-    const char* e = std::getenv("UNSO_ENGINE");
+    const char* e = dev_override("UNSO_ENGINE");
     v = (e && std::strcmp(e, "1cta") == 0) ? 0 : 1;
   }
   return v == 1;
@@ -705,7 +705,7 @@ static int scal_mode(int scaling) {
 // Returns false when the problem does not qualify (the caller then runs the per-step launches).
 static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, const double* G, int32_t* status,
                                  cudaStream_t st) {
-  static const bool no_f64_chain = std::getenv("UNSO_NO_F64_CHAIN") != nullptr;  // developer override, read once
+  static const bool no_f64_chain = dev_override("UNSO_NO_F64_CHAIN") != nullptr;  // developer override, read once
   // rows are pulled with 16-byte-granular bulk copies: h must be even
   if (p.h > CF_MAX_H || (p.h & 1) || p.order < 2 || p.order > CHAIN_MAX_ORDER ||
       p.scaling == UNSO_SCALING_GELFAND || no_f64_chain)
@@ -714,14 +714,15 @@ static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, con
   const int T = cf_tile(h);
   const int smem = cf_smem_bytes(h, T);
   auto kernel = T == 16 ? chain_f64_kernel<16> : chain_f64_kernel<32>;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceFlag configured;
+  const int cfg_dev = PerDeviceFlag::current();
+  if (!configured.test(cfg_dev)) {
     if (cudaFuncSetAttribute(chain_f64_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              cf_smem_bytes(128, 16)) != cudaSuccess ||
         cudaFuncSetAttribute(chain_f64_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              cf_smem_bytes(CF_MAX_H, 32)) != cudaSuccess)
       return false;
-    configured = true;
+    configured.set(cfg_dev);
   }
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem) != cudaSuccess || per_sm < 1)
@@ -922,8 +923,8 @@ static int32_t gram_bf16_split(const Problem& p, const Plan& pl, void* ws, const
 
 constexpr int CHAIN_HI_ONLY_STEPS = 3;
 // developer overrides (A/B timing and precision): cross terms in every squaring; another count
-static const bool g_dev_cross_all = std::getenv("UNSO_CHAIN_CROSS_ALL") != nullptr;
-static const int g_dev_hi_only = std::getenv("UNSO_CHAIN_HI_ONLY_STEPS") ? std::atoi(std::getenv("UNSO_CHAIN_HI_ONLY_STEPS")) : -1;
+static const bool g_dev_cross_all = dev_override("UNSO_CHAIN_CROSS_ALL") != nullptr;
+static const int g_dev_hi_only = dev_override("UNSO_CHAIN_HI_ONLY_STEPS") ? std::atoi(dev_override("UNSO_CHAIN_HI_ONLY_STEPS")) : -1;  // clamped at use
 
 // Multi-launch pipeline for large h (multi_chain.cuh): scalars from the norm partials, N-1 CTA-pair
 // squaring steps (the first folds C_1 = G/s^2 and initialises P, the last emits P statistics),
@@ -949,7 +950,7 @@ static int32_t scale_chain_bf16_glue_free(const Problem& p, const Plan& pl, void
   // (tools/chain_precision_emulation.py: 2.6-2.7e-3 -> 2.7-3.3e-3 on the cfg2/3/5-like spectra;
   // dropping them in the LAST step instead gives 2-7e-2).
   const int hi_only_steps =
-      (f8 && N >= 12 && !g_dev_cross_all) ? (g_dev_hi_only >= 0 ? g_dev_hi_only : CHAIN_HI_ONLY_STEPS) : 0;
+      (f8 && N >= 12 && !g_dev_cross_all) ? (g_dev_hi_only >= 0 ? std::min(g_dev_hi_only, N - 1) : CHAIN_HI_ONLY_STEPS) : 0;
   int cur = 0;
   bool p_pending = false;
   for (int k = 1; k < N; ++k) {
@@ -1137,7 +1138,11 @@ static int32_t scale_chain_bf16_multi(const Problem& p, const Plan& pl, void* ws
 // Can the fused persistent chain run (all tiles co-resident, order and scaling supported)?
 static bool chain_persistent_fits(const Problem& p) {
   if (p.order < 1 || p.order > CHAIN_MAX_ORDER || p.scaling == UNSO_SCALING_GELFAND) return false;
-  static int max_blocks_per_sm = -1;
+  static int max_blocks[64] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
+                                -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
+                                -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
+                                -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+  int& max_blocks_per_sm = max_blocks[PerDeviceFlag::current()];
   if (max_blocks_per_sm < 0) {
     if (cudaFuncSetAttribute(chain_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CH_SMEM) !=
         cudaSuccess)
@@ -1252,7 +1257,7 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
 
 // h <= 128: one CTA per matrix, the chain entirely on chip (chain_small.cuh).
 static bool chain_small_fits(const Problem& p) {
-  static const bool no_small_chain = std::getenv("UNSO_NO_SMALL_CHAIN") != nullptr;  // developer override
+  static const bool no_small_chain = dev_override("UNSO_NO_SMALL_CHAIN") != nullptr;  // developer override
   return p.h <= 128 && p.order >= 1 && p.order <= CHAIN_MAX_ORDER && p.scaling != UNSO_SCALING_GELFAND &&
          !no_small_chain;
 }
@@ -1262,14 +1267,15 @@ static bool chain_small_fits(const Problem& p) {
 static int32_t scale_chain_bf16_small(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
                                       int64_t part_ld, int64_t part_mat, int32_t* status, cudaStream_t st,
                                       const __nv_bfloat16* xb = nullptr, int64_t ldx = 0, int64_t bsx = 0) {
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceFlag configured;
+  const int cfg_dev = PerDeviceFlag::current();
+  if (!configured.test(cfg_dev)) {
     if (cudaFuncSetAttribute(chain_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CS_SMEM) !=
             cudaSuccess ||
         cudaFuncSetAttribute(chain_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CS_SMEM) !=
             cudaSuccess)
       return UNSO_ERR_CUDA;
-    configured = true;
+    configured.set(cfg_dev);
   }
   ChainParams cp = chain_params(p, pl, ws, part, splits, part_ld, part_mat, status);
   SmallGram sg;
@@ -1298,7 +1304,7 @@ static int32_t scale_chain_bf16_small(const Problem& p, const Plan& pl, void* ws
 
 // tall bf16 X with h <= 128 and few enough rows that one CTA per matrix does the Gram too
 static bool small_fused_gram(const Problem& p) {
-  static const bool no_fused = std::getenv("UNSO_NO_FUSED_SMALL_GRAM") != nullptr;  // developer override
+  static const bool no_fused = dev_override("UNSO_NO_FUSED_SMALL_GRAM") != nullptr;  // developer override
   return chain_small_fits(p) && p.tall && p.w <= 8192 && use_pair_engine() &&
          !no_fused;
 }
@@ -1306,7 +1312,7 @@ static bool small_fused_gram(const Problem& p) {
 // Which scale+chain implementation a BF16 UNSO problem takes.
 enum Bf16Route { ROUTE_SMALL, ROUTE_PERSISTENT, ROUTE_GLUE_FREE, ROUTE_LEGACY };
 static Bf16Route bf16_route(const Problem& p) {
-  static const char* const route_override = std::getenv("UNSO_BF16_ROUTE");  // developer override (A/B timing)
+  static const char* const route_override = dev_override("UNSO_BF16_ROUTE");  // developer override (A/B timing)
   if (const char* f = route_override) {
     if (!std::strcmp(f, "glue") && use_pair_engine() && p.order >= 2 && p.scaling != UNSO_SCALING_GELFAND)
       return ROUTE_GLUE_FREE;

@@ -205,12 +205,20 @@ class NvlinkGramReducer:
 
 
 _REDUCERS: dict = {}
+_SPLITS: dict = {}
 
 
 def _nvlink_reducer(h: int, w_local: int, group, device) -> NvlinkGramReducer:
-    wmin = torch.tensor([w_local], dtype=torch.int64, device=device)
-    dist.all_reduce(wmin, op=dist.ReduceOp.MIN, group=group)
-    splits = gram_push_splits(h, int(wmin.item()))
+    """The cached reducer for this (h, local rows).  The split count must be the same on every rank
+    (it is derived from the smallest shard), which costs one MIN all-reduce + host read -- done once
+    per (h, local rows, group, device), not per call: calls run in lockstep on every rank, so every
+    rank meets a new shape in the same call and the collective stays matched."""
+    skey = (h, w_local, id(group), device)
+    splits = _SPLITS.get(skey)
+    if splits is None:
+        wmin = torch.tensor([w_local], dtype=torch.int64, device=device)
+        dist.all_reduce(wmin, op=dist.ReduceOp.MIN, group=group)
+        splits = _SPLITS[skey] = gram_push_splits(h, int(wmin.item()))
     key = (h, splits, id(group), device)
     if key not in _REDUCERS:
         _REDUCERS[key] = NvlinkGramReducer.symmetric(h, splits, group, device)

@@ -148,22 +148,32 @@ class Muon(torch.optim.Optimizer):
         p0 = items[0]
         dev, n, numel = p0.device, len(items), rows * cols
         dt = N.DTYPE_BF16 if p0.dtype == torch.bfloat16 else N.DTYPE_F32
-        key = tuple((p.grad.data_ptr(), self.state[p]["momentum_buffer"].data_ptr(), p.data_ptr()) for p in items)
+        # Parameter and momentum-buffer addresses are stable across steps: their device pointer
+        # lists are cached.  Gradients are usually reallocated every step (zero_grad(set_to_none=True)),
+        # so their list goes through a reused pinned staging buffer and a non-blocking copy.
+        key = tuple((self.state[p]["momentum_buffer"].data_ptr(), p.data_ptr()) for p in items)
         cache = self.__dict__.setdefault("_ptr_lists", {})
-        ptrs = cache.get(key)
-        if ptrs is None:  # device pointer lists, rebuilt only when a tensor moved (e.g. grads set to None)
-            ptrs = torch.tensor(list(zip(*key)), dtype=torch.int64).to(dev)
+        ent = cache.get(key)
+        if ent is None:
+            stable = torch.tensor(list(zip(*key)), dtype=torch.int64).to(dev)
+            ent = (stable, torch.empty(n, dtype=torch.int64, pin_memory=True),
+                   torch.empty(n, dtype=torch.int64, device=dev), torch.cuda.Event())
             if len(cache) > 64:
                 cache.clear()
-            cache[key] = ptrs
+            cache[key] = ent
+        stable, g_host, g_dev, g_ready = ent
+        g_ready.synchronize()  # the previous step's copy out of the staging buffer has finished
+        g_host.numpy()[:] = [p.grad.data_ptr() for p in items]
+        g_dev.copy_(g_host, non_blocking=True)
+        g_ready.record(torch.cuda.current_stream(dev))
         stacked = torch.empty((n, rows, cols), dtype=p0.dtype, device=dev)
         maxabs = torch.empty(n, dtype=torch.float32, device=dev)
         stream = torch.cuda.current_stream(dev).cuda_stream
         lib = N.lib()
-        N.check(lib.unso_muon_prepare(n, ptrs[0].data_ptr(), ptrs[1].data_ptr(), stacked.data_ptr(), numel, dt,
+        N.check(lib.unso_muon_prepare(n, g_dev.data_ptr(), stable[0].data_ptr(), stacked.data_ptr(), numel, dt,
                                       float(mu), 1 if nesterov else 0, maxabs.data_ptr(), stream), "unso_muon_prepare")
         ortho = self._orthogonalize_group(stacked).contiguous()
-        N.check(lib.unso_muon_update(n, ptrs[2].data_ptr(), ortho.data_ptr(), numel, dt, maxabs.data_ptr(),
+        N.check(lib.unso_muon_update(n, stable[1].data_ptr(), ortho.data_ptr(), numel, dt, maxabs.data_ptr(),
                                      float(decay), float(alpha), stream), "unso_muon_update")
 
 

@@ -471,7 +471,12 @@ def preprocess(m: torch.Tensor, scaling: Scaling, counter: FlopsCounter | None =
             counter.record_matmul(h, w, h)
     a = m.transpose(-1, -2) if tall else m
     shape = (-1, 1, 1) if m.dim() == 3 else ()
-    x = (a.to(torch.float64) / denom.view(shape)).to(m.dtype).contiguous()
+    # The reference keeps the rescaled copy in fp64 (ortho.py:167).  A bf16 input is returned as
+    # fp32 (exact: bf16 x fp64 scale rounded once to fp32, 24 significant bits) so that
+    # unso(preprocess(x)) computes on the same values as the fused orthogonalize path instead of a
+    # twice-rounded bf16 copy; fp32 / fp64 inputs keep their dtype.
+    out_dtype = torch.float32 if m.dtype == torch.bfloat16 else m.dtype
+    x = (a.to(torch.float64) / denom.view(shape)).to(out_dtype).contiguous()
     return x, tall
 
 

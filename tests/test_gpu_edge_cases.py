@@ -301,3 +301,17 @@ def test_side_streams_run_concurrently_and_match():
     for ya, yb in outs:
         assert torch.equal(ya, ref_a)
         assert torch.equal(yb, ref_b)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_two_step_api_on_bf16_input(precision):
+    """unso(preprocess(x)) on a bf16 tall input: preprocess returns the rescaled, transposed copy in
+    fp32 (the reference keeps it in fp64, ortho.py:167), not a second bf16 rounding, so the fp32
+    mode reaches 1e-5 of the oracle on the bf16 values and the bf16 mode stays within its bar."""
+    x = gaussian((1000, 300), 77).to(torch.bfloat16)
+    xs, tall = U.preprocess(x, U.Scaling.FROBENIUS_GRAM)
+    assert tall and xs.dtype == torch.float32 and xs.shape == (300, 1000)
+    y = U.unso(xs, U.default_coefficients(), precision=precision)
+    ref = O.run(x.double().cpu().numpy(), "unso")["y"].T
+    r = rel(y.double().cpu().numpy(), ref)
+    assert r <= TOL[precision], (precision, r)
