@@ -909,39 +909,46 @@ def parallelism_name(wl, world, multi, collective):
 
 
 def shard_projection(work, U, N, dev, ms_full):
-    """Measured per-rank critical path of the row-sharded cfg4 at N = 2, 4, 8 on this one GPU: the
-    local stages of one rank (its w/N rows: Gram, chain + P, apply) timed with CUDA events, plus an
-    ASSUMED Gram all-reduce (not measurable on one GPU: 16.8 MB fp32, ring/NVLS bus bandwidth of
-    700 GB/s + 15 us latency).  Projected efficiency = T_1 / (N * T_N)."""
+    """Measured per-rank critical path of the row-sharded cfg4 at N = 2, 4, 8 on this one GPU: one
+    rank's stages on its w/N rows exactly as orthogonalize_row_sharded runs them -- the local Gram
+    (unso_gram), then scale + chain + apply from the GLOBAL Gram (unso_orthogonalize_from_gram; the
+    all-reduce's result is stood in for by the full matrix's Gram, so the scale, truncation and apply
+    decision are the full problem's) -- timed with CUDA events, plus an ASSUMED Gram all-reduce
+    (not measurable on one GPU: 16.8 MB fp32, 700 GB/s bus bandwidth + 15 us latency).
+    Projected efficiency = T_1 / (N * T_N)."""
     import torch
     from paper_2602_02500_b200 import distributed as D
     out = {}
     rows = work.x.shape[0]
     h = work.h
+    g_full = D.native_gram(work.x, work.spec, None)
     ar_bytes = 4.0 * h * h
     for n in (2, 4, 8):
         xs = work.x[: rows // n]
         ys = torch.empty_like(xs)
-        for _ in range(3):
-            U.orthogonalize(xs, work.spec, out=ys, check=False)
-        torch.cuda.synchronize()
+        gbuf = torch.empty_like(g_full)
         reps = 20
-        with N.StageProfiler(reps) as prof:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_g, t_f = 0.0, 0.0
+        for it in range(reps + 3):
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record()
-            for _ in range(reps):
-                U.orthogonalize(xs, work.spec, out=ys, check=False)
+            g = D.native_gram(xs, work.spec, None)
             e1.record()
+            gbuf.copy_(g_full)  # the all-reduce's result (not timed; the all-reduce is assumed below)
+            e2.record()
+            D.native_finish(xs, gbuf, work.spec, None, ys)
+            e3 = torch.cuda.Event(enable_timing=True)
+            e3.record()
             torch.cuda.synchronize()
-            st = prof.read().mean(axis=0)
-        t_local = e0.elapsed_time(e1) / reps
+            del g
+            if it >= 3:
+                t_g += e0.elapsed_time(e1) / reps
+                t_f += e2.elapsed_time(e3) / reps
         t_ar = 1e3 * (2.0 * (n - 1) / n * ar_bytes / 700e9) + 0.015
-        t_n = t_local + t_ar
-        out[str(n)] = {"rows_per_rank": rows // n, "local_ms": t_local,
-                       "stages_ms": {k: float(v) for k, v in zip(N.PROFILE_STAGES, st)},
+        t_n = t_g + t_f + t_ar
+        out[str(n)] = {"rows_per_rank": rows // n, "gram_ms": t_g, "chain_and_apply_ms": t_f,
                        "allreduce_ms_assumed": t_ar, "critical_path_ms": t_n,
                        "projected_efficiency": ms_full / (n * t_n)}
-    del D
     return out
 
 

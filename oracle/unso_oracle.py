@@ -23,7 +23,8 @@ __all__ = [
     "axpy_cost", "model_flops", "ContractionLog",
     "scale_and_orient", "unso_poly", "cubic_ns", "quintic_ns",
     "muon_rows", "cesista_rows", "run", "ortho_error", "ortho_error_any",
-    "composed_map", "haar_columns", "controlled_spectrum_matrix",
+    "composed_map", "haar_columns", "controlled_spectrum_matrix", "unso_sampled", "quintic_sampled",
+    "unso_rows_of_tall",
 ]
 
 # ---------------------------------------------------------------------------
@@ -390,6 +391,62 @@ def unso_rows_of_tall(m: np.ndarray, rows: np.ndarray, order: int = DEFAULT_ORDE
         bk = bk @ bk
     p = p + b * bk
     return (m[rows] / denom) @ p
+
+
+
+def _oriented(m: np.ndarray):
+    """Row-wide orientation of preprocess (ortho.py:149-150): transpose iff rows > cols."""
+    tall = m.shape[0] > m.shape[1]
+    return (np.ascontiguousarray(m.T) if tall else np.asarray(m, dtype=np.float64)), tall
+
+
+def unso_sampled(m: np.ndarray, idx, order: int = DEFAULT_ORDER, a=DEFAULT_A, rule: str = DEFAULT_RULE,
+                 scaling: str = "gram") -> np.ndarray:
+    """orthogonalize(m, UNSO) restricted to long-side indices `idx`, any orientation: rows idx of
+    Y for a tall m, columns idx of Y for a wide or square m.  Same operations as the reference
+    (ortho.py:140-205): gram / plain scale (:153-157), B_1 = I - G (:199), P += a_k B_k,
+    B <- B B (:201-203), P += b B_N (:204), Y = P X (:205) -- with P applied only to the requested
+    long-side columns of X (each column of P X depends on that column of X alone).  For
+    full-size parity checks of BASELINE configs[2]-[4] where forming all of Y is unnecessary."""
+    x, tall = _oriented(m)
+    g = x @ _T(x)                                               # ortho.py:156 (the Gram of A)
+    if scaling == "gram":
+        denom = float(np.sqrt(float(np.sqrt(np.sum(g * g)))))   # ortho.py:157
+    elif scaling == "plain":
+        denom = float(np.sqrt(float(np.sum(x * x))))             # ortho.py:153-154
+    else:
+        raise ValueError("unso_sampled supports gram and plain scaling")
+    g = g / (denom * denom)                                     # == (x/denom)(x/denom)^T up to rounding
+    b = final_coefficient(order, a, rule)
+    h = g.shape[0]
+    bk = np.eye(h) - g
+    p = np.eye(h)
+    for k in range(1, order):
+        p = p + float(a[k - 1]) * bk
+        bk = bk @ bk
+    p = p + b * bk
+    y = p @ (x[:, idx] / denom)                                 # columns idx of P X
+    return np.ascontiguousarray(y.T) if tall else y
+
+
+def quintic_sampled(m: np.ndarray, idx, rows=None) -> np.ndarray:
+    """The quintic NS iteration (_quintic_steps ortho.py:221-231 after plain scaling, :153-154)
+    restricted to long-side indices `idx` (rows of Y if tall, else columns).  Every iterate is
+    X_k = M_k X_0 with M_k a polynomial in G_0 = X_0 X_0^T, so G_k = M_k G_0 M_k and
+    M_{k+1} = (a I + b G_k + c G_k^2) M_k: the same map in h x h arithmetic (exact restatement;
+    pinned against quintic_ns on small cases by tests/test_oracle_golden.py), then Y = M_T X_0."""
+    if rows is None:
+        rows = muon_rows(MUON_DEFAULT_ITERS)
+    x, tall = _oriented(m)
+    x = x / float(np.sqrt(float(np.sum(x * x))))
+    g0 = x @ _T(x)
+    h = g0.shape[0]
+    mk = np.eye(h)
+    for ac, bc, cc in np.asarray(rows, dtype=np.float64):
+        gk = mk @ g0 @ mk
+        mk = (float(ac) * np.eye(h) + float(bc) * gk + float(cc) * (gk @ gk)) @ mk
+    y = mk @ x[:, idx]
+    return np.ascontiguousarray(y.T) if tall else y
 
 
 # ---------------------------------------------------------------------------

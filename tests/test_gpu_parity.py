@@ -558,6 +558,12 @@ def test_nvlink_gram_reduction_emulated_ranks(h, world):
     y = torch.cat([native_finish(s, gs[r].clone(), spec, "bf16")[0] for r, s in enumerate(shards)])
     full = U.orthogonalize(x, spec, precision="bf16").y
     torch.cuda.synchronize()
+    # against the oracle (ortho.py:140-205 on the same bf16 values), on rows of every rank's shard
+    rows = np.arange(0, w, 3)
+    ref = O.unso_rows_of_tall(x.double().cpu().numpy(), rows)
+    r_or = rel(y.double().cpu().numpy()[rows], ref)
+    print(f"nvlink-reduced h={h} world={world}: vs oracle rows {r_or:.2e}")
+    assert r_or <= TOL["bf16"] + 2.0 ** -9
     assert rel(y.double().cpu().numpy(), full.double().cpu().numpy()) <= 5e-3
 
 

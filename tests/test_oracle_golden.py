@@ -106,3 +106,23 @@ def test_degenerate_and_shape_errors():
         O.run(np.zeros((4, 8)), "unso")
     with pytest.raises(ValueError, match="shape"):
         O.unso_poly(np.ones((4, 2)))
+
+
+def test_sampled_restatements_match_the_full_oracle():
+    """unso_sampled / quintic_sampled (long-side samples for full-size GPU parity) equal the
+    op-for-op oracle on tall, wide and square inputs."""
+    rng = np.random.default_rng(3)
+    for shape in ((96, 40), (40, 96), (50, 50)):
+        m = rng.standard_normal(shape)
+        long = max(shape)
+        idx = np.sort(rng.choice(long, 17, replace=False))
+        tall = shape[0] > shape[1]
+        for scaling in ("gram", "plain"):
+            full = O.run(m, "unso", scaling=scaling)["y"]
+            got = O.unso_sampled(m, idx, scaling=scaling)
+            want = full[idx] if tall else full[:, idx]
+            assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max()), (shape, scaling)
+        full = O.run(m, "muon", iterations=5)["y"]
+        got = O.quintic_sampled(m, idx)
+        want = full[idx] if tall else full[:, idx]
+        assert np.abs(got - want).max() <= 1e-11 * max(1.0, np.abs(want).max()), shape
