@@ -70,6 +70,10 @@ typedef enum unso_method { UNSO_METHOD_UNSO = 0, UNSO_METHOD_ORIGINAL_NS = 1, UN
 #define UNSO_FLAG_NS_SINGLE_STATE 0x10 /* NS/Muon, BF16: round the fp32 state to one bf16 term in its
                                           long-side products (1 + 2 instead of 3 + 3 bf16 products per
                                           step; ~1e-2 instead of ~1e-4 from the fp64 result). */
+#define UNSO_FLAG_FP32_DMMA 0x20        /* UNSO, FP32, h > 256: run the Gram, the squarings and the apply on the
+                                           fp64 DMMA engine instead of the default int8 tensor-core split
+                                           (5 int8 digits per operand, 15 exact int8 products per contraction,
+                                           fp64 combination; ~1e-7 from the fp64 reference). */
 #define UNSO_FLAG_NO_TRUNCATION 0x8     /* UNSO, BF16: run all N-1 squarings.  Default: the persistent chain
                                            (h <= ~1900 per co-resident batch) stops before step k once every
                                            matrix has sum_{j>k}|c_j| * ||I - C_k||_F^2 <= 2^-12 and subtracts

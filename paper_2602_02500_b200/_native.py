@@ -43,6 +43,7 @@ FLAG_TWO_TERM_APPLY = 0x2
 FLAG_NO_TRUNCATION = 0x8
 FLAG_CHAIN_BF16X3 = 0x4
 FLAG_NS_SINGLE_STATE = 0x10
+FLAG_FP32_DMMA = 0x20
 PROFILE_STAGES = ("convert", "gram", "scale_prep", "chain", "finalize_p", "apply")
 
 

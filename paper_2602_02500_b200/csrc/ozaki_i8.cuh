@@ -1,0 +1,510 @@
+// fp64-grade products on the int8 tensor cores (tcgen05.mma kind::i8) for the fp32 mode: an
+// Ozaki-style split of both operands into OZ_S signed int8 digits.
+//
+// Reference contractions carried: the Gram densemat.matmul(a, transpose(a)) (ortho.py:156, 198), the
+// squarings B_{k+1} = B_k B_k (ortho.py:201-203, run in the C-form C' = 2C - C^2) and the apply
+// P(A) . X (ortho.py:205) -- all computed by the reference in numpy float64.
+//
+// Split (oz_split_kernel): every operand row r (the contraction runs along the row) is scaled by
+// 2^-e_r, e_r = the frexp exponent of the row's max |a|, so |a 2^-e_r| < 1, and written as
+//   a = 2^e_r * sum_{s=1..S} d_s 2^-(6 + 7(s-1)),   d_1 = rint(64 r), d_{s+1} = rint(128 (r_s - d_s))
+// with every |d_s| <= 64 (the remainder after round-to-nearest is within +-1/2).  The product keeps
+// the digit pairs with s + t <= S + 1 (S(S+1)/2 int8 GEMMs, exact int32 sums); pairs with the same
+// s + t share one TMEM accumulator, so the epilogue combines S accumulators in fp64:
+//   (A B^T)_mn = 2^(e_m + e_n - 12) * sum_{g=0..S-1} acc_g(m, n) 2^(-7 g).
+// The dropped pairs bound the error at ~2^-(6 + 7S) relative to (row max x column max x K); S = 5
+// keeps the whole UNSO pipeline within 1.5e-7 (configs[1]) / 2.6e-7 (configs[4]-like Pareto
+// spectrum) of the fp64 oracle (tools/ozaki_emulation.py, an exact emulation of this scheme).
+// int32 bound: a group holds <= S products of |d_s d_t| <= 4096, so K <= OZ_MAX_K per split-K slice.
+//
+// Engine: one persistent CTA per SM, 128 x 64 output tiles, K staged 64 bytes at a time with all S
+// digit planes of A (S x 8 KB) and of B (S x 4 KB) in one 4-D TMA box each (SWIZZLE_64B), 3 stages;
+// warp 0 TMA, warp 1 MMA (15 products x 2 k-steps per stage into S accumulators of 64 columns),
+// warp 2 TMEM, warps 4..7 epilogue (drain + fp64 combination, exponents, coalesced block functors).
+#pragma once
+#include "common.cuh"
+#include "ptx_sm100.cuh"
+#include "simt_gemm.cuh"
+
+namespace unso {
+
+constexpr int OZ_S = 5;                       // digits per operand
+constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 64;  // BK in int8 elements (= bytes)
+constexpr int OZ_STAGES = 3;
+constexpr int OZ_A_TILE = OZ_BM * OZ_BK;       // 8 KB per digit plane
+constexpr int OZ_B_TILE = OZ_BN * OZ_BK;       // 4 KB
+constexpr int OZ_STAGE_BYTES = OZ_S * (OZ_A_TILE + OZ_B_TILE);
+constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE_BYTES + 1024 + 4 * 32 * 33 * 8 + 1024;  // stages, barriers, staging
+constexpr uint32_t OZ_TMEM_COLS = 512;         // OZ_S * OZ_BN = 320 used
+constexpr int64_t OZ_MAX_K = 65536;            // 5 * 64 * 64 * 65536 < 2^31
+static_assert(OZ_S * OZ_BN <= 512, "tmem");
+static_assert(OZ_SMEM <= 227 * 1024, "smem");
+
+// kind::i8: s8 x s8 -> s32 (c_format 2, a/b format 1 = signed), K-major operands.
+__host__ __device__ constexpr uint32_t idesc_s8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_s8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* m, uint64_t* bar, void* smem_dst, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// Row scale exponent from the row's max |a| (as the u64 bits of a non-negative double): the frexp
+// exponent, so |a| 2^-e < 1.  0 for an all-zero row.  Split kernel and epilogue use the same rule.
+__device__ __forceinline__ int oz_exponent(unsigned long long maxbits) {
+  const double m = __longlong_as_double(static_cast<long long>(maxbits));
+  return m > 0.0 ? ilogb(m) + 1 : 0;
+}
+
+// ---------------------------------------------------------------- max |a| per operand row
+// Per source row (one warp per row): out[b * out_bs + r] = bits of max_c |src[b][r][c]|.
+__global__ void oz_rowmax_kernel(const void* __restrict__ src, int dt, int64_t ld, int64_t bs, int64_t rows,
+                                 int64_t cols, int batch, unsigned long long* __restrict__ out, int64_t out_bs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int b = blockIdx.y;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += nw) {
+    double m = 0.0;
+    bool bad = false;
+    for (int64_t c = lane; c < cols; c += 32) {
+      const double v = fabs(load_as_f64(src, b * bs + r * ld + c, dt));
+      bad |= !(v <= 1.7976931348623157e308);  // NaN or Inf
+      m = fmax(m, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      bad |= __shfl_xor_sync(0xffffffffu, bad ? 1 : 0, o) != 0;
+    }
+    if (lane == 0) out[b * out_bs + r] = static_cast<unsigned long long>(__double_as_longlong(bad ? __longlong_as_double(0x7FF8000000000000ll) : m));
+  }
+  (void)batch;
+}
+
+// Per source column: out[b * out_bs + c] = bits of max_r |src[b][r][c]| (out zeroed beforehand;
+// non-negative doubles order like their bit patterns, NaN 0x7FF8.. above every finite value).
+__global__ void oz_colmax_kernel(const void* __restrict__ src, int dt, int64_t ld, int64_t bs, int64_t rows,
+                                 int64_t cols, unsigned long long* __restrict__ out, int64_t out_bs, int rows_per_block) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int b = blockIdx.z;
+  if (c >= cols) return;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
+  const int64_t r1 = r0 + rows_per_block < rows ? r0 + rows_per_block : rows;
+  double m = 0.0;
+  bool bad = false;
+  for (int64_t r = r0; r < r1; ++r) {
+    const double v = fabs(load_as_f64(src, b * bs + r * ld + c, dt));
+    bad |= !(v <= 1.7976931348623157e308);
+    m = fmax(m, v);
+  }
+  const unsigned long long bits =
+      bad ? 0x7FF8000000000000ull : static_cast<unsigned long long>(__double_as_longlong(m));
+  atomicMax(out + b * out_bs + c, bits);
+}
+
+// ---------------------------------------------------------------- digit planes
+// dst[s][b][R][ldd] (plane stride `plane`, batch stride `dbs`), operand row R of K entries.
+// transpose = 0: operand row = source row (R = rows, K = cols); 1: operand row = source column.
+// Scale exponent of operand row R from maxbits[b * max_bs + R].
+__device__ __forceinline__ void oz_digits(double v, int e, int8_t (&d)[OZ_S]) {
+  double r = ldexp(v, 6 - e);  // 64 * v * 2^-e, |r| < 64
+#pragma unroll
+  for (int s = 0; s < OZ_S; ++s) {
+    const double q = rint(r);
+    d[s] = static_cast<int8_t>(static_cast<int>(q));
+    r = (r - q) * 128.0;
+  }
+}
+
+__global__ void oz_split_kernel(const void* __restrict__ src, int dt, int64_t ld, int64_t bs, int64_t rows,
+                                int64_t cols, int transpose, const unsigned long long* __restrict__ maxbits,
+                                int64_t max_bs, int8_t* __restrict__ dst, int64_t ldd, int64_t dbs, int64_t plane) {
+  __shared__ double tile[32][33];
+  const int b = blockIdx.z;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  if (!transpose) {
+    for (int i = ty; i < 32; i += 8) {
+      const int64_t r = r0 + i, c = c0 + tx;
+      if (r >= rows || c >= cols) continue;
+      const int e = oz_exponent(maxbits[b * max_bs + r]);
+      int8_t d[OZ_S];
+      oz_digits(load_as_f64(src, b * bs + r * ld + c, dt), e, d);
+      const int64_t o = b * dbs + r * ldd + c;
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) dst[s * plane + o] = d[s];
+    }
+  } else {
+    for (int i = ty; i < 32; i += 8) {
+      const int64_t r = r0 + i, c = c0 + tx;
+      tile[i][tx] = (r < rows && c < cols) ? load_as_f64(src, b * bs + r * ld + c, dt) : 0.0;
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+      const int64_t R = c0 + i, k = r0 + tx;  // operand row = source column c0 + i
+      if (R >= cols || k >= rows) continue;
+      const int e = oz_exponent(maxbits[b * max_bs + R]);
+      int8_t d[OZ_S];
+      oz_digits(tile[tx][i], e, d);
+      const int64_t o = b * dbs + R * ldd + k;
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) dst[s * plane + o] = d[s];
+    }
+  }
+}
+
+// One warp per row r of matrix b, the C-form chain bookkeeping fused with the next squaring's split:
+//   mode 0 (C_1):     c = G * (1 / s^2),       P  = alpha I - coef c
+//   mode 1 (C_{k+1}): c = 2 C_k - S (S = C_k^2), P -= coef c
+// writes c to Cn, then (digits != nullptr) the row max and the row's digit planes (re-reading c).
+struct OzStepParams {
+  const double* src;    // G (mode 0) or C_k (mode 1)
+  const double* S;      // mode 1
+  double* Cn;
+  double* P;
+  const double* scal;   // mode 0: per-matrix scalars (S_S2)
+  double alpha, coef;
+  int mode, h;
+  int64_t ld, bs;
+  unsigned long long* maxbits;  // [b * h + r]
+  int8_t* digits;               // [s][b][r][ld] planes (plane stride `plane`, batch stride bs)
+  int64_t plane;
+};
+__global__ void oz_chain_step_kernel(const OzStepParams p) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const double inv_s2 = p.mode == 0 ? 1.0 / p.scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_S2] : 0.0;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.h; r += nw) {
+    const int64_t o0 = static_cast<int64_t>(b) * p.bs + r * p.ld;
+    double m = 0.0;
+    bool bad = false;
+    for (int c = lane; c < p.h; c += 32) {
+      const int64_t o = o0 + c;
+      double cn, pv;
+      if (p.mode == 0) {
+        cn = p.src[o] * inv_s2;
+        pv = (c == r ? p.alpha : 0.0) - p.coef * cn;
+      } else {
+        cn = 2.0 * p.src[o] - p.S[o];
+        pv = p.P[o] - p.coef * cn;
+      }
+      p.Cn[o] = cn;
+      p.P[o] = pv;
+      const double a = fabs(cn);
+      bad |= !(a <= 1.7976931348623157e308);
+      m = fmax(m, a);
+    }
+    if (!p.digits) continue;
+#pragma unroll
+    for (int q = 16; q > 0; q >>= 1) {
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, q));
+      bad |= __shfl_xor_sync(0xffffffffu, bad ? 1 : 0, q) != 0;
+    }
+    const unsigned long long bits =
+        bad ? 0x7FF8000000000000ull : static_cast<unsigned long long>(__double_as_longlong(m));
+    if (lane == 0) p.maxbits[static_cast<int64_t>(b) * p.h + r] = bits;
+    const int e = oz_exponent(bits);
+    __syncwarp();
+    for (int c = lane; c < p.h; c += 32) {
+      int8_t d[OZ_S];
+      oz_digits(p.Cn[o0 + c], e, d);
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) p.digits[s * p.plane + o0 + c] = d[s];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- GEMM / SYRK on the digits
+struct OzWork {
+  int tiles_m, tiles_n, syrk, splits, k_tiles, batch, tiles_per_mat, num_work;
+  int dbg;  // timing experiments only (developer builds): 1 = skip the MMAs, 2 = skip the TMA loads
+};
+
+// SYRK (square, BM = 2 BN): tile (tm, tn) is kept when tn >= 2 tm (it touches the upper triangle).
+__device__ __forceinline__ void oz_decode(const OzWork& w, int idx, int& b, int& split, int& tm, int& tn, int& kt0,
+                                          int& kt1) {
+  int t = idx % w.tiles_per_mat;
+  const int r = idx / w.tiles_per_mat;
+  split = r % w.splits;
+  b = r / w.splits;
+  if (w.syrk) {
+    tm = 0;
+    for (;;) {
+      const int n = w.tiles_n - 2 * tm;
+      if (t < n) break;
+      t -= n;
+      ++tm;
+    }
+    tn = 2 * tm + t;
+  } else {
+    constexpr int G = 8;  // row-block groups: the tiles in flight share ~G A row blocks
+    const int per_group = G * w.tiles_n;
+    const int g = t / per_group;
+    const int q = t - g * per_group;
+    const int rows = min(G, w.tiles_m - g * G);
+    tn = q / rows;
+    tm = g * G + (q - tn * rows);
+  }
+  kt0 = static_cast<int>(static_cast<int64_t>(split) * w.k_tiles / w.splits);
+  kt1 = static_cast<int>(static_cast<int64_t>(split + 1) * w.k_tiles / w.splits);
+}
+
+struct OzScales {
+  const unsigned long long* a;  // per A row max bits: a[b * a_bs + m]
+  int64_t a_bs;
+  const unsigned long long* b;  // per B row max bits
+  int64_t b_bs;
+  int M, N;
+};
+
+// 2^k as an exact double for |k| <= 1022 (ldexp beyond: denormal / overflow ranges).
+__device__ __forceinline__ double oz_pow2(int k) {
+  if (k >= -1022 && k <= 1023) return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
+  return ldexp(1.0, k);
+}
+
+// Block functors: blk[r * 33 + c] = D(m0 + r, n0 + c), r, c < 32; `lane` is the caller's lane.
+// Row pass: lanes along n (coalesced row segments); SYRK keeps n >= m.
+#define OZ_ROW_PASS(body)                                           \
+  for (int r = 0; r < 32; ++r) {                                    \
+    const int m = m0 + r, n = n0 + lane;                            \
+    if (m >= M || n >= N || (syrk && n < m)) continue;              \
+    const double v = blk[r * 33 + lane];                            \
+    body;                                                           \
+  }
+
+// Gram split-K partial (fp64), the layout of EpiPartialF64 / finalize_sum_kernel.
+struct OzEpiPartial {
+  double* part;
+  int64_t bs, ld;
+  int batch;
+  __device__ void block(int b, int split, int m0, int n0, const double* blk, int lane, int M, int N, bool syrk) const {
+    double* base = part + (static_cast<int64_t>(split) * batch + b) * bs;
+    OZ_ROW_PASS(base[static_cast<int64_t>(m) * ld + n] = v);
+  }
+};
+
+// Symmetric product S = C C^T (the squaring): upper tile rows, then the mirror through the staging
+// block (lanes along m) -- stores only; oz_chain_step_kernel consumes S row by row.
+struct OzEpiSym {
+  double* out;
+  int64_t ld, bs;
+  __device__ void block(int b, int, int m0, int n0, const double* blk, int lane, int M, int N, bool syrk) const {
+    double* base = out + static_cast<int64_t>(b) * bs;
+    OZ_ROW_PASS(base[static_cast<int64_t>(m) * ld + n] = v);
+    const int m = m0 + lane;
+#pragma unroll 4
+    for (int c = 0; c < 32; ++c) {
+      const int n = n0 + c;
+      if (m < M && n < N && n > m) base[static_cast<int64_t>(n) * ld + m] = blk[lane * 33 + c];
+    }
+  }
+};
+
+// Output in the caller's dtype (the apply).
+struct OzEpiOut {
+  void* out;
+  int dt;
+  int64_t ld, bs;
+  __device__ void block(int b, int, int m0, int n0, const double* blk, int lane, int M, int N, bool syrk) const {
+    const int64_t base = static_cast<int64_t>(b) * bs;
+    OZ_ROW_PASS(store_from_f64(out, base + static_cast<int64_t>(m) * ld + n, dt, v));
+  }
+};
+
+__device__ __forceinline__ uint64_t oz_desc(uint32_t tile, int ks) {
+  return sdesc_sw64(tile + ks * 32, 16, 512);  // 64-byte K rows, 8-row atoms 512 B apart; k-step = 32 B
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(256, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const OzWork work, const OzScales sc, const Epi epi) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * OZ_STAGE_BYTES);
+  uint64_t* empty = full + OZ_STAGES;
+  uint64_t* tfull = empty + OZ_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, OZ_TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int idx = blockIdx.x; idx < work.num_work; idx += gridDim.x) {
+        int b, split, tm, tn, kt0, kt1;
+        oz_decode(work, idx, b, split, tm, tn, kt0, kt1);
+        for (int kt = kt0; kt < kt1; ++kt) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * OZ_STAGE_BYTES;
+          if (work.dbg & 2) {
+            mbar_arrive(&full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], OZ_STAGE_BYTES);
+            tma_load_4d(&tmA, &full[stage], st, kt * OZ_BK, tm * OZ_BM, b, 0);                  // S planes
+            tma_load_4d(&tmB, &full[stage], st + OZ_S * OZ_A_TILE, kt * OZ_BK, tn * OZ_BN, b, 0);
+          }
+          if (++stage == OZ_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC = idesc_s8(OZ_BM, OZ_BN);
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int idx = blockIdx.x; idx < work.num_work; idx += gridDim.x) {
+        int b, split, tm, tn, kt0, kt1;
+        oz_decode(work, idx, b, split, tm, tn, kt0, kt1);
+        mbar_wait(tempty, acc_phase ^ 1);
+        tc_fence_after();
+        for (int kt = kt0; kt < kt1; ++kt) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * OZ_STAGE_BYTES);
+          const uint32_t sb = sa + OZ_S * OZ_A_TILE;
+#pragma unroll
+          for (int ks = 0; ks < ((work.dbg & 1) ? 0 : OZ_BK / 32); ++ks) {
+#pragma unroll
+            for (int g = 0; g < OZ_S; ++g) {      // digit pairs (s, t) with s + t = g (0-based)
+#pragma unroll
+              for (int s = 0; s <= g; ++s) {
+                const int t = g - s;
+                const uint32_t acc = (kt > kt0 || ks > 0 || s > 0) ? 1u : 0u;
+                umma_s8(tmem_base + static_cast<uint32_t>(g * OZ_BN), oz_desc(sa + s * OZ_A_TILE, ks),
+                        oz_desc(sb + t * OZ_B_TILE, ks), IDESC, acc);
+              }
+            }
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == OZ_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(tfull);
+        acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // Drain first: the S accumulator groups of the thread's row are combined in fp64 (chunk 0 into the
+    // staging block, chunk 1 in registers) and the TMEM is released at once, so the next tile's MMAs
+    // overlap the rest of this epilogue (the
+    // 5 x 64 accumulator columns cannot be double-buffered in 512 TMEM columns).  Then scaling by
+    // 2^(e_m + e_n - 12), a per-warp 32 x 32 fp64 staging block, and the functor's coalesced row pass
+    // (lanes along n) and optional column pass (lanes along m).
+    const int ew = warp - 4;
+    double* blk = reinterpret_cast<double*>(smem + OZ_STAGES * OZ_STAGE_BYTES + 1024) + ew * 32 * 33;
+    uint32_t acc_phase = 0;
+    for (int idx = blockIdx.x; idx < work.num_work; idx += gridDim.x) {
+      int b, split, tm, tn, kt0, kt1;
+      oz_decode(work, idx, b, split, tm, tn, kt0, kt1);
+      mbar_wait(tfull, acc_phase);
+      acc_phase ^= 1;
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
+      const int m0 = tm * OZ_BM + ew * 32;
+      const int row = m0 + lane;
+      const unsigned long long ma = row < sc.M ? sc.a[b * sc.a_bs + row] : 0ull;
+      const bool a_bad = !(__longlong_as_double(static_cast<long long>(ma)) <= 1.7976931348623157e308);
+      const int ea = oz_exponent(ma) - 12;
+      int eb[OZ_BN / 32];
+      bool b_bad[OZ_BN / 32];
+#pragma unroll
+      for (int c = 0; c < OZ_BN / 32; ++c) {
+        const int coln = tn * OZ_BN + c * 32 + lane;
+        const unsigned long long mb = coln < sc.N ? sc.b[b * sc.b_bs + coln] : 0ull;
+        eb[c] = oz_exponent(mb);
+        b_bad[c] = !(__longlong_as_double(static_cast<long long>(mb)) <= 1.7976931348623157e308);
+      }
+      // chunk c: combine the S groups of 32 columns; chunk 0 goes to the staging block at once,
+      // the last chunk stays in registers until the TMEM is released.
+      double v[32];
+#pragma unroll
+      for (int c = 0; c < OZ_BN / 32; ++c) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.0;
+#pragma unroll
+        for (int g = 0; g < OZ_S; ++g) {
+          uint32_t r[32];
+          tmem_ld32(taddr + g * OZ_BN + c * 32, r);
+          tmem_wait_ld();
+          const double wgt = oz_pow2(-7 * g);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = fma(static_cast<double>(static_cast<int32_t>(r[j])), wgt, v[j]);
+        }
+        if (c + 1 < OZ_BN / 32) {
+          __syncwarp();
+          if (c > 0) epi.block(b, split, m0, tn * OZ_BN + (c - 1) * 32, blk, lane, sc.M, sc.N, work.syrk != 0);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int ej = __shfl_sync(0xffffffffu, eb[c], j);
+            const bool bj = __shfl_sync(0xffffffffu, b_bad[c] ? 1 : 0, j) != 0;
+            blk[lane * 33 + j] = (a_bad || bj) ? __longlong_as_double(0x7FF8000000000000ll) : v[j] * oz_pow2(ea + ej);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);  // every accumulator column is in registers / staging now
+      constexpr int CL = OZ_BN / 32 - 1;
+      __syncwarp();
+      if (CL > 0) epi.block(b, split, m0, tn * OZ_BN + (CL - 1) * 32, blk, lane, sc.M, sc.N, work.syrk != 0);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int ej = __shfl_sync(0xffffffffu, eb[CL], j);
+        const bool bj = __shfl_sync(0xffffffffu, b_bad[CL] ? 1 : 0, j) != 0;
+        blk[lane * 33 + j] = (a_bad || bj) ? __longlong_as_double(0x7FF8000000000000ll) : v[j] * oz_pow2(ea + ej);
+      }
+      __syncwarp();
+      epi.block(b, split, m0, tn * OZ_BN + CL * 32, blk, lane, sc.M, sc.N, work.syrk != 0);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, OZ_TMEM_COLS);
+  }
+}
+
+}  // namespace unso

@@ -32,6 +32,7 @@
 #include "umma2_gemm.cuh"
 #include "chain_pair.cuh"
 #include "ns_bf16.cuh"
+#include "ozaki_i8.cuh"
 #include "multi_chain.cuh"
 #include "muon_update.cuh"
 #include <cstdlib>
@@ -423,7 +424,7 @@ struct Problem {
   int dt;
   bool tall;
   int64_t h, w;
-  int method, scaling, gpow, prec, order, steps, flags;
+  int method = 0, scaling = 0, gpow = 1, prec = 0, order = 0, steps = 0, flags = 0;
   std::vector<double> co;
 };
 
@@ -491,6 +492,8 @@ struct Plan {
   size_t mnorm = 0, mpstat = 0;                   // multi-launch pipeline: norm / final-P partials
   size_t C8h[2] = {0, 0}, C8l[2] = {0, 0};        // e4m3 operand planes of C_k (2^8 hi, 2^16 lo)
   size_t C8i[2] = {0, 0};                         // e4m3 interleaved [hi8 | lo8] per 64-column block
+  size_t ozX = 0, ozC = 0, ozMaxA = 0, ozMaxB = 0;  // FP32 on the int8 tensor cores: digit planes, row maxima
+  int64_t ozX_plane = 0, ozC_plane = 0, ozMaxA_bs = 0;
 };
 
 static size_t take(Plan& pl, size_t bytes) {
@@ -517,7 +520,25 @@ static int pick_splits(int64_t tiles, int64_t ktiles, int64_t slots) {
   return best;
 }
 
-static int gram_splits(const Problem& p) {
+// FP32 mode on the int8 tensor cores (ozaki_i8.cuh): UNSO with h > 256 (smaller h runs the
+// one-launch fp64 chain, latency-bound) unless UNSO_FLAG_FP32_DMMA asks for the fp64 DMMA engine.
+static bool use_oz(const Problem& p) {
+  return p.prec == UNSO_PREC_FP32 && p.method == UNSO_METHOD_UNSO && p.h > 256 && (p.flags & UNSO_FLAG_FP32_DMMA) == 0;
+}
+static int64_t oz_syrk_tiles(int64_t h) {
+  const int64_t tm = (h + OZ_BM - 1) / OZ_BM, tn = (h + OZ_BN - 1) / OZ_BN;
+  int64_t t = 0;
+  for (int64_t i = 0; i < tm; ++i) t += std::max<int64_t>(0, tn - 2 * i);
+  return t;
+}
+
+static int gram_splits(const Problem& p, bool for_error = false) {
+  if (!for_error && use_oz(p)) {  // every split-K slice within the int32 bound, then fill the last wave
+    const int64_t kt = (p.w + OZ_BK - 1) / OZ_BK;
+    const int min_s = static_cast<int>((p.w + OZ_MAX_K - 1) / OZ_MAX_K);
+    const int s = pick_splits(oz_syrk_tiles(p.h) * p.batch, kt, device_sm_count());
+    return std::max(min_s, s);
+  }
   if (p.prec == UNSO_PREC_BF16) {
     const int64_t tm = use_pair_engine() ? 256 : 128;
     const int64_t t = (p.h + tm - 1) / tm;
@@ -535,7 +556,7 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
   const int64_t B = p.batch;
   const bool bf = !for_error && p.prec == UNSO_PREC_BF16;
   const size_t ge = bf ? 4 : 8;  // Gram element size
-  pl.splits = with_gram ? gram_splits(p) : 1;
+  pl.splits = with_gram ? gram_splits(p, for_error) : 1;
   pl.scal = take(pl, static_cast<size_t>(B) * SCAL_STRIDE * 8);  // first: same offset for every plan
   pl.ldx = p.ld;
   pl.xcopy = false;
@@ -586,6 +607,18 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       pl.gbar = take(pl, CHAIN_ROUNDS * 8);  // chain_f64_kernel rounds and phase-A partials
       const int64_t nt16 = (p.h + 15) / 16;
       pl.normbuf = take(pl, static_cast<size_t>(nt16 * (nt16 + 1) / 2 * B) * 2 * 8);
+      if (use_oz(p)) {
+        // X digit planes: [S][B][h][round_up(w, 64)] (Gram operand) or [S][B][w][round_up(h, 64)]
+        // (apply operand) -- one buffer, the Gram's planes are dead before the apply's are written.
+        const int64_t xa = p.h * round_up(p.w, 64), xb = p.w * round_up(p.h, 64);
+        pl.ozX_plane = B * std::max(xa, xb);
+        pl.ozX = take(pl, static_cast<size_t>(OZ_S * pl.ozX_plane));
+        pl.ozC_plane = B * pl.hh;  // C_k digit planes, then P's
+        pl.ozC = take(pl, static_cast<size_t>(OZ_S * pl.ozC_plane));
+        pl.ozMaxA_bs = std::max(p.w, p.h);
+        pl.ozMaxA = take(pl, static_cast<size_t>(B * pl.ozMaxA_bs) * 8);
+        pl.ozMaxB = take(pl, static_cast<size_t>(B * p.h) * 8);
+      }
     }
   } else if (bf) {
     // NS in BF16: fp32 state ping-pong + bf16 operand copy (always), G hi/lo, operator B (P), B hi/lo
@@ -696,6 +729,111 @@ static int32_t gelfand_scale(const Problem& p, const Plan& pl, void* ws, const T
   return UNSO_OK;
 }
 
+// ---------------------------------------------------------------- FP32 mode: int8 tensor-core engine
+// 4-D map over the digit planes: {K, rows, batch, digit}, box {64, box_rows, 1, OZ_S}, SWIZZLE_64B --
+// one TMA instruction stages all digit planes of a 64-byte k-block (ozaki_i8.cuh).
+static bool oz_map(CUtensorMap* m, const int8_t* base, int64_t k, int64_t rows, int64_t batch, int64_t ld, int64_t bs,
+                   int64_t plane, int box_rows) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(batch), static_cast<cuuint64_t>(OZ_S)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(batch > 1 ? bs : rows * ld),
+                                 static_cast<cuuint64_t>(plane)};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(OZ_BK), static_cast<cuuint32_t>(box_rows), 1u,
+                             static_cast<cuuint32_t>(OZ_S)};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Digit planes of one operand: operand row = source row (transpose = false) or source column
+// (true); maxbuf[b * max_bs + operand row] receives the row's max |a| first.
+static int32_t oz_slice(const void* src, int dt, int64_t ld, int64_t bs, int64_t rows, int64_t cols, int64_t batch,
+                        bool transpose, unsigned long long* maxbuf, int64_t max_bs, int8_t* dst, int64_t ldd,
+                        int64_t dbs, int64_t plane, cudaStream_t st) {
+  if (!transpose) {
+    dim3 g(static_cast<unsigned>(std::min<int64_t>((rows + 7) / 8, 148 * 16)), static_cast<unsigned>(batch));
+    oz_rowmax_kernel<<<g, 256, 0, st>>>(src, dt, ld, bs, rows, cols, static_cast<int>(batch), maxbuf, max_bs);
+    UNSO_CHECK_LAUNCH();
+  } else {
+    if (cudaMemsetAsync(maxbuf, 0, static_cast<size_t>(batch * max_bs) * 8, st) != cudaSuccess) return UNSO_ERR_CUDA;
+    const int rpb = 256;
+    dim3 g(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>((rows + rpb - 1) / rpb),
+           static_cast<unsigned>(batch));
+    oz_colmax_kernel<<<g, 256, 0, st>>>(src, dt, ld, bs, rows, cols, maxbuf, max_bs, rpb);
+    UNSO_CHECK_LAUNCH();
+  }
+  dim3 g(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>(batch));
+  oz_split_kernel<<<g, 256, 0, st>>>(src, dt, ld, bs, rows, cols, transpose ? 1 : 0, maxbuf, max_bs, dst, ldd, dbs,
+                                     plane);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+struct OzOperand {
+  const int8_t* planes;
+  int64_t ld, bs, plane;                 // bytes
+  const unsigned long long* maxbits;     // per operand row
+  int64_t max_bs;
+};
+
+// D[b](m, n) = sum_k A[b](m, k) B[b](n, k) through the digit planes; SYRK keeps n >= m.
+template <class Epi>
+static int32_t oz_gemm(const OzOperand& A, const OzOperand& B, int64_t M, int64_t N, int64_t K, int64_t batch,
+                       bool syrk, int splits, const Epi& epi, cudaStream_t st) {
+  static PerDeviceFlag configured;
+  const int cfg_dev = PerDeviceFlag::current();
+  if (!configured.test(cfg_dev)) {
+    if (cudaFuncSetAttribute(oz_gemm_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM) != cudaSuccess)
+      return UNSO_ERR_CUDA;
+    configured.set(cfg_dev);
+  }
+  OzWork w;
+  w.tiles_m = static_cast<int>((M + OZ_BM - 1) / OZ_BM);
+  w.tiles_n = static_cast<int>((N + OZ_BN - 1) / OZ_BN);
+  w.syrk = syrk ? 1 : 0;
+  w.k_tiles = static_cast<int>((K + OZ_BK - 1) / OZ_BK);
+  w.splits = std::max(1, std::min(splits, w.k_tiles));
+  if ((K + w.splits - 1) / w.splits > OZ_MAX_K) return UNSO_ERR_UNSUPPORTED;  // int32 accumulator bound
+  w.batch = static_cast<int>(batch);
+  static const int oz_dbg = dev_override("UNSO_OZ_DEBUG") ? std::atoi(dev_override("UNSO_OZ_DEBUG")) : 0;
+  w.dbg = oz_dbg;
+  w.tiles_per_mat = static_cast<int>(syrk ? oz_syrk_tiles(M) : static_cast<int64_t>(w.tiles_m) * w.tiles_n);
+  const int64_t nw = static_cast<int64_t>(w.tiles_per_mat) * w.splits * batch;
+  if (nw <= 0) return UNSO_OK;
+  if (nw > (1ll << 31) - 1) return UNSO_ERR_UNSUPPORTED;
+  w.num_work = static_cast<int>(nw);
+  CUtensorMap ta, tb;
+  if (!oz_map(&ta, A.planes, K, M, batch, A.ld, A.bs, A.plane, OZ_BM) ||
+      !oz_map(&tb, B.planes, K, N, batch, B.ld, B.bs, B.plane, OZ_BN))
+    return UNSO_ERR_CUDA;
+  OzScales sc{A.maxbits, A.max_bs, B.maxbits, B.max_bs, static_cast<int>(M), static_cast<int>(N)};
+  const int grid = static_cast<int>(std::min<int64_t>(nw, device_sm_count()));
+  oz_gemm_kernel<Epi><<<grid, 256, OZ_SMEM, st>>>(ta, tb, w, sc, epi);
+  UNSO_CHECK_LAUNCH();
+  return UNSO_OK;
+}
+
+// Gram split-K partials of X on the int8 engine (the fp64 partial layout of gram_simt).
+static int32_t gram_oz(const Problem& p, const void* x, const Plan& pl, void* ws, int splits, cudaStream_t st) {
+  int8_t* planes = at<int8_t>(ws, pl.ozX);
+  unsigned long long* mx = at<unsigned long long>(ws, pl.ozMaxA);
+  const int64_t ldd = round_up(p.w, 64), dbs = p.h * ldd;
+  // operand rows = the h short-side vectors: columns of a tall X, rows of a wide one
+  UNSO_TRY(oz_slice(x, p.dt, p.ld, p.bs, p.rows, p.cols, p.batch, p.tall, mx, pl.ozMaxA_bs, planes, ldd, dbs,
+                    pl.ozX_plane, st));
+  const OzOperand X{planes, ldd, dbs, pl.ozX_plane, mx, pl.ozMaxA_bs};
+  OzEpiPartial epi{at<double>(ws, pl.part), pl.hh, pl.ldc, static_cast<int>(p.batch)};
+  return oz_gemm(X, X, p.h, p.h, p.w, p.batch, true, splits, epi, st);
+}
+
+static int32_t gram_fp32(const Problem& p, const void* x, const Plan& pl, void* ws, int splits, cudaStream_t st) {
+  if (use_oz(p)) return gram_oz(p, x, pl, ws, splits, st);
+  return gram_simt(p, x, p.dt, p.ld, p.bs, pl, ws, splits, st);
+}
+
 static int scal_mode(int scaling) {
   return scaling == UNSO_SCALING_PLAIN ? SM_PLAIN : (scaling == UNSO_SCALING_NONE ? SM_NONE : SM_GRAM);
 }
@@ -789,6 +927,43 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
   if (p.scaling == UNSO_SCALING_GELFAND) UNSO_TRY(gelfand_scale<double>(p, pl, ws, G, DT_F64, status, st));
   double alpha = 1.0;
   for (double v : p.co) alpha += v;
+  if (use_oz(p)) {
+    // int8 engine: per squaring one SYRK on C_k's digit planes writing S = C_k^2 (stores only),
+    // then one fused row kernel: C_{k+1} = 2 C_k - S, P -= c_{k+1} C_{k+1}, row max + digit planes.
+    OzStepParams sp;
+    sp.S = at<double>(ws, pl.Pout);  // scratch for S until finalize_p
+    sp.P = at<double>(ws, pl.P);
+    sp.scal = at<double>(ws, pl.scal);
+    sp.alpha = alpha;
+    sp.h = h;
+    sp.ld = pl.ldc;
+    sp.bs = pl.hh;
+    sp.maxbits = at<unsigned long long>(ws, pl.ozMaxB);
+    sp.plane = pl.ozC_plane;
+    const dim3 rgrid(static_cast<unsigned>(std::min<int64_t>((h + 7) / 8, 148 * 16)), static_cast<unsigned>(p.batch));
+    sp.mode = 0;
+    sp.src = G;
+    sp.Cn = at<double>(ws, pl.C[0]);
+    sp.coef = p.co[0];
+    sp.digits = N > 1 ? at<int8_t>(ws, pl.ozC) : nullptr;
+    oz_chain_step_kernel<<<rgrid, 256, 0, st>>>(sp);
+    UNSO_CHECK_LAUNCH();
+    prof_mark(3, st);
+    const OzOperand C{at<int8_t>(ws, pl.ozC), pl.ldc, pl.hh, pl.ozC_plane, sp.maxbits, h};
+    const OzEpiSym se{at<double>(ws, pl.Pout), pl.ldc, pl.hh};
+    int cur = 0;
+    for (int k = 1; k < N; ++k) {  // produces C_{k+1}
+      UNSO_TRY(oz_gemm(C, C, h, h, h, p.batch, true, 1, se, st));
+      sp.mode = 1;
+      sp.src = at<double>(ws, pl.C[cur]);
+      sp.Cn = at<double>(ws, pl.C[cur ^ 1]);
+      sp.coef = p.co[k];
+      sp.digits = k + 1 < N ? at<int8_t>(ws, pl.ozC) : nullptr;
+      oz_chain_step_kernel<<<rgrid, 256, 0, st>>>(sp);
+      UNSO_CHECK_LAUNCH();
+      cur ^= 1;
+    }
+  } else {
   {
     dim3 grid(grid_for(static_cast<int64_t>(h) * h, 256, 1024), static_cast<unsigned>(p.batch));
     prep_f64_kernel<double><<<grid, 256, 0, st>>>(G, h, pl.ldc, at<double>(ws, pl.scal), alpha, p.co[0],
@@ -798,16 +973,14 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
   prof_mark(3, st);
   int cur = 0;
   for (int k = 1; k < N; ++k) {  // produces C_{k+1}
-    SimtOperand C{at<double>(ws, pl.C[cur]), pl.ldc, pl.hh, DT_F64, 1};
     EpiChainF64 epi{at<double>(ws, pl.C[cur]), at<double>(ws, pl.C[cur ^ 1]), at<double>(ws, pl.P), pl.ldc, pl.hh,
                     p.co[k], k + 1 < N ? 1 : 0};
-    const int t = (h + SIMT_BM - 1) / SIMT_BM;
-    const int splits = 1;
-    (void)t;
-    if (launch_simt_gemm(C, C, h, h, h, static_cast<int>(p.batch), true, splits, epi, st) != cudaSuccess)
+    SimtOperand C{at<double>(ws, pl.C[cur]), pl.ldc, pl.hh, DT_F64, 1};
+    if (launch_simt_gemm(C, C, h, h, h, static_cast<int>(p.batch), true, 1, epi, st) != cudaSuccess)
       return UNSO_ERR_CUDA;
     ++g_launches;
     cur ^= 1;
+  }
   }
   prof_mark(4, st);
   }
@@ -819,6 +992,27 @@ static int32_t unso_fp32_from_G(const Problem& p, const Plan& pl, void* ws, cons
     UNSO_CHECK_LAUNCH();
   }
   prof_mark(5, st);
+  if (use_oz(p)) {  // apply on the int8 engine: tall Y = X P, wide Y = P X (P symmetric: its rows are B's)
+    int8_t* pp = at<int8_t>(ws, pl.ozC);
+    unsigned long long* pm = at<unsigned long long>(ws, pl.ozMaxB);
+    UNSO_TRY(oz_slice(at<double>(ws, pl.Pout), DT_F64, pl.ldc, pl.hh, h, h, p.batch, false, pm, h, pp, pl.ldc, pl.hh,
+                      pl.ozC_plane, st));
+    const OzOperand Pd{pp, pl.ldc, pl.hh, pl.ozC_plane, pm, h};
+    int8_t* xp = at<int8_t>(ws, pl.ozX);
+    unsigned long long* xm = at<unsigned long long>(ws, pl.ozMaxA);
+    const int64_t ldd = round_up(p.h, 64), dbs = p.w * ldd;
+    // operand rows = the w long-side vectors of length h: rows of a tall X, columns of a wide one
+    UNSO_TRY(oz_slice(x, p.dt, p.ld, p.bs, p.rows, p.cols, p.batch, !p.tall, xm, pl.ozMaxA_bs, xp, ldd, dbs,
+                      pl.ozX_plane, st));
+    const OzOperand Xd{xp, ldd, dbs, pl.ozX_plane, xm, pl.ozMaxA_bs};
+    OzEpiOut epi{y, p.dt, p.cols, p.rows * p.cols};
+    if (p.tall)
+      UNSO_TRY(oz_gemm(Xd, Pd, p.w, h, h, p.batch, false, 1, epi, st));
+    else
+      UNSO_TRY(oz_gemm(Pd, Xd, h, p.w, h, p.batch, false, 1, epi, st));
+    prof_mark(6, st);
+    return UNSO_OK;
+  }
   // apply: tall Y = X P (A = X K-major over w rows), wide Y = P X (B = X MN-major)
   SimtOperand Xop{x, p.ld, p.bs, p.dt, 1};
   SimtOperand Pop{at<double>(ws, pl.Pout), pl.ldc, pl.hh, DT_F64, 1};
@@ -1666,7 +1860,7 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
   prof_mark(0, st);
   if (p.prec == UNSO_PREC_FP32) {
     prof_mark(1, st);
-    UNSO_TRY(gram_simt(p, x_ptr, p.dt, p.ld, p.bs, pl, workspace, pl.splits, st));
+    UNSO_TRY(gram_fp32(p, x_ptr, pl, workspace, pl.splits, st));
     prof_mark(2, st);
     double* G = at<double>(workspace, pl.G);
     UNSO_TRY(finalize_gram<double>(p, pl, workspace, pl.splits, G, st));
@@ -1759,7 +1953,7 @@ int32_t unso_gram(const unso_matrix_desc* x, const void* x_ptr, void* g_ptr, con
   // g_ptr is dense batch x h x h; finalize into the padded workspace G, then compact
   const int64_t h = p.h;
   if (p.prec == UNSO_PREC_FP32) {
-    UNSO_TRY(gram_simt(p, x_ptr, p.dt, p.ld, p.bs, pl, workspace, pl.splits, st));
+    UNSO_TRY(gram_fp32(p, x_ptr, pl, workspace, pl.splits, st));
     return finalize_gram<double>(p, pl, workspace, pl.splits, static_cast<double*>(g_ptr), st, h, h * h);
   }
   const __nv_bfloat16* xb;

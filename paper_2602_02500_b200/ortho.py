@@ -79,6 +79,8 @@ class MethodSpec:
     truncate: bool = True            # bf16 mode, persistent chain: stop once ||I - C_k||_F bounds the rest
     ns_products: str | None = None   # bf16 mode, NS kinds: None / "bf16x3" = hi/lo state in the long-side
                                      # products (~1e-4 from fp64), "bf16" = one bf16 term (faster, ~1e-2)
+    fp32_engine: str | None = None   # fp32 mode, UNSO, h > 256: None / "int8" = int8 tensor-core digit split
+                                     # (~1e-7 from fp64), "dmma" = the fp64 tensor cores (~1e-14, slower)
 
     def __post_init__(self):
         object.__setattr__(self, "_cache", {})  # per-spec memo of the native method descriptor / FLOP model
@@ -96,6 +98,8 @@ class MethodSpec:
             raise ValueError("chain must be None (bf16 + e4m3 cross terms) or 'bf16x3'")
         if self.ns_products not in (None, "bf16x3", "bf16"):
             raise ValueError("ns_products must be None / 'bf16x3' (hi/lo state) or 'bf16'")
+        if self.fp32_engine not in (None, "int8", "dmma"):
+            raise ValueError("fp32_engine must be None / 'int8' (int8 tensor-core split) or 'dmma' (fp64)")
         if kind is MethodKind.UNSO:
             if self.coeffs is None:
                 raise ValueError("unso requires a CoefficientSet")
@@ -339,6 +343,8 @@ def _build_method_desc(spec: MethodSpec, precision: Precision, scaling_code: int
         flags |= N.FLAG_CHAIN_BF16X3
     if not spec.truncate:
         flags |= N.FLAG_NO_TRUNCATION
+    if spec.fp32_engine == "dmma":
+        flags |= N.FLAG_FP32_DMMA
     md = N.MethodDesc(method, scaling_code, spec.gelfand_power,
                       N.PREC_BF16 if precision is Precision.BF16 else N.PREC_FP32, order, steps,
                       co.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), flags, 0)

@@ -39,7 +39,9 @@ def test_library_is_sm100a_cubin():
         pytest.skip("cuobjdump not available")
     out = subprocess.run([exe, "-sass", N.LIB_PATH], capture_output=True, text=True, check=True).stdout
     assert "sm_100a" in out
-    assert "UTCHMMA" in out      # tcgen05.mma
+    assert "UTCHMMA" in out      # tcgen05.mma kind::f16
+    assert "UTCIMMA" in out      # tcgen05.mma kind::i8 (fp32 mode digit products)
+    assert "UTMALDG.4D" in out   # 4-D TMA box of the int8 digit planes
     assert "UTMALDG" in out      # TMA tensor loads
     assert "LDTM" in out         # tcgen05.ld
 
@@ -137,7 +139,7 @@ def test_header_constants_match_the_binding():
         "UNSO_METHOD_QUINTIC": N.METHOD_QUINTIC,
         "UNSO_FLAG_SINGLE_TERM_APPLY": N.FLAG_SINGLE_TERM_APPLY, "UNSO_FLAG_TWO_TERM_APPLY": N.FLAG_TWO_TERM_APPLY,
         "UNSO_FLAG_CHAIN_BF16X3": N.FLAG_CHAIN_BF16X3, "UNSO_FLAG_NO_TRUNCATION": N.FLAG_NO_TRUNCATION,
-        "UNSO_FLAG_NS_SINGLE_STATE": N.FLAG_NS_SINGLE_STATE,
+        "UNSO_FLAG_NS_SINGLE_STATE": N.FLAG_NS_SINGLE_STATE, "UNSO_FLAG_FP32_DMMA": N.FLAG_FP32_DMMA,
         "UNSO_MAX_PEERS": N.MAX_PEERS, "UNSO_SCALARS": N.SCALARS, "UNSO_PROFILE_STAGES": len(N.PROFILE_STAGES),
     }
     for name, value in expect.items():
