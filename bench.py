@@ -340,6 +340,28 @@ def executed_flops_bf16_unso(h: int, w: int, order: int, chain_steps: float, app
     return {"gram": gram, "chain": chain, "apply": apply, "total": gram + chain + apply}
 
 
+OZ_BM, OZ_BN, OZ_PRODUCTS = 256, 96, 15  # csrc/ozaki_i8.cuh: CTA-pair tile, S(S+1)/2 digit products (S = 5)
+
+
+def _oz_syrk_tiles(h: int) -> int:
+    tm, tn = -(-h // OZ_BM), -(-h // OZ_BN)
+    return sum(max(0, tn - (OZ_BM * i) // OZ_BN) for i in range(tm))
+
+
+def executed_ops_int8_unso(h: int, w: int, order: int, tall: bool) -> dict:
+    """int8 tensor-core ops (2 per MAC) the fp32-mode digit engine issues for one h x w matrix
+    (csrc/ozaki_i8.cuh, h > 256): every contraction is 15 int8 products over 256 x 96 pair tiles --
+    the Gram and each of the order-1 squarings as SYRKs (upper pair tiles), the apply over all tiles."""
+    hp64 = -(-h // 64) * 64
+    wp64 = -(-w // 64) * 64
+    tile = 2.0 * OZ_BM * OZ_BN * OZ_PRODUCTS
+    gram = tile * wp64 * _oz_syrk_tiles(h)
+    chain = (order - 1) * tile * hp64 * _oz_syrk_tiles(h)
+    m, n = (w, h) if tall else (h, w)
+    apply = tile * hp64 * (-(-m // OZ_BM)) * (-(-n // OZ_BN))
+    return {"gram": gram, "chain": chain, "apply": apply, "total": gram + chain + apply}
+
+
 # ----------------------------------------------------------------------------- workloads
 
 WORKLOAD_NAMES = {
@@ -491,7 +513,13 @@ class MatrixWorkload:
         return out
 
     def executed(self, info):
-        """Executed bf16-equivalent FLOPs per step (whole job), bf16 mode only."""
+        """Executed bf16-equivalent FLOPs per step (whole job) in bf16 mode; int8 tensor-core ops of
+        the digit engine in fp32 mode (h > 256)."""
+        if self.precision == "fp32" and self.h > 256:
+            e = executed_ops_int8_unso(self.h, self.w, self.spec.coeffs.order, self.shape[0] > self.shape[1])
+            e = {k: v * self.total_batch for k, v in e.items()}
+            e["unit"] = "int8 ops"
+            return e
         if self.precision != "bf16" or not info:
             return None
         route = "persistent" if self.h <= 2048 else "glue-free"
@@ -777,7 +805,16 @@ def main(argv=None):
     # ---- executed work (what the tensor cores actually issue)
     execd = work.executed(gate.get("info"))
     executed = None
-    if execd:
+    int8_peak = 2.0 * peak  # B200 dense int8 = 2x dense bf16 (4.5 POPS vs 2.25 PFLOPS); no measured int8 peak
+    if execd and execd.get("unit") == "int8 ops":
+        executed = {"int8_ops_per_step": execd["total"], "tops": execd["total"] / (ms_step / 1e3) / 1e12,
+                    "frac_of_int8_peak": execd["total"] / (ms_step / 1e3) / 1e12 / int8_peak,
+                    "by_stage": {k: execd[k] for k in ("gram", "chain", "apply")},
+                    "int8_peak_tops": int8_peak,
+                    "how": "int8 tcgen05.mma ops the fp32-mode digit engine issues (15 digit products per "
+                           "contraction, 256 x 96 pair tiles, SYRK upper tiles); int8 peak = 2 x the measured "
+                           "bf16 burst peak (datasheet ratio)"}
+    elif execd:
         executed = {"flops_per_step": execd["total"], "tflops": execd["total"] / (ms_step / 1e3) / 1e12,
                     "frac_of_peak": execd["total"] / (ms_step / 1e3) / 1e12 / peak,
                     "by_stage": {k: execd[k] for k in ("gram", "chain", "apply")},
@@ -820,7 +857,15 @@ def main(argv=None):
                     "frac": achieved / peak, "frac_of_sustained": achieved / peak_sus, "traffic": traffic,
                     "peak_source": f"{peaks_src} bf16_tflops (burst)",
                     "algorithmic_flops_per_step": algo[dom], "stage_ms_per_step": stages[dom]}
-        if execd and dom in execd:
+        if execd and execd.get("unit") == "int8 ops" and dom in execd:
+            # fp32 mode: the dominant contraction runs on the int8 tensor cores -- its roofline is int8 ops
+            ach = execd[dom] / (stages[dom] / 1e3) / 1e12
+            roofline.update({"achieved": ach, "peak": int8_peak, "unit": "TOPS (int8)", "frac": ach / int8_peak,
+                             "frac_of_sustained": ach / (2.0 * peak_sus),
+                             "peak_source": f"2 x {peaks_src} bf16_tflops (burst): dense int8 = 2x bf16",
+                             "algorithmic_int8_ops_per_step": execd[dom],
+                             "model_tflops_fp64_equivalent": algo[dom] / (stages[dom] / 1e3) / 1e12})
+        elif execd and dom in execd:
             roofline["executed_tflops"] = execd[dom] / (stages[dom] / 1e3) / 1e12
             roofline["executed_frac"] = roofline["executed_tflops"] / peak
         hb = work.hbm_bytes()

@@ -217,47 +217,45 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------------------------------------------------------- MMA issuer
-      int stage = 0;
-      uint32_t phase = 0, acc_phase = 0;
-      for (int k = 1; k < N; ++k) {
-        if (k >= 2 && p.trunc_tau > 0.0 && chain_truncate_before(p, k, grid_wait(p.gbar, k))) break;
-        mbar_wait(tempty, acc_phase ^ 1);
+    // ---------------------------------------------------------------- MMA issuer (whole warp, one
+    // elected lane issues: warp-uniform control flow keeps the descriptors in uniform registers)
+    int stage = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int k = 1; k < N; ++k) {
+      if (k >= 2 && p.trunc_tau > 0.0 && chain_truncate_before(p, k, grid_wait(p.gbar, k))) break;
+      mbar_wait(tempty, acc_phase ^ 1);
+      tc_fence_after();
+      for (int kt = 0; kt < KT; ++kt) {
+        mbar_wait(&full[stage], phase);
+        CHAIN_KB(k, 0, kt);
+        if (kt == 0) CHAIN_TRACE(k, 1);
         tc_fence_after();
-        for (int kt = 0; kt < KT; ++kt) {
-          mbar_wait(&full[stage], phase);
-          CHAIN_KB(k, 0, kt);
-          if (kt == 0) CHAIN_TRACE(k, 1);
-          tc_fence_after();
-          const int kb = kt >> 1;
-          const bool a_mn = kb < ti, b_mn = kb < tj;
-          const uint32_t idesc = idesc_bf16(128, 128, a_mn ? 1 : 0, b_mn ? 1 : 0);
-          const uint32_t st = smem_u32(smem + stage * CH_STAGE_BYTES);
+        const int kb = kt >> 1;
+        const bool a_mn = kb < ti, b_mn = kb < tj;
+        const uint32_t idesc = idesc_bf16(128, 128, a_mn ? 1 : 0, b_mn ? 1 : 0);
+        const uint32_t st = smem_u32(smem + stage * CH_STAGE_BYTES);
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t ah = a_mn ? operand_desc<true>(st, ks) : operand_desc<false>(st, ks);
-            const uint64_t al = a_mn ? operand_desc<true>(st + CH_TILE, ks) : operand_desc<false>(st + CH_TILE, ks);
-            const uint64_t bh = b_mn ? operand_desc<true>(st + 2 * CH_TILE, ks)
-                                     : operand_desc<false>(st + 2 * CH_TILE, ks);
-            const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * CH_TILE, ks)
-                                     : operand_desc<false>(st + 3 * CH_TILE, ks);
-            umma_bf16(tmem + CH_ACC, ah, bh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
-            umma_bf16(tmem + CH_ACC, ah, bl, idesc, 1u);
-            umma_bf16(tmem + CH_ACC, al, bh, idesc, 1u);
-          }
-          umma_commit(&empty[stage]);
-          if (++stage == CH_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint64_t ah = a_mn ? operand_desc<true>(st, ks) : operand_desc<false>(st, ks);
+          const uint64_t al = a_mn ? operand_desc<true>(st + CH_TILE, ks) : operand_desc<false>(st + CH_TILE, ks);
+          const uint64_t bh = b_mn ? operand_desc<true>(st + 2 * CH_TILE, ks)
+                                   : operand_desc<false>(st + 2 * CH_TILE, ks);
+          const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * CH_TILE, ks)
+                                   : operand_desc<false>(st + 3 * CH_TILE, ks);
+          umma_bf16_warp(tmem + CH_ACC, ah, bh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
+          umma_bf16_warp(tmem + CH_ACC, ah, bl, idesc, 1u);
+          umma_bf16_warp(tmem + CH_ACC, al, bh, idesc, 1u);
         }
-        umma_commit(tfull);
-        CHAIN_TRACE(k, 2);
-        acc_phase ^= 1;
+        umma_commit_warp(&empty[stage]);
+        if (++stage == CH_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      umma_commit_warp(tfull);
+      CHAIN_TRACE(k, 2);
+      acc_phase ^= 1;
     }
-    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue warps
     const int ew = warp - 4;

@@ -17,10 +17,13 @@
 // spectrum) of the fp64 oracle (tools/ozaki_emulation.py, an exact emulation of this scheme).
 // int32 bound: a group holds <= S products of |d_s d_t| <= 4096, so K <= OZ_MAX_K per split-K slice.
 //
-// Engine: one persistent CTA per SM, 128 x 64 output tiles, K staged 64 bytes at a time with all S
-// digit planes of A (S x 8 KB) and of B (S x 4 KB) in one 4-D TMA box each (SWIZZLE_64B), 3 stages;
-// warp 0 TMA, warp 1 MMA (15 products x 2 k-steps per stage into S accumulators of 64 columns),
-// warp 2 TMEM, warps 4..7 epilogue (drain + fp64 combination, exponents, coalesced block functors).
+// Engine: persistent CTA pairs (cta_group::2), 256 x 96 output tiles per pair (TMEM: S accumulators
+// of 96 columns = 480 of 512), K staged 64 bytes at a time: each CTA loads its 128 A rows and 48 of the
+// B rows in all S digit planes with one 4-D TMA box each (SWIZZLE_64B), 3 stages; warp 0 TMA (both
+// CTAs), warp 1 of the leader MMA (15 products x 2 k-steps per stage, M = 256 per instruction: the
+// i8 MMAs are short, so fewer and larger instructions matter -- issue, not the tensor pipe, bounds
+// small-N tiles), warp 2 TMEM, warps 4..7 epilogue (drain + fp64 combination, exponents, coalesced
+// block functors) in both CTAs.
 #pragma once
 #include "common.cuh"
 #include "ptx_sm100.cuh"
@@ -28,41 +31,55 @@
 
 namespace unso {
 
-constexpr int OZ_S = 5;                       // digits per operand
-constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 64;  // BK in int8 elements (= bytes)
+constexpr int OZ_S = 5;                        // digits per operand
+constexpr int OZ_BM = 256, OZ_BN = 96, OZ_BK = 64;   // CTA-pair tile; BK in int8 elements (= bytes)
+constexpr int OZ_HB = OZ_BN / 2;               // B rows staged per CTA
 constexpr int OZ_STAGES = 3;
-constexpr int OZ_A_TILE = OZ_BM * OZ_BK;       // 8 KB per digit plane
-constexpr int OZ_B_TILE = OZ_BN * OZ_BK;       // 4 KB
-constexpr int OZ_STAGE_BYTES = OZ_S * (OZ_A_TILE + OZ_B_TILE);
+constexpr int OZ_A_TILE = 128 * OZ_BK;         // 8 KB per digit plane (the CTA's 128 A rows)
+constexpr int OZ_B_TILE = OZ_HB * OZ_BK;       // 3 KB
+constexpr int OZ_STAGE_BYTES = OZ_S * (OZ_A_TILE + OZ_B_TILE);  // per CTA
 constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE_BYTES + 1024 + 4 * 32 * 33 * 8 + 1024;  // stages, barriers, staging
-constexpr uint32_t OZ_TMEM_COLS = 512;         // OZ_S * OZ_BN = 320 used
+constexpr uint32_t OZ_TMEM_COLS = 512;         // OZ_S * OZ_BN = 480 used
 constexpr int64_t OZ_MAX_K = 65536;            // 5 * 64 * 64 * 65536 < 2^31
 static_assert(OZ_S * OZ_BN <= 512, "tmem");
 static_assert(OZ_SMEM <= 227 * 1024, "smem");
+static_assert(OZ_STAGE_BYTES % 1024 == 0 && OZ_B_TILE % 512 == 0, "swizzle atom alignment");
 
 // kind::i8: s8 x s8 -> s32 (c_format 2, a/b format 1 = signed), K-major operands.
 __host__ __device__ constexpr uint32_t idesc_s8(int M, int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
          (static_cast<uint32_t>(M >> 4) << 24);
 }
-__device__ __forceinline__ void umma_s8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                        uint32_t accumulate) {
+// Warp-collective forms: every lane of a converged warp executes the asm, one elected lane issues.
+// Descriptors computed in warp-uniform control flow then stay in uniform registers (no per-MMA
+// R2UR waterfall around a lane-0-only issue, which cost ~80 cycles per instruction here).
+__device__ __forceinline__ void umma_s8_pair_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                  uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_4d(const CUtensorMap* m, uint64_t* bar, void* smem_dst, int c0, int c1,
-                                            int c2, int c3) {
+__device__ __forceinline__ void umma_commit_pair_warp(uint64_t* bar, uint16_t mask) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
-
+__device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* m, uint32_t leader_bar, void* smem_dst, int c0,
+                                                 int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 // Row scale exponent from the row's max |a| (as the u64 bits of a non-negative double): the frexp
 // exponent, so |a| 2^-e < 1.  0 for an all-zero row.  Split kernel and epilogue use the same rule.
 __device__ __forceinline__ int oz_exponent(unsigned long long maxbits) {
@@ -130,39 +147,62 @@ __device__ __forceinline__ void oz_digits(double v, int e, int8_t (&d)[OZ_S]) {
   }
 }
 
-__global__ void oz_split_kernel(const void* __restrict__ src, int dt, int64_t ld, int64_t bs, int64_t rows,
-                                int64_t cols, int transpose, const unsigned long long* __restrict__ maxbits,
-                                int64_t max_bs, int8_t* __restrict__ dst, int64_t ldd, int64_t dbs, int64_t plane) {
-  __shared__ double tile[32][33];
+// 64 x 64 source tiles, 256 threads; every thread digitises 4 consecutive operand-row entries and
+// writes them as one 4-byte word per digit plane (ldd % 64 == 0; entries past K are written as 0
+// digits and never read: the TMA map's K extent ends at K).
+__global__ void __launch_bounds__(256) oz_split_kernel(const void* __restrict__ src, int dt, int64_t ld, int64_t bs,
+                                                       int64_t rows, int64_t cols, int transpose,
+                                                       const unsigned long long* __restrict__ maxbits, int64_t max_bs,
+                                                       int8_t* __restrict__ dst, int64_t ldd, int64_t dbs,
+                                                       int64_t plane) {
+  __shared__ double tile[64][65];
   const int b = blockIdx.z;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int tq = threadIdx.x & 15, tr = threadIdx.x >> 4;  // 16 x 16
+  const char* srcb = static_cast<const char*>(src) + b * bs * dtype_size(dt);
+  auto emit = [&](int64_t R, int64_t k, const double (&v)[4], int e) {
+    uint32_t w[OZ_S];
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) w[s] = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int8_t d[OZ_S];
+      oz_digits(v[q], e, d);
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) w[s] |= static_cast<uint32_t>(static_cast<uint8_t>(d[s])) << (8 * q);
+    }
+    const int64_t o = b * dbs + R * ldd + k;
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint32_t*>(dst + s * plane + o) = w[s];
+  };
   if (!transpose) {
-    for (int i = ty; i < 32; i += 8) {
-      const int64_t r = r0 + i, c = c0 + tx;
+    for (int i = tr; i < 64; i += 16) {
+      const int64_t r = r0 + i, c = c0 + 4 * tq;
       if (r >= rows || c >= cols) continue;
       const int e = oz_exponent(maxbits[b * max_bs + r]);
-      int8_t d[OZ_S];
-      oz_digits(load_as_f64(src, b * bs + r * ld + c, dt), e, d);
-      const int64_t o = b * dbs + r * ldd + c;
+      double v[4];
 #pragma unroll
-      for (int s = 0; s < OZ_S; ++s) dst[s * plane + o] = d[s];
+      for (int q = 0; q < 4; ++q) v[q] = (c + q < cols) ? load_as_f64(srcb, r * ld + c + q, dt) : 0.0;
+      emit(r, c, v, e);
     }
   } else {
-    for (int i = ty; i < 32; i += 8) {
-      const int64_t r = r0 + i, c = c0 + tx;
-      tile[i][tx] = (r < rows && c < cols) ? load_as_f64(src, b * bs + r * ld + c, dt) : 0.0;
+    for (int i = tr; i < 64; i += 16) {
+      const int64_t r = r0 + i;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t c = c0 + 4 * tq + q;
+        tile[i][4 * tq + q] = (r < rows && c < cols) ? load_as_f64(srcb, r * ld + c, dt) : 0.0;
+      }
     }
     __syncthreads();
-    for (int i = ty; i < 32; i += 8) {
-      const int64_t R = c0 + i, k = r0 + tx;  // operand row = source column c0 + i
+    for (int i = tr; i < 64; i += 16) {
+      const int64_t R = c0 + i, k = r0 + 4 * tq;  // operand row = source column c0 + i
       if (R >= cols || k >= rows) continue;
       const int e = oz_exponent(maxbits[b * max_bs + R]);
-      int8_t d[OZ_S];
-      oz_digits(tile[tx][i], e, d);
-      const int64_t o = b * dbs + R * ldd + k;
+      double v[4];
 #pragma unroll
-      for (int s = 0; s < OZ_S; ++s) dst[s * plane + o] = d[s];
+      for (int q = 0; q < 4; ++q) v[q] = tile[4 * tq + q][i];
+      emit(R, k, v, e);
     }
   }
 }
@@ -184,30 +224,41 @@ struct OzStepParams {
   int8_t* digits;               // [s][b][r][ld] planes (plane stride `plane`, batch stride bs)
   int64_t plane;
 };
-__global__ void oz_chain_step_kernel(const OzStepParams p) {
+__global__ void __launch_bounds__(256) oz_chain_step_kernel(const OzStepParams p) {
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.y;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const double inv_s2 = p.mode == 0 ? 1.0 / p.scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_S2] : 0.0;
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.h; r += nw) {
-    const int64_t o0 = static_cast<int64_t>(b) * p.bs + r * p.ld;
+    const int64_t o0 = static_cast<int64_t>(b) * p.bs + r * p.ld;  // 16-byte aligned (ld % 256 == 0)
     double m = 0.0;
     bool bad = false;
-    for (int c = lane; c < p.h; c += 32) {
+    for (int c = 2 * lane; c < p.h; c += 64) {  // two entries per lane: 16-byte accesses
       const int64_t o = o0 + c;
-      double cn, pv;
+      const bool two = c + 1 < p.h;
+      double2 cn, pv;
       if (p.mode == 0) {
-        cn = p.src[o] * inv_s2;
-        pv = (c == r ? p.alpha : 0.0) - p.coef * cn;
+        const double2 g = two ? *reinterpret_cast<const double2*>(p.src + o) : make_double2(p.src[o], 0.0);
+        cn = make_double2(g.x * inv_s2, g.y * inv_s2);
+        pv = make_double2((c == r ? p.alpha : 0.0) - p.coef * cn.x, (c + 1 == r ? p.alpha : 0.0) - p.coef * cn.y);
       } else {
-        cn = 2.0 * p.src[o] - p.S[o];
-        pv = p.P[o] - p.coef * cn;
+        const double2 cc = two ? *reinterpret_cast<const double2*>(p.src + o) : make_double2(p.src[o], 0.0);
+        const double2 ss = two ? *reinterpret_cast<const double2*>(p.S + o) : make_double2(p.S[o], 0.0);
+        const double2 pp = two ? *reinterpret_cast<const double2*>(p.P + o) : make_double2(p.P[o], 0.0);
+        cn = make_double2(2.0 * cc.x - ss.x, 2.0 * cc.y - ss.y);
+        pv = make_double2(pp.x - p.coef * cn.x, pp.y - p.coef * cn.y);
       }
-      p.Cn[o] = cn;
-      p.P[o] = pv;
-      const double a = fabs(cn);
-      bad |= !(a <= 1.7976931348623157e308);
-      m = fmax(m, a);
+      if (two) {
+        *reinterpret_cast<double2*>(p.Cn + o) = cn;
+        *reinterpret_cast<double2*>(p.P + o) = pv;
+      } else {
+        p.Cn[o] = cn.x;
+        p.P[o] = pv.x;
+        cn.y = 0.0;
+      }
+      const double a0 = fabs(cn.x), a1 = fabs(cn.y);
+      bad |= !(a0 <= 1.7976931348623157e308) || !(a1 <= 1.7976931348623157e308);
+      m = fmax(m, fmax(a0, a1));
     }
     if (!p.digits) continue;
 #pragma unroll
@@ -220,11 +271,23 @@ __global__ void oz_chain_step_kernel(const OzStepParams p) {
     if (lane == 0) p.maxbits[static_cast<int64_t>(b) * p.h + r] = bits;
     const int e = oz_exponent(bits);
     __syncwarp();
-    for (int c = lane; c < p.h; c += 32) {
-      int8_t d[OZ_S];
-      oz_digits(p.Cn[o0 + c], e, d);
+    for (int c = 4 * lane; c < p.h; c += 128) {  // four entries per lane: one 4-byte word per plane
+      const int64_t o = o0 + c;
+      double v[4];
 #pragma unroll
-      for (int s = 0; s < OZ_S; ++s) p.digits[s * p.plane + o0 + c] = d[s];
+      for (int q = 0; q < 4; ++q) v[q] = (c + q < p.h) ? p.Cn[o + q] : 0.0;
+      uint32_t w[OZ_S];
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) w[s] = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int8_t d[OZ_S];
+        oz_digits(v[q], e, d);
+#pragma unroll
+        for (int s = 0; s < OZ_S; ++s) w[s] |= static_cast<uint32_t>(static_cast<uint8_t>(d[s])) << (8 * q);
+      }
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint32_t*>(p.digits + s * p.plane + o) = w[s];
     }
   }
 }
@@ -235,7 +298,9 @@ struct OzWork {
   int dbg;  // timing experiments only (developer builds): 1 = skip the MMAs, 2 = skip the TMA loads
 };
 
-// SYRK (square, BM = 2 BN): tile (tm, tn) is kept when tn >= 2 tm (it touches the upper triangle).
+// SYRK (square): pair tile (tm, tn) is kept when its columns reach the diagonal block's first row,
+// tn >= tn_min(tm) = floor(256 tm / 96); the epilogue drops the elements with n < m.
+__host__ __device__ __forceinline__ int oz_tn_min(int tm) { return (OZ_BM * tm) / OZ_BN; }
 __device__ __forceinline__ void oz_decode(const OzWork& w, int idx, int& b, int& split, int& tm, int& tn, int& kt0,
                                           int& kt1) {
   int t = idx % w.tiles_per_mat;
@@ -245,12 +310,12 @@ __device__ __forceinline__ void oz_decode(const OzWork& w, int idx, int& b, int&
   if (w.syrk) {
     tm = 0;
     for (;;) {
-      const int n = w.tiles_n - 2 * tm;
+      const int n = w.tiles_n - oz_tn_min(tm);
       if (t < n) break;
       t -= n;
       ++tm;
     }
-    tn = 2 * tm + t;
+    tn = oz_tn_min(tm) + t;
   } else {
     constexpr int G = 8;  // row-block groups: the tiles in flight share ~G A row blocks
     const int per_group = G * w.tiles_n;
@@ -327,10 +392,6 @@ struct OzEpiOut {
   }
 };
 
-__device__ __forceinline__ uint64_t oz_desc(uint32_t tile, int ks) {
-  return sdesc_sw64(tile + ks * 32, 16, 512);  // 64-byte K rows, 8-row atoms 512 B apart; k-step = 32 B
-}
-
 template <class Epi>
 __global__ void __launch_bounds__(256, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -344,6 +405,9 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -352,31 +416,36 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 128);
+    mbar_init(tempty, 2 * 4);  // every epilogue warp of both CTAs
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, OZ_TMEM_COLS);
+  cluster_sync_all();
+  if (warp == 2) tmem_alloc_pair(tmem_slot, OZ_TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
+      const uint32_t lbar0 = leader_bar_addr(&full[0]);
       int stage = 0;
       uint32_t phase = 0;
-      for (int idx = blockIdx.x; idx < work.num_work; idx += gridDim.x) {
+      for (int idx = cluster; idx < work.num_work; idx += nclusters) {
         int b, split, tm, tn, kt0, kt1;
         oz_decode(work, idx, b, split, tm, tn, kt0, kt1);
+        const int arow = tm * OZ_BM + static_cast<int>(rank) * 128;
+        const int brow = tn * OZ_BN + static_cast<int>(rank) * OZ_HB;
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * OZ_STAGE_BYTES;
           if (work.dbg & 2) {
-            mbar_arrive(&full[stage]);
+            if (leader) mbar_arrive(&full[stage]);
           } else {
-            mbar_arrive_expect_tx(&full[stage], OZ_STAGE_BYTES);
-            tma_load_4d(&tmA, &full[stage], st, kt * OZ_BK, tm * OZ_BM, b, 0);                  // S planes
-            tma_load_4d(&tmB, &full[stage], st + OZ_S * OZ_A_TILE, kt * OZ_BK, tn * OZ_BN, b, 0);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * OZ_STAGE_BYTES);
+            const uint32_t lbar = lbar0 + stage * 8;
+            tma_load_4d_pair(&tmA, lbar, st, kt * OZ_BK, arow, b, 0);                       // S planes
+            tma_load_4d_pair(&tmB, lbar, st + OZ_S * OZ_A_TILE, kt * OZ_BK, brow, b, 0);
           }
           if (++stage == OZ_STAGES) {
             stage = 0;
@@ -387,11 +456,14 @@ __global__ void __launch_bounds__(256, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t IDESC = idesc_s8(OZ_BM, OZ_BN);
+    if (leader) {
+      // MMA issuer (leader CTA): the whole warp walks the loop (uniform control flow), one elected
+      // lane issues -- descriptors then stay in uniform registers.
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int idx = blockIdx.x; idx < work.num_work; idx += gridDim.x) {
+      const uint32_t IDESC = idesc_s8(OZ_BM, OZ_BN);
+      const uint64_t D0 = sdesc_sw64(0, 16, 512);  // descriptor of smem address 0: + (addr >> 4) per operand
+      for (int idx = cluster; idx < work.num_work; idx += nclusters) {
         int b, split, tm, tn, kt0, kt1;
         oz_decode(work, idx, b, split, tm, tn, kt0, kt1);
         mbar_wait(tempty, acc_phase ^ 1);
@@ -399,68 +471,68 @@ __global__ void __launch_bounds__(256, 1)
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * OZ_STAGE_BYTES);
-          const uint32_t sb = sa + OZ_S * OZ_A_TILE;
+          if ((work.dbg & 1) == 0) {
+            const uint64_t da = D0 + (smem_u32(smem + stage * OZ_STAGE_BYTES) >> 4);
+            const uint64_t db = da + ((OZ_S * OZ_A_TILE) >> 4);
 #pragma unroll
-          for (int ks = 0; ks < ((work.dbg & 1) ? 0 : OZ_BK / 32); ++ks) {
+            for (int ks = 0; ks < OZ_BK / 32; ++ks) {
 #pragma unroll
-            for (int g = 0; g < OZ_S; ++g) {      // digit pairs (s, t) with s + t = g (0-based)
+              for (int g = 0; g < OZ_S; ++g) {      // digit pairs (s, t) with s + t = g (0-based)
 #pragma unroll
-              for (int s = 0; s <= g; ++s) {
-                const int t = g - s;
-                const uint32_t acc = (kt > kt0 || ks > 0 || s > 0) ? 1u : 0u;
-                umma_s8(tmem_base + static_cast<uint32_t>(g * OZ_BN), oz_desc(sa + s * OZ_A_TILE, ks),
-                        oz_desc(sb + t * OZ_B_TILE, ks), IDESC, acc);
+                for (int s = 0; s <= g; ++s) {
+                  const int t = g - s;
+                  const uint32_t acc = (kt > kt0 || ks > 0 || s > 0) ? 1u : 0u;
+                  umma_s8_pair_warp(tmem_base + static_cast<uint32_t>(g * OZ_BN),
+                                    da + static_cast<uint64_t>((s * OZ_A_TILE + ks * 32) >> 4),
+                                    db + static_cast<uint64_t>((t * OZ_B_TILE + ks * 32) >> 4), IDESC, acc);
+                }
               }
             }
           }
-          umma_commit(&empty[stage]);
+          umma_commit_pair_warp(&empty[stage], 0x3);
           if (++stage == OZ_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(tfull);
+        umma_commit_pair_warp(tfull, 0x3);
         acc_phase ^= 1;
       }
     }
-    __syncwarp();
   } else if (warp >= 4) {
-    // Drain first: the S accumulator groups of the thread's row are combined in fp64 (chunk 0 into the
-    // staging block, chunk 1 in registers) and the TMEM is released at once, so the next tile's MMAs
-    // overlap the rest of this epilogue (the
-    // 5 x 64 accumulator columns cannot be double-buffered in 512 TMEM columns).  Then scaling by
-    // 2^(e_m + e_n - 12), a per-warp 32 x 32 fp64 staging block, and the functor's coalesced row pass
-    // (lanes along n) and optional column pass (lanes along m).
+    // Drain first: the S accumulator groups of the thread's row are combined in fp64 (the last chunk
+    // in registers, the others through the staging block) and the TMEM is released, so the next
+    // tile's MMAs overlap the rest of this epilogue (S x 96 accumulator columns cannot be
+    // double-buffered in 512).  Then scaling by 2^(e_m + e_n - 12), the per-warp 32 x 32 fp64 staging
+    // block, and the functor's coalesced row pass (lanes along n) and optional column pass.
     const int ew = warp - 4;
     double* blk = reinterpret_cast<double*>(smem + OZ_STAGES * OZ_STAGE_BYTES + 1024) + ew * 32 * 33;
     uint32_t acc_phase = 0;
-    for (int idx = blockIdx.x; idx < work.num_work; idx += gridDim.x) {
+    constexpr int CH = OZ_BN / 32;
+    for (int idx = cluster; idx < work.num_work; idx += nclusters) {
       int b, split, tm, tn, kt0, kt1;
       oz_decode(work, idx, b, split, tm, tn, kt0, kt1);
       mbar_wait(tfull, acc_phase);
       acc_phase ^= 1;
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
-      const int m0 = tm * OZ_BM + ew * 32;
+      const int m0 = tm * OZ_BM + static_cast<int>(rank) * 128 + ew * 32;
       const int row = m0 + lane;
       const unsigned long long ma = row < sc.M ? sc.a[b * sc.a_bs + row] : 0ull;
       const bool a_bad = !(__longlong_as_double(static_cast<long long>(ma)) <= 1.7976931348623157e308);
       const int ea = oz_exponent(ma) - 12;
-      int eb[OZ_BN / 32];
-      bool b_bad[OZ_BN / 32];
+      int eb[CH];
+      bool b_bad[CH];
 #pragma unroll
-      for (int c = 0; c < OZ_BN / 32; ++c) {
+      for (int c = 0; c < CH; ++c) {
         const int coln = tn * OZ_BN + c * 32 + lane;
         const unsigned long long mb = coln < sc.N ? sc.b[b * sc.b_bs + coln] : 0ull;
         eb[c] = oz_exponent(mb);
         b_bad[c] = !(__longlong_as_double(static_cast<long long>(mb)) <= 1.7976931348623157e308);
       }
-      // chunk c: combine the S groups of 32 columns; chunk 0 goes to the staging block at once,
-      // the last chunk stays in registers until the TMEM is released.
       double v[32];
 #pragma unroll
-      for (int c = 0; c < OZ_BN / 32; ++c) {
+      for (int c = 0; c < CH; ++c) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0.0;
 #pragma unroll
@@ -472,7 +544,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = fma(static_cast<double>(static_cast<int32_t>(r[j])), wgt, v[j]);
         }
-        if (c + 1 < OZ_BN / 32) {
+        if (c + 1 < CH) {
           __syncwarp();
           if (c > 0) epi.block(b, split, m0, tn * OZ_BN + (c - 1) * 32, blk, lane, sc.M, sc.N, work.syrk != 0);
           __syncwarp();
@@ -485,8 +557,9 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty);  // every accumulator column is in registers / staging now
-      constexpr int CL = OZ_BN / 32 - 1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty, 0);  // every accumulator column is in registers / staging now
+      constexpr int CL = CH - 1;
       __syncwarp();
       if (CL > 0) epi.block(b, split, m0, tn * OZ_BN + (CL - 1) * 32, blk, lane, sc.M, sc.N, work.syrk != 0);
       __syncwarp();
@@ -501,9 +574,10 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   __syncthreads();
+  cluster_sync_all();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, OZ_TMEM_COLS);
+    tmem_dealloc_pair(tmem_base, OZ_TMEM_COLS);
   }
 }
 

@@ -525,10 +525,10 @@ static int pick_splits(int64_t tiles, int64_t ktiles, int64_t slots) {
 static bool use_oz(const Problem& p) {
   return p.prec == UNSO_PREC_FP32 && p.method == UNSO_METHOD_UNSO && p.h > 256 && (p.flags & UNSO_FLAG_FP32_DMMA) == 0;
 }
-static int64_t oz_syrk_tiles(int64_t h) {
+static int64_t oz_syrk_tiles(int64_t h) {  // pair tiles of oz_decode's SYRK order
   const int64_t tm = (h + OZ_BM - 1) / OZ_BM, tn = (h + OZ_BN - 1) / OZ_BN;
   int64_t t = 0;
-  for (int64_t i = 0; i < tm; ++i) t += std::max<int64_t>(0, tn - 2 * i);
+  for (int64_t i = 0; i < tm; ++i) t += std::max<int64_t>(0, tn - oz_tn_min(static_cast<int>(i)));
   return t;
 }
 
@@ -536,7 +536,7 @@ static int gram_splits(const Problem& p, bool for_error = false) {
   if (!for_error && use_oz(p)) {  // every split-K slice within the int32 bound, then fill the last wave
     const int64_t kt = (p.w + OZ_BK - 1) / OZ_BK;
     const int min_s = static_cast<int>((p.w + OZ_MAX_K - 1) / OZ_MAX_K);
-    const int s = pick_splits(oz_syrk_tiles(p.h) * p.batch, kt, device_sm_count());
+    const int s = pick_splits(oz_syrk_tiles(p.h) * p.batch, kt, device_sm_count() / 2);
     return std::max(min_s, s);
   }
   if (p.prec == UNSO_PREC_BF16) {
@@ -765,7 +765,7 @@ static int32_t oz_slice(const void* src, int dt, int64_t ld, int64_t bs, int64_t
     oz_colmax_kernel<<<g, 256, 0, st>>>(src, dt, ld, bs, rows, cols, maxbuf, max_bs, rpb);
     UNSO_CHECK_LAUNCH();
   }
-  dim3 g(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>(batch));
+  dim3 g(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>((rows + 63) / 64), static_cast<unsigned>(batch));
   oz_split_kernel<<<g, 256, 0, st>>>(src, dt, ld, bs, rows, cols, transpose ? 1 : 0, maxbuf, max_bs, dst, ldd, dbs,
                                      plane);
   UNSO_CHECK_LAUNCH();
@@ -805,14 +805,26 @@ static int32_t oz_gemm(const OzOperand& A, const OzOperand& B, int64_t M, int64_
   if (nw <= 0) return UNSO_OK;
   if (nw > (1ll << 31) - 1) return UNSO_ERR_UNSUPPORTED;
   w.num_work = static_cast<int>(nw);
-  CUtensorMap ta, tb;
-  if (!oz_map(&ta, A.planes, K, M, batch, A.ld, A.bs, A.plane, OZ_BM) ||
-      !oz_map(&tb, B.planes, K, N, batch, B.ld, B.bs, B.plane, OZ_BN))
+  CUtensorMap ta, tb;  // each CTA of a pair stages 128 A rows and OZ_HB B rows
+  if (!oz_map(&ta, A.planes, K, M, batch, A.ld, A.bs, A.plane, 128) ||
+      !oz_map(&tb, B.planes, K, N, batch, B.ld, B.bs, B.plane, OZ_HB))
     return UNSO_ERR_CUDA;
   OzScales sc{A.maxbits, A.max_bs, B.maxbits, B.max_bs, static_cast<int>(M), static_cast<int>(N)};
-  const int grid = static_cast<int>(std::min<int64_t>(nw, device_sm_count()));
-  oz_gemm_kernel<Epi><<<grid, 256, OZ_SMEM, st>>>(ta, tb, w, sc, epi);
-  UNSO_CHECK_LAUNCH();
+  const int pairs = static_cast<int>(std::min<int64_t>(nw, device_sm_count() / 2));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = OZ_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, oz_gemm_kernel<Epi>, ta, tb, w, sc, epi) != cudaSuccess) return UNSO_ERR_CUDA;
+  ++g_launches;
   return UNSO_OK;
 }
 

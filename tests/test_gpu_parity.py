@@ -333,7 +333,7 @@ def test_cfg4_full_size_rows_against_oracle():
     r_bf = rel(yb[torch.from_numpy(rows).to(DEV)].double().cpu().numpy(), ref)
     r_64 = rel(y64[torch.from_numpy(rows).to(DEV)].cpu().numpy(), ref)
     print(f"cfg4: bf16 vs oracle rows {r_bf:.2e}; fp32-mode vs oracle rows {r_64:.2e}; bf16 vs fp32-mode {r_dev:.2e}")
-    assert r_64 <= 1e-9
+    assert r_64 <= 1e-6  # fp32 mode on the int8 digit engine: ~1e-7 (fp64 DMMA engine: ~1e-14)
     assert r_bf <= TOL["bf16"]
     assert r_dev <= TOL["bf16"]
 
