@@ -12,6 +12,7 @@
 //       finalize P: P/s, symmetric, split for the apply          (ortho.py:167 folded)
 //   K3  apply Y = X P (tall) or P X (wide), written in the input dtype   (ortho.py:205, :275-276)
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -52,7 +53,28 @@ struct Profiler {
 static Profiler g_prof;
 static thread_local bool g_prof_call = false;
 constexpr int PROF_EV = UNSO_PROFILE_STAGES + 1;
+// NVTX ranges (header-only NVTX v3: inert unless a tool such as nsys / ncu --nvtx is attached): one
+// range per stage of an orthogonalization, opened and closed at the same marks as the profiler's events.
+static nvtxDomainHandle_t nvtx_domain() {
+  static nvtxDomainHandle_t d = nvtxDomainCreateA("unso_b200");
+  return d;
+}
+static thread_local nvtxRangeId_t g_nvtx_range = 0;
+static void nvtx_stage(int idx) {
+  static const char* const names[UNSO_PROFILE_STAGES] = {"unso.convert", "unso.gram", "unso.scale_prep",
+                                                         "unso.chain", "unso.finalize_p", "unso.apply"};
+  if (g_nvtx_range) nvtxDomainRangeEnd(nvtx_domain(), g_nvtx_range);
+  g_nvtx_range = 0;
+  if (idx < 0 || idx >= UNSO_PROFILE_STAGES) return;
+  nvtxEventAttributes_t a = {};
+  a.version = NVTX_VERSION;
+  a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+  a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+  a.message.ascii = names[idx];
+  g_nvtx_range = nvtxDomainRangeStartEx(nvtx_domain(), &a);
+}
 static void prof_mark(int idx, cudaStream_t st) {
+  nvtx_stage(idx);  // mark idx opens stage idx (the profiler's stage idx runs from mark idx to idx + 1)
   if (g_prof_call && g_prof.on && g_prof.n < g_prof.cap) cudaEventRecord(g_prof.ev[g_prof.n * PROF_EV + idx], st);
 }
 
@@ -1865,6 +1887,7 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
   struct ProfGuard {
     ProfGuard() { g_prof_call = true; }
     ~ProfGuard() {
+      nvtx_stage(-1);  // close the last stage range (also on an early error return)
       if (g_prof.on && g_prof.n < g_prof.cap) ++g_prof.n;
       g_prof_call = false;
     }
