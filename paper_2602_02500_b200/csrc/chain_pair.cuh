@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {  // whole warp walks the loop, one elected lane issues (uniform descriptors)
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int idx = cluster; idx < work.num_work; idx += nclusters) {
@@ -127,19 +127,19 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
                                      : operand_desc<false>(st + 2 * SC_TILE, ks);
             const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * SC_TILE, ks)
                                      : operand_desc<false>(st + 3 * SC_TILE, ks);
-            umma_bf16_pair(d_tmem, ah, bh, idesc, (kt > kt0 || ks > 0) ? 1u : 0u);
+            umma_bf16_pair_warp(d_tmem, ah, bh, idesc, (kt > kt0 || ks > 0) ? 1u : 0u);
             if (!work.no_cross) {
-              umma_bf16_pair(d_tmem, ah, bl, idesc, 1u);
-              umma_bf16_pair(d_tmem, al, bh, idesc, 1u);
+              umma_bf16_pair_warp(d_tmem, ah, bl, idesc, 1u);
+              umma_bf16_pair_warp(d_tmem, al, bh, idesc, 1u);
             }
           }
-          umma_commit_pair(&empty[stage], 0x3);
+          umma_commit_pair_warp(&empty[stage], 0x3);
           if (++stage == SC_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(&tfull[acc], 0x3);
+        umma_commit_pair_warp(&tfull[acc], 0x3);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {  // whole warp walks the loop, one elected lane issues (uniform descriptors)
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int idx = cluster; idx < work.num_work; idx += nclusters) {
@@ -369,21 +369,21 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ah = a_mn ? operand_desc<true>(st, ks) : operand_desc<false>(st, ks);
             const uint64_t bh = b_mn ? operand_desc<true>(st + OFF_BH, ks) : operand_desc<false>(st + OFF_BH, ks);
-            umma_bf16_pair(d_tmem, ah, bh, id16, (kt > kt0 || ks > 0) ? 1u : 0u);
+            umma_bf16_pair_warp(d_tmem, ah, bh, id16, (kt > kt0 || ks > 0) ? 1u : 0u);
           }
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
             if (work.no_cross) break;
-            umma_f8_pair(d_tmem, f8_desc(st + OFF_A8, a_mn, 0, ks), f8_desc(st + OFF_B8, b_mn, 1, ks), id8, 1u);
-            umma_f8_pair(d_tmem, f8_desc(st + OFF_A8, a_mn, 1, ks), f8_desc(st + OFF_B8, b_mn, 0, ks), id8, 1u);
+            umma_f8_pair_warp(d_tmem, f8_desc(st + OFF_A8, a_mn, 0, ks), f8_desc(st + OFF_B8, b_mn, 1, ks), id8, 1u);
+            umma_f8_pair_warp(d_tmem, f8_desc(st + OFF_A8, a_mn, 1, ks), f8_desc(st + OFF_B8, b_mn, 0, ks), id8, 1u);
           }
-          umma_commit_pair(&empty[stage], 0x3);
+          umma_commit_pair_warp(&empty[stage], 0x3);
           if (++stage == F8_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(&tfull[acc], 0x3);
+        umma_commit_pair_warp(&tfull[acc], 0x3);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;

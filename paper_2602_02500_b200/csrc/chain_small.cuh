@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------------------------------------------------------- MMA issuer
+    {
+      // ---------------------------------------------------------------- MMA issuer (whole warp, one
+      // elected lane issues: descriptors stay in uniform registers)
       const uint32_t idesc = idesc_bf16(128, 128, 0, 0);
       const uint32_t hi = smem_u32(c_hi), lo = smem_u32(c_lo);
       uint32_t phase = 0;
@@ -106,11 +107,11 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t d = operand_desc<true>(st, ks);
-            umma_bf16(tmem + CH_ACC, d, d, gdesc, (kt > 0 || ks > 0) ? 1u : 0u);
+            umma_bf16_warp(tmem + CH_ACC, d, d, gdesc, (kt > 0 || ks > 0) ? 1u : 0u);
           }
-          umma_commit(&gempty[s]);
+          umma_commit_warp(&gempty[s]);
         }
-        umma_commit(tfull);
+        umma_commit_warp(tfull);
       }
       for (int k = 1; k < N; ++k) {
         mbar_wait(ready, phase);  // C_k's operands in shared memory (and the truncation verdict)
@@ -122,11 +123,11 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
           const uint32_t off = (ks >> 2) * CS_CHUNK;
           const uint64_t dh = operand_desc<false>(hi + off, ks & 3);
           const uint64_t dl = operand_desc<false>(lo + off, ks & 3);
-          umma_bf16(tmem + CH_ACC, dh, dh, idesc, ks > 0 ? 1u : 0u);
-          umma_bf16(tmem + CH_ACC, dh, dl, idesc, 1u);
-          umma_bf16(tmem + CH_ACC, dl, dh, idesc, 1u);
+          umma_bf16_warp(tmem + CH_ACC, dh, dh, idesc, ks > 0 ? 1u : 0u);
+          umma_bf16_warp(tmem + CH_ACC, dh, dl, idesc, 1u);
+          umma_bf16_warp(tmem + CH_ACC, dl, dh, idesc, 1u);
         }
-        umma_commit(tfull);
+        umma_commit_warp(tfull);
       }
     }
     __syncwarp();

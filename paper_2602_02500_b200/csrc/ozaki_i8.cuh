@@ -63,15 +63,6 @@ __device__ __forceinline__ void umma_s8_pair_warp(uint32_t d_tmem, uint64_t ades
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void umma_commit_pair_warp(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
 __device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* m, uint32_t leader_bar, void* smem_dst, int c0,
                                                  int c1, int c2, int c3) {
   asm volatile(

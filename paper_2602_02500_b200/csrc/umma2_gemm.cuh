@@ -177,8 +177,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader) {
+      // ------------------------------------------------------------ MMA issuer (leader only): the whole
+      // warp walks the loop, one elected lane issues (descriptors stay in uniform registers)
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int idx = cluster; idx < work.num_work; idx += nclusters) {
@@ -203,23 +204,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
               if (skip && ((Cfg::OPT == 1 && bi == 1) || (Cfg::OPT == 2 && ai == 1))) continue;
               const uint64_t ad = operand_desc<Cfg::A_MN>(st + ai * Cfg::A_TILE, ks);
               const uint64_t bd = operand_desc<Cfg::B_MN>(sb + bi * Cfg::B_TILE, ks);
-              umma_bf16_pair(d_tmem, ad, bd, Cfg::IDESC, (kt > kt0 || ks > 0 || t > 0) ? 1u : 0u);
+              umma_bf16_pair_warp(d_tmem, ad, bd, Cfg::IDESC, (kt > kt0 || ks > 0 || t > 0) ? 1u : 0u);
             }
           }
-          umma_commit_pair(&empty[stage], 0x3);
+          umma_commit_pair_warp(&empty[stage], 0x3);
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(&tfull[acc], 0x3);
+        umma_commit_pair_warp(&tfull[acc], 0x3);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
     }
-    __syncwarp();
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue (both CTAs)
     const int ew = warp - 4;
