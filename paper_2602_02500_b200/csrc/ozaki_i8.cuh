@@ -38,7 +38,7 @@ constexpr int OZ_STAGES = 3;
 constexpr int OZ_A_TILE = 128 * OZ_BK;         // 8 KB per digit plane (the CTA's 128 A rows)
 constexpr int OZ_B_TILE = OZ_HB * OZ_BK;       // 3 KB
 constexpr int OZ_STAGE_BYTES = OZ_S * (OZ_A_TILE + OZ_B_TILE);  // per CTA
-constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE_BYTES + 1024 + 4 * 32 * 33 * 8 + 1024;  // stages, barriers, staging
+constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE_BYTES + 1024 + 1024;  // stages, barriers, alignment slack
 constexpr uint32_t OZ_TMEM_COLS = 512;         // OZ_S * OZ_BN = 480 used
 constexpr int64_t OZ_MAX_K = 65536;            // 5 * 64 * 64 * 65536 < 2^31
 static_assert(OZ_S * OZ_BN <= 512, "tmem");
@@ -334,40 +334,59 @@ __device__ __forceinline__ double oz_pow2(int k) {
   return ldexp(1.0, k);
 }
 
-// Block functors: blk[r * 33 + c] = D(m0 + r, n0 + c), r, c < 32; `lane` is the caller's lane.
-// Row pass: lanes along n (coalesced row segments); SYRK keeps n >= m.
-#define OZ_ROW_PASS(body)                                           \
-  for (int r = 0; r < 32; ++r) {                                    \
-    const int m = m0 + r, n = n0 + lane;                            \
-    if (m >= M || n >= N || (syrk && n < m)) continue;              \
-    const double v = blk[r * 33 + lane];                            \
-    body;                                                           \
+// Row functors: the calling thread owns output row `row`, columns n0 .. n0 + 31 (v[j] = D(row, n0 + j)).
+// Full in-bounds segments go out as 32-byte vector stores (each lane writes whole sectors of its own
+// row: no shared-memory transpose -- the epilogue runs one warp per scheduler and its per-element
+// instruction count sets the time of short-K tiles); edges and misaligned rows element by element.
+// SYRK keeps n >= row.
+__device__ __forceinline__ void oz_store_row_f64(double* dst, int row, int n0, const double (&v)[32], int M, int N,
+                                                 bool syrk) {
+  if (row >= M) return;
+  const bool full = n0 + 32 <= N && !(syrk && n0 < row) && (reinterpret_cast<uintptr_t>(dst) & 31) == 0;
+  if (full) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      uint32_t w[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v[j + q]));
+        w[2 * q] = static_cast<uint32_t>(u);
+        w[2 * q + 1] = static_cast<uint32_t>(u >> 32);
+      }
+      st_global_v8(dst + j, w);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (n0 + j < N && !(syrk && n0 + j < row)) dst[j] = v[j];
   }
+}
 
 // Gram split-K partial (fp64), the layout of EpiPartialF64 / finalize_sum_kernel.
 struct OzEpiPartial {
   double* part;
   int64_t bs, ld;
   int batch;
-  __device__ void block(int b, int split, int m0, int n0, const double* blk, int lane, int M, int N, bool syrk) const {
-    double* base = part + (static_cast<int64_t>(split) * batch + b) * bs;
-    OZ_ROW_PASS(base[static_cast<int64_t>(m) * ld + n] = v);
+  __device__ void rows(int b, int split, int row, int n0, const double (&v)[32], int M, int N, bool syrk) const {
+    double* dst = part + (static_cast<int64_t>(split) * batch + b) * bs + static_cast<int64_t>(row) * ld + n0;
+    oz_store_row_f64(dst, row, n0, v, M, N, syrk);
   }
 };
 
-// Symmetric product S = C C^T (the squaring): upper tile rows, then the mirror through the staging
-// block (lanes along m) -- stores only; oz_chain_step_kernel consumes S row by row.
+// Symmetric product S = C C^T (the squaring): the upper row segment, then the mirror -- for a fixed
+// column the 32 lanes of the warp hold 32 consecutive rows, so S[n][row] is one coalesced 256-byte
+// store per column.  Stores only; oz_chain_step_kernel consumes S row by row.
 struct OzEpiSym {
   double* out;
   int64_t ld, bs;
-  __device__ void block(int b, int, int m0, int n0, const double* blk, int lane, int M, int N, bool syrk) const {
+  __device__ void rows(int b, int, int row, int n0, const double (&v)[32], int M, int N, bool syrk) const {
     double* base = out + static_cast<int64_t>(b) * bs;
-    OZ_ROW_PASS(base[static_cast<int64_t>(m) * ld + n] = v);
-    const int m = m0 + lane;
-#pragma unroll 4
-    for (int c = 0; c < 32; ++c) {
-      const int n = n0 + c;
-      if (m < M && n < N && n > m) base[static_cast<int64_t>(n) * ld + m] = blk[lane * 33 + c];
+    oz_store_row_f64(base + static_cast<int64_t>(row) * ld + n0, row, n0, v, M, N, syrk);
+    if (row >= M) return;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = n0 + j;
+      if (n > row && n < N) base[static_cast<int64_t>(n) * ld + row] = v[j];
     }
   }
 };
@@ -377,9 +396,45 @@ struct OzEpiOut {
   void* out;
   int dt;
   int64_t ld, bs;
-  __device__ void block(int b, int, int m0, int n0, const double* blk, int lane, int M, int N, bool syrk) const {
-    const int64_t base = static_cast<int64_t>(b) * bs;
-    OZ_ROW_PASS(store_from_f64(out, base + static_cast<int64_t>(m) * ld + n, dt, v));
+  __device__ void rows(int b, int, int row, int n0, const double (&v)[32], int M, int N, bool) const {
+    if (row >= M) return;
+    const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + n0;
+    if (dt == DT_F64) {
+      oz_store_row_f64(static_cast<double*>(out) + o, row, n0, v, M, N, false);
+      return;
+    }
+    if (dt == DT_F32) {
+      float* dst = static_cast<float*>(out) + o;
+      if (n0 + 32 <= N && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint32_t w[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) w[q] = __float_as_uint(static_cast<float>(v[j + q]));
+          st_global_v8(dst + j, w);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < N) dst[j] = static_cast<float>(v[j]);
+      }
+      return;
+    }
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + o;
+    if (n0 + 32 <= N && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 16) {
+        uint32_t w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          w[q] = pack_bf16x2(static_cast<float>(v[j + 2 * q]), static_cast<float>(v[j + 2 * q + 1]));
+        st_global_v8(dst + j, w);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) dst[j] = __float2bfloat16_rn(static_cast<float>(v[j]));
+    }
   }
 };
 
@@ -497,7 +552,6 @@ __global__ void __launch_bounds__(256, 1)
     // double-buffered in 512).  Then scaling by 2^(e_m + e_n - 12), the per-warp 32 x 32 fp64 staging
     // block, and the functor's coalesced row pass (lanes along n) and optional column pass.
     const int ew = warp - 4;
-    double* blk = reinterpret_cast<double*>(smem + OZ_STAGES * OZ_STAGE_BYTES + 1024) + ew * 32 * 33;
     uint32_t acc_phase = 0;
     constexpr int CH = OZ_BN / 32;
     for (int idx = cluster; idx < work.num_work; idx += nclusters) {
@@ -511,57 +565,51 @@ __global__ void __launch_bounds__(256, 1)
       const int row = m0 + lane;
       const unsigned long long ma = row < sc.M ? sc.a[b * sc.a_bs + row] : 0ull;
       const bool a_bad = !(__longlong_as_double(static_cast<long long>(ma)) <= 1.7976931348623157e308);
-      const int ea = oz_exponent(ma) - 12;
-      int eb[CH];
-      bool b_bad[CH];
+      // The S groups of an element are combined exactly in int64 (Q = sum_g acc_g 128^(S-1-g), |Q| < 2^60:
+      // integer multiply-adds instead of S fp64 FMAs), rounded once to fp64 and scaled by the exact powers
+      // of two 2^(e_m - 12 - 7(S-1)) (row) and 2^(e_n) (column).  The epilogue runs one warp per scheduler,
+      // so its per-element instruction count sets the tile time of short-K tiles.  All three chunks are drained before the TMEM is released
+      // (chunk 0 to the staging block, chunks 1 and 2 in registers), so the next tile's MMAs start early.
+      // exact power-of-two scales (NaN marks a non-finite operand row / column and propagates)
+      const double rowscale = a_bad ? __longlong_as_double(0x7FF8000000000000ll)
+                                    : oz_pow2(oz_exponent(ma) - 12 - 7 * (OZ_S - 1));
+      double colscale[CH];  // lane j: scale of column (chunk start + j), shuffled per element
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const int coln = tn * OZ_BN + c * 32 + lane;
         const unsigned long long mb = coln < sc.N ? sc.b[b * sc.b_bs + coln] : 0ull;
-        eb[c] = oz_exponent(mb);
-        b_bad[c] = !(__longlong_as_double(static_cast<long long>(mb)) <= 1.7976931348623157e308);
+        const bool bad = !(__longlong_as_double(static_cast<long long>(mb)) <= 1.7976931348623157e308);
+        colscale[c] = bad ? __longlong_as_double(0x7FF8000000000000ll) : oz_pow2(oz_exponent(mb));
       }
-      double v[32];
+      auto drain = [&](int c, long long (&q)[32]) {
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.0;
+        for (int j = 0; j < 32; ++j) q[j] = 0;
 #pragma unroll
         for (int g = 0; g < OZ_S; ++g) {
           uint32_t r[32];
           tmem_ld32(taddr + g * OZ_BN + c * 32, r);
           tmem_wait_ld();
-          const double wgt = oz_pow2(-7 * g);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = fma(static_cast<double>(static_cast<int32_t>(r[j])), wgt, v[j]);
+          for (int j = 0; j < 32; ++j) q[j] = q[j] * 128 + static_cast<long long>(static_cast<int32_t>(r[j]));
         }
-        if (c + 1 < CH) {
-          __syncwarp();
-          if (c > 0) epi.block(b, split, m0, tn * OZ_BN + (c - 1) * 32, blk, lane, sc.M, sc.N, work.syrk != 0);
-          __syncwarp();
+      };
+      auto emit = [&](int c, const long long (&q)[32]) {
+        double v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int ej = __shfl_sync(0xffffffffu, eb[c], j);
-            const bool bj = __shfl_sync(0xffffffffu, b_bad[c] ? 1 : 0, j) != 0;
-            blk[lane * 33 + j] = (a_bad || bj) ? __longlong_as_double(0x7FF8000000000000ll) : v[j] * oz_pow2(ea + ej);
-          }
-        }
-      }
+        for (int j = 0; j < 32; ++j) v[j] = __ll2double_rn(q[j]) * rowscale * __shfl_sync(0xffffffffu, colscale[c], j);
+        epi.rows(b, split, row, tn * OZ_BN + c * 32, v, sc.M, sc.N, work.syrk != 0);
+      };
+      static_assert(CH == 3, "the epilogue is written for 96-column tiles");
+      long long v0[32], v1[32], v2[32];
+      drain(0, v0);
+      drain(1, v1);
+      drain(2, v2);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty, 0);  // every accumulator column is in registers / staging now
-      constexpr int CL = CH - 1;
-      __syncwarp();
-      if (CL > 0) epi.block(b, split, m0, tn * OZ_BN + (CL - 1) * 32, blk, lane, sc.M, sc.N, work.syrk != 0);
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int ej = __shfl_sync(0xffffffffu, eb[CL], j);
-        const bool bj = __shfl_sync(0xffffffffu, b_bad[CL] ? 1 : 0, j) != 0;
-        blk[lane * 33 + j] = (a_bad || bj) ? __longlong_as_double(0x7FF8000000000000ll) : v[j] * oz_pow2(ea + ej);
-      }
-      __syncwarp();
-      epi.block(b, split, m0, tn * OZ_BN + CL * 32, blk, lane, sc.M, sc.N, work.syrk != 0);
+      if (lane == 0) mbar_arrive_cluster(tempty, 0);  // every accumulator column is in registers now
+      emit(0, v0);
+      emit(1, v1);
+      emit(2, v2);
     }
   }
   __syncthreads();

@@ -1923,6 +1923,9 @@ int32_t unso_orthogonalize(const unso_matrix_desc* x, const void* x_ptr, void* y
 extern "C" int32_t unso_debug_chain_trace(unsigned long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, g_chain_trace, sizeof(g_chain_trace)) == cudaSuccess ? UNSO_OK : UNSO_ERR_CUDA;
 }
+extern "C" int32_t unso_debug_oz_trace(unsigned long long* host_out) {  // 2 x 16 x 8 timestamps
+  return cudaMemcpyFromSymbol(host_out, g_oz_trace, sizeof(g_oz_trace)) == cudaSuccess ? UNSO_OK : UNSO_ERR_CUDA;
+}
 extern "C" int32_t unso_debug_chain_kb(unsigned long long* host_out) {  // 2 x 64 per-k-block timestamps
   return cudaMemcpyFromSymbol(host_out, g_chain_kb, sizeof(g_chain_kb)) == cudaSuccess ? UNSO_OK : UNSO_ERR_CUDA;
 }
