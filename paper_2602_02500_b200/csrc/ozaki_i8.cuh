@@ -438,6 +438,19 @@ struct OzEpiOut {
   }
 };
 
+#ifdef UNSO_EXP_TIMING  // timing experiment only (tools/oz_trace.py): per-tile events of pair 0
+__device__ unsigned long long g_oz_trace[2][16][8];
+__device__ __forceinline__ void oz_trace(int t, int ev) {
+  if ((blockIdx.x >> 1) != 0 || t >= 16) return;
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  g_oz_trace[blockIdx.x & 1][t][ev] = v;
+}
+#define OZ_TRACE(t, ev) oz_trace(t, ev)
+#else
+#define OZ_TRACE(t, ev)
+#endif
+
 template <class Epi>
 __global__ void __launch_bounds__(256, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -451,6 +464,7 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) OZ_TRACE(15, 0);
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
@@ -471,6 +485,7 @@ __global__ void __launch_bounds__(256, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) OZ_TRACE(15, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -514,6 +529,7 @@ __global__ void __launch_bounds__(256, 1)
         oz_decode(work, idx, b, split, tm, tn, kt0, kt1);
         mbar_wait(tempty, acc_phase ^ 1);
         tc_fence_after();
+        if (lane == 0) OZ_TRACE((idx - cluster) / nclusters, 2);
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -542,6 +558,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
         umma_commit_pair_warp(tfull, 0x3);
+        if (lane == 0) OZ_TRACE((idx - cluster) / nclusters, 3);
         acc_phase ^= 1;
       }
     }
@@ -560,6 +577,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(tfull, acc_phase);
       acc_phase ^= 1;
       tc_fence_after();
+      if (ew == 0 && lane == 0) OZ_TRACE((idx - cluster) / nclusters, 4);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
       const int m0 = tm * OZ_BM + static_cast<int>(rank) * 128 + ew * 32;
       const int row = m0 + lane;
@@ -607,9 +625,11 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty, 0);  // every accumulator column is in registers now
+      if (ew == 0 && lane == 0) OZ_TRACE((idx - cluster) / nclusters, 5);
       emit(0, v0);
       emit(1, v1);
       emit(2, v2);
+      if (ew == 0 && lane == 0) OZ_TRACE((idx - cluster) / nclusters, 6);
     }
   }
   __syncthreads();
