@@ -270,34 +270,46 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     if (tid == 0) CHAIN_TRACE(0, 0);
     double tr = 0.0, fr = 0.0;
     const double wgt = (ti == tj) ? 1.0 : 2.0;
+    // all four 32-column chunks of a split-K slice are loaded before any is summed: 32 independent
+    // 16-byte loads in flight per thread (the phase was load-latency-bound chunk by chunk)
+    float g4[4][32];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) g4[c][j] = 0.f;
+    if (row_ok) {
+      for (int sp = 0; sp < p.splits; ++sp) {
+        const float* src = p.part + (static_cast<int64_t>(sp) * p.batch + b) * p.part_mat +
+                           static_cast<int64_t>(gr) * p.part_ld + tj * 128;
+        float4 v[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = __ldcg(reinterpret_cast<const float4*>(src) + q);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          float* gq = &g4[q >> 3][(q & 7) * 4];
+          gq[0] += v[q].x;
+          gq[1] += v[q].y;
+          gq[2] += v[q].z;
+          gq[3] += v[q].w;
+        }
+      }
+    }
     for (int c = 0; c < 4; ++c) {
       const int gc0 = tj * 128 + c * 32;
       float g[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) g[j] = 0.f;
-      if (row_ok) {
-        for (int s = 0; s < p.splits; ++s) {
-          const float* src =
-              p.part + (static_cast<int64_t>(s) * p.batch + b) * p.part_mat + static_cast<int64_t>(gr) * p.part_ld + gc0;
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float4 v = *reinterpret_cast<const float4*>(src + j);
-            g[j] += v.x;
-            g[j + 1] += v.y;
-            g[j + 2] += v.z;
-            g[j + 3] += v.w;
-          }
-        }
-      }
+      for (int j = 0; j < 32; ++j) g[j] = g4[c][j];
       uint32_t u[32];
+      float frc = 0.f;  // fp32 partial over the 32 columns, accumulated in fp64 across chunks
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const bool ok = row_ok && (gc0 + j) < p.h;
         const float v = ok ? g[j] : 0.f;
         if (ok && gc0 + j == gr) tr += v;
-        fr += wgt * static_cast<double>(v) * v;
+        frc = fmaf(v, v, frc);
         u[j] = __float_as_uint(v);
       }
+      fr += wgt * static_cast<double>(frc);
       tmem_st32(lane_base + CH_C + c * 32, u);
     }
     tmem_wait_st();
@@ -340,7 +352,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     }
     named_bar_sync(1, 128);
     const float inv_s2 = static_cast<float>(s_scale[0]);
-    (void)0;
+    const float alpha_f = static_cast<float>(p.alpha);
 
     // ---- C_1 = G / s^2 (TMEM + global buffer 0), P = alpha I - coef_1 C_1 (TMEM)
     for (int c = 0; c < 4; ++c) {
@@ -352,10 +364,9 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       __align__(16) __nv_bfloat16 lo[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float cv = static_cast<float>(static_cast<double>(__uint_as_float(u[j])) * s_scale[0]);
+        const float cv = __uint_as_float(u[j]) * inv_s2;  // fp32 arithmetic: the state is fp32 anyway
         u[j] = __float_as_uint(cv);
-        const float pv = static_cast<float>(((gr == gc0 + j && row_ok) ? p.alpha : 0.0) -
-                                            static_cast<double>(p.coef[0]) * cv);
+        const float pv = fmaf(-p.coef[0], cv, (gr == gc0 + j && row_ok) ? alpha_f : 0.f);
         pu[j] = __float_as_uint(pv);
         split_bf16(cv, hi[j], lo[j]);
       }
@@ -371,7 +382,6 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       }
     }
     tmem_wait_st();
-    (void)inv_s2;
     fence_proxy_async_global();
     named_bar_sync(1, 128);
     if (tid == 0) {
@@ -479,13 +489,15 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         uint32_t up[32];
         tmem_ld32(lane_base + CH_P + c * 32, up);
         tmem_wait_ld();
+        float s2c = 0.f;  // fp32 partial over 32 columns, fp64 across chunks
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const bool ok = row_ok && gc0 + j < p.h;
-          const double v = ok ? static_cast<double>(__uint_as_float(up[j])) : 0.0;
+          const float v = ok ? __uint_as_float(up[j]) : 0.f;
           if (ok && gc0 + j == gr) trp += v;
-          sp2 += wgt * v * v;
+          s2c = fmaf(v, v, s2c);
         }
+        sp2 += wgt * static_cast<double>(s2c);
       }
       trp = warp_sum(trp);
       sp2 = warp_sum(sp2);
@@ -518,7 +530,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         s_scale[0] = d;
         if (t == 0) {
           double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
-          o[S_SHIFT] = d * s_scale[1];
+          o[S_SHIFT] = static_cast<double>(static_cast<float>(d)) * s_scale[1];  // the shift R was formed with
           o[S_MODE] = single ? 1.0 : 0.0;
           o[S_BOUND] = bound;
           o[S_STEPS] = steps;
@@ -526,6 +538,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       }
       named_bar_sync(1, 128);
       const double d = s_scale[0];
+      const float d_f = static_cast<float>(d), inv_s_f = static_cast<float>(s_scale[1]);
       if ((p.h & 31) == 0) {
         // Whole 32 x 32 blocks: every lane stores its row segment with 16-byte vector stores, and
         // the mirror block goes through a per-warp shared-memory transpose (the pipeline stages
@@ -542,9 +555,9 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
           uint32_t hl[32];                              // (hi << 16) | lo of row gr, columns gc0 + j
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const double rv = static_cast<double>(__uint_as_float(up[j])) - (gc0 + j == gr ? d : 0.0);
+            const float rv = __uint_as_float(up[j]) - (gc0 + j == gr ? d_f : 0.f);
             __nv_bfloat16 hi, lo;
-            split_bf16(static_cast<float>(rv * s_scale[1]), hi, lo);
+            split_bf16(rv * inv_s_f, hi, lo);
             hl[j] = (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16) | __bfloat16_as_ushort(lo);
           }
 #pragma unroll
@@ -602,9 +615,9 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
             for (int j = 0; j < 32; ++j) {
               const int gc = gc0 + j;
               if (gc >= p.h || (ti == tj && gc < gr)) continue;
-              const double rv = static_cast<double>(__uint_as_float(up[j])) - (gc == gr ? d : 0.0);
+              const float rv = __uint_as_float(up[j]) - (gc == gr ? d_f : 0.f);
               __nv_bfloat16 hi, lo;
-              split_bf16(static_cast<float>(rv * s_scale[1]), hi, lo);
+              split_bf16(rv * inv_s_f, hi, lo);
               const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
               const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
               p.phi[o] = hi;
