@@ -38,4 +38,4 @@ def test_five_digits_meet_the_fp32_bar_four_in_the_chain_do_not():
     err5 = np.linalg.norm(Z.unso_ozaki(m, 5, 5, 5) - ref) / np.linalg.norm(ref)
     err4 = np.linalg.norm(Z.unso_ozaki(m, 5, 4, 5) - ref) / np.linalg.norm(ref)
     assert err5 <= 1e-6, err5
-    assert err4 > err5
+    assert err4 > 1e-5, err4  # 4 chain digits: 1.2e-5, over the fp32-mode bar
