@@ -451,8 +451,10 @@ __device__ __forceinline__ void oz_trace(int t, int ev) {
 #define OZ_TRACE(t, ev)
 #endif
 
+constexpr int OZ_THREADS = 128 + 12 * 32;  // 4 role warps + 12 epilogue warps (3 chunks x 4 lane quarters)
+
 template <class Epi>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(OZ_THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const OzWork work, const OzScales sc, const Epi epi) {
   extern __shared__ uint8_t smem_raw[];
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 2 * 4);  // every epilogue warp of both CTAs
+    mbar_init(tempty, 2 * 12);  // every epilogue warp of both CTAs
     fence_mbar_init();
   }
   cluster_sync_all();
@@ -563,72 +565,58 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    // Drain first: the S accumulator groups of the thread's row are combined in fp64 (the last chunk
-    // in registers, the others through the staging block) and the TMEM is released, so the next
-    // tile's MMAs overlap the rest of this epilogue (S x 96 accumulator columns cannot be
-    // double-buffered in 512).  Then scaling by 2^(e_m + e_n - 12), the per-warp 32 x 32 fp64 staging
-    // block, and the functor's coalesced row pass (lanes along n) and optional column pass.
+    // Epilogue: 12 warps, one per (TMEM lane quarter, 32-column chunk) -- it runs at one warp per
+    // scheduler per chunk set and its per-element instruction count sets the tile time of short-K
+    // tiles, so the three chunks run in parallel.  Each warp drains its chunk's S accumulator groups
+    // and combines them exactly in int64 (Q = sum_g acc_g 128^(S-1-g), |Q| < 2^60), releases the TMEM
+    // (the S x 96 accumulator columns cannot be double-buffered in 512), then rounds Q once to fp64,
+    // scales it by the exact powers of two 2^(e_m - 12 - 7(S-1)) (row) and 2^(e_n) (column; NaN marks
+    // a non-finite operand row / column) and hands its row segment to the functor.
     const int ew = warp - 4;
+    const int q4 = warp & 3;   // TMEM lane quarter this warp may access
+    const int c = ew >> 2;     // 32-column chunk of the tile
     uint32_t acc_phase = 0;
-    constexpr int CH = OZ_BN / 32;
     for (int idx = cluster; idx < work.num_work; idx += nclusters) {
       int b, split, tm, tn, kt0, kt1;
       oz_decode(work, idx, b, split, tm, tn, kt0, kt1);
+      // the row / column maxima are loaded before waiting for the accumulator: their latency under the
+      // operand stream (several µs) then hides behind the tile's MMAs instead of following the drain
+      const int row = tm * OZ_BM + static_cast<int>(rank) * 128 + q4 * 32 + lane;
+      const int n0 = tn * OZ_BN + c * 32;
+      const unsigned long long ma = row < sc.M ? __ldg(sc.a + b * sc.a_bs + row) : 0ull;
+      const unsigned long long mb = n0 + lane < sc.N ? __ldg(sc.b + b * sc.b_bs + n0 + lane) : 0ull;
       mbar_wait(tfull, acc_phase);
       acc_phase ^= 1;
       tc_fence_after();
       if (ew == 0 && lane == 0) OZ_TRACE((idx - cluster) / nclusters, 4);
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
-      const int m0 = tm * OZ_BM + static_cast<int>(rank) * 128 + ew * 32;
-      const int row = m0 + lane;
-      const unsigned long long ma = row < sc.M ? sc.a[b * sc.a_bs + row] : 0ull;
-      const bool a_bad = !(__longlong_as_double(static_cast<long long>(ma)) <= 1.7976931348623157e308);
-      // The S groups of an element are combined exactly in int64 (Q = sum_g acc_g 128^(S-1-g), |Q| < 2^60:
-      // integer multiply-adds instead of S fp64 FMAs), rounded once to fp64 and scaled by the exact powers
-      // of two 2^(e_m - 12 - 7(S-1)) (row) and 2^(e_n) (column).  The epilogue runs one warp per scheduler,
-      // so its per-element instruction count sets the tile time of short-K tiles.  All three chunks are drained before the TMEM is released
-      // (chunk 0 to the staging block, chunks 1 and 2 in registers), so the next tile's MMAs start early.
-      // exact power-of-two scales (NaN marks a non-finite operand row / column and propagates)
-      const double rowscale = a_bad ? __longlong_as_double(0x7FF8000000000000ll)
-                                    : oz_pow2(oz_exponent(ma) - 12 - 7 * (OZ_S - 1));
-      double colscale[CH];  // lane j: scale of column (chunk start + j), shuffled per element
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q4 * 32) << 16) + static_cast<uint32_t>(c * 32);
+      long long v[32];
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int coln = tn * OZ_BN + c * 32 + lane;
-        const unsigned long long mb = coln < sc.N ? sc.b[b * sc.b_bs + coln] : 0ull;
-        const bool bad = !(__longlong_as_double(static_cast<long long>(mb)) <= 1.7976931348623157e308);
-        colscale[c] = bad ? __longlong_as_double(0x7FF8000000000000ll) : oz_pow2(oz_exponent(mb));
+      for (int j = 0; j < 32; ++j) v[j] = 0;
+#pragma unroll
+      for (int g = 0; g < OZ_S; ++g) {
+        uint32_t r[32];
+        tmem_ld32(taddr + g * OZ_BN, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = v[j] * 128 + static_cast<long long>(static_cast<int32_t>(r[j]));
       }
-      auto drain = [&](int c, long long (&q)[32]) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) q[j] = 0;
-#pragma unroll
-        for (int g = 0; g < OZ_S; ++g) {
-          uint32_t r[32];
-          tmem_ld32(taddr + g * OZ_BN + c * 32, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) q[j] = q[j] * 128 + static_cast<long long>(static_cast<int32_t>(r[j]));
-        }
-      };
-      auto emit = [&](int c, const long long (&q)[32]) {
-        double v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __ll2double_rn(q[j]) * rowscale * __shfl_sync(0xffffffffu, colscale[c], j);
-        epi.rows(b, split, row, tn * OZ_BN + c * 32, v, sc.M, sc.N, work.syrk != 0);
-      };
-      static_assert(CH == 3, "the epilogue is written for 96-column tiles");
-      long long v0[32], v1[32], v2[32];
-      drain(0, v0);
-      drain(1, v1);
-      drain(2, v2);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty, 0);  // every accumulator column is in registers now
+      if (lane == 0) mbar_arrive_cluster(tempty, 0);  // this warp's accumulator columns are in registers
       if (ew == 0 && lane == 0) OZ_TRACE((idx - cluster) / nclusters, 5);
-      emit(0, v0);
-      emit(1, v1);
-      emit(2, v2);
+      const bool a_bad = !(__longlong_as_double(static_cast<long long>(ma)) <= 1.7976931348623157e308);
+      const double rowscale = a_bad ? __longlong_as_double(0x7FF8000000000000ll)
+                                    : oz_pow2(oz_exponent(ma) - 12 - 7 * (OZ_S - 1));
+      const double colscale = !(__longlong_as_double(static_cast<long long>(mb)) <= 1.7976931348623157e308)
+                                  ? __longlong_as_double(0x7FF8000000000000ll)
+                                  : oz_pow2(oz_exponent(mb));
+      if (ew == 0 && lane == 0) OZ_TRACE((idx - cluster) / nclusters, 0);
+      double d[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) d[j] = __ll2double_rn(v[j]) * rowscale * __shfl_sync(0xffffffffu, colscale, j);
+      if (ew == 0 && lane == 0) OZ_TRACE((idx - cluster) / nclusters, 1);
+      epi.rows(b, split, row, n0, d, sc.M, sc.N, work.syrk != 0);
       if (ew == 0 && lane == 0) OZ_TRACE((idx - cluster) / nclusters, 6);
     }
   }

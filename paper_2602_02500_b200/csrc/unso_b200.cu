@@ -835,7 +835,7 @@ static int32_t oz_gemm(const OzOperand& A, const OzOperand& B, int64_t M, int64_
   const int pairs = static_cast<int>(std::min<int64_t>(nw, device_sm_count() / 2));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(OZ_THREADS);
   cfg.dynamicSmemBytes = OZ_SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

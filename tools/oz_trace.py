@@ -30,4 +30,5 @@ for cta in range(2):
             continue
         f = lambda v: (v - t0) / 1e3 if v else float('nan')
         print(f"  tile {k}: mma start {f(e[2]):8.2f}  mma issued {f(e[3]):8.2f}  epi tfull {f(e[4]):8.2f}  "
-              f"released {f(e[5]):8.2f}  done {f(e[6]):8.2f}")
+              f"released {f(e[5]):8.2f}  scales {f(e[0]) if k < 15 else 0:8.2f}  converted {f(e[1]) if k < 15 else 0:8.2f}  "
+              f"done {f(e[6]):8.2f}")
