@@ -82,6 +82,7 @@ struct ChainParams {
   double alpha;        // 1 + sum a + b
   float coef[CHAIN_MAX_ORDER];  // coef[k-1] multiplies C_k
   double trunc_tau;    // 0 disables truncation
+  int hi_only;         // squarings k <= hi_only take the hi*hi product alone (lo tiles not loaded)
   float tail[CHAIN_MAX_ORDER];      // tail[k] = sum_{j > k} coef[j-1]
   float tail_abs[CHAIN_MAX_ORDER];  // tail_abs[k] = sum_{j > k} |coef[j-1]|
 };
@@ -203,11 +204,12 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
           mbar_wait(&empty[stage], phase ^ 1);
           CHAIN_KB(k, 1, kt);
           uint8_t* st = smem + stage * CH_STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], CH_STAGE_BYTES);
+          const bool hi_only = k <= p.hi_only;
+          mbar_arrive_expect_tx(&full[stage], hi_only ? 2 * CH_TILE : CH_STAGE_BYTES);
           ch_load_block(maps, buf, 0, &full[stage], st, ti, kt, b);
-          ch_load_block(maps, buf, 1, &full[stage], st + CH_TILE, ti, kt, b);
+          if (!hi_only) ch_load_block(maps, buf, 1, &full[stage], st + CH_TILE, ti, kt, b);
           ch_load_block(maps, buf, 0, &full[stage], st + 2 * CH_TILE, tj, kt, b);
-          ch_load_block(maps, buf, 1, &full[stage], st + 3 * CH_TILE, tj, kt, b);
+          if (!hi_only) ch_load_block(maps, buf, 1, &full[stage], st + 3 * CH_TILE, tj, kt, b);
           if (++stage == CH_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -243,8 +245,10 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
           const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * CH_TILE, ks)
                                    : operand_desc<false>(st + 3 * CH_TILE, ks);
           umma_bf16_warp(tmem + CH_ACC, ah, bh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
-          umma_bf16_warp(tmem + CH_ACC, ah, bl, idesc, 1u);
-          umma_bf16_warp(tmem + CH_ACC, al, bh, idesc, 1u);
+          if (k > p.hi_only) {
+            umma_bf16_warp(tmem + CH_ACC, ah, bl, idesc, 1u);
+            umma_bf16_warp(tmem + CH_ACC, al, bh, idesc, 1u);
+          }
         }
         umma_commit_warp(&empty[stage]);
         if (++stage == CH_STAGES) {

@@ -1390,6 +1390,8 @@ static bool chain_persistent_fits(const Problem& p) {
   return (p.batch + per - 1) / per <= 4;
 }
 
+constexpr int CHAIN_PERSISTENT_HI_ONLY = 0;  // A/B in DESIGN §9: 0.5 % of configs[3] for 2.4x the error, not taken
+
 // Parameters shared by the on-chip chain kernels (chain_persistent.cuh, chain_small.cuh).
 static ChainParams chain_params(const Problem& p, const Plan& pl, void* ws, const float* part, int splits,
                                 int64_t part_ld, int64_t part_mat, int32_t* status) {
@@ -1429,6 +1431,13 @@ static ChainParams chain_params(const Problem& p, const Plan& pl, void* ws, cons
   }
   // truncation (chain_persistent.cuh): tail[k] = sum_{j>k} c_j, c_j = co[j-1]
   cp.trunc_tau = (p.flags & UNSO_FLAG_NO_TRUNCATION) ? 0.0 : std::ldexp(1.0, -12);
+  // hi*hi alone in the first squarings (as the large-h route): an error there is damped by the later
+  // squarings; shipped-order chains only, UNSO_FLAG_CHAIN_BF16X3 keeps bf16x3 in every step
+  {
+    static const char* const f = dev_override("UNSO_PCHAIN_HI_ONLY");  // developer override (A/B)
+    const int dflt = (p.order >= 12 && (p.flags & UNSO_FLAG_CHAIN_BF16X3) == 0) ? CHAIN_PERSISTENT_HI_ONLY : 0;
+    cp.hi_only = f ? std::max(0, std::min(std::atoi(f), p.order - 1)) : dflt;
+  }
   for (int k = 0; k <= p.order && k < CHAIN_MAX_ORDER; ++k) {
     double t = 0.0, ta = 0.0;
     for (int j = k + 1; j <= p.order; ++j) {
