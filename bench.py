@@ -77,6 +77,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-projection", action="store_true", help="cfg4: skip the per-rank shard projection")
+    ap.add_argument("--no-comparison", action="store_true",
+                    help="skip the untimed-for-value NS comparison (5 Muon-coefficient steps, configs[0])")
     ap.add_argument("--sharded", action="store_true",
                     help="cfg4: run the row-sharded multi-rank path (process group, Gram reduction) even at world 1")
     ap.add_argument("--probe-ranks", action="store_true", help=argparse.SUPPRESS)  # launcher self-test (CPU)
@@ -883,6 +885,12 @@ def main(argv=None):
     if wl == "cfg4" and world == 1 and not args.sharded and not args.no_projection:
         projection = shard_projection(work, U, N, dev, ms_step)
 
+    # ---- the NS comparison path (configs[0]: "compared against 5 Muon-coefficient NS steps")
+    comparison = None
+    if (wl != "cfg3" and world == 1 and not args.sharded and not args.no_comparison
+            and not (wl == "cfg5" and work.precision == "fp32")):
+        comparison = ns_comparison(work, U, dev, ms_step, {"cfg1": 50, "cfg2": 10, "cfg4": 5, "cfg5": 2}[wl])
+
     # ---- CPU baseline: the same bounded sample as --impl reference, on this box's host cores
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -930,6 +938,8 @@ def main(argv=None):
         }
         if projection:
             line["shard_projection"] = projection
+        if comparison:
+            line["comparison"] = comparison
         info = gate.get("info")
         if isinstance(info, list) and info and wl == "cfg4":
             d = info[0]
@@ -938,6 +948,40 @@ def main(argv=None):
         print(json.dumps(line), flush=True)
     if multi:
         dist.destroy_process_group()
+
+
+def ns_comparison(work, U, dev, ms_unso, steps):
+    """The comparison path of configs[0] (and of the other matrix configs): 5 Muon-coefficient NS steps
+    (ortho.py:221-237) on the same input and precision, timed like the headline (CUDA events, inputs
+    resident); its orthogonality error next to the reference's exact-arithmetic value (the composed
+    quintic map on sigma(X)/||X||_F, plain scaling)."""
+    import numpy as np
+    import torch
+    spec_m = U.MethodSpec(U.MethodKind.MUON_NS, iterations=5)
+    yc = torch.empty_like(work.x)
+    for _ in range(2):
+        U.orthogonalize(work.x, spec_m, precision=work.precision, out=yc, check=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        U.orthogonalize(work.x, spec_m, precision=work.precision, out=yc, check=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    F = U.kernel_model_flops(work.h, work.w, spec_m) * work.total_batch
+    y0 = (yc if yc.dim() == 2 else yc[0]).double()
+    x0 = (work.x if work.x.dim() == 2 else work.x[0]).double()
+    tall = y0.shape[0] > y0.shape[1]
+    gy = y0.T @ y0 if tall else y0 @ y0.T
+    gx = x0.T @ x0 if tall else x0 @ x0.T
+    err = float(torch.linalg.norm(gy - torch.eye(gy.shape[0], device=gy.device, dtype=gy.dtype)))
+    sx = torch.sqrt(torch.linalg.eigvalsh(gx).clamp_min(0.0)).cpu().numpy()
+    sy = U.scalar_map(spec_m)(sx / float(np.sqrt((sx ** 2).sum())))
+    return {"method": "Muon-5 Newton-Schulz, (a,b,c) = (3.4445, -4.7750, 2.0315) x 5, plain scaling",
+            "ms_per_step": ms, "model_flops_per_step": F, "model_tflops": F / (ms / 1e3) / 1e12,
+            "unso_speedup": ms / ms_unso, "steps": steps,
+            "ortho_error": err, "ortho_error_reference": float(np.sqrt(((sy ** 2 - 1.0) ** 2).sum()))}
 
 
 def parallelism_name(wl, world, multi, collective):
