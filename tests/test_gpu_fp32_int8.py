@@ -111,3 +111,43 @@ def test_int8_engine_nonfinite_input_is_flagged():
     x[17, 5] = float("nan")
     with pytest.raises(U.DegenerateInputError):
         U.orthogonalize(x, spec(), precision="fp32")
+
+
+SWEEP = list(range(16))
+
+
+@pytest.mark.parametrize("case", SWEEP)
+def test_int8_engine_random_sweep(case):
+    """Seeded sweep of the int8 digit engine (fp32 mode, 256 < h <= 1500): ragged tall / wide shapes,
+    batches, input dtypes, scalings and ill-conditioned controlled spectra (singular values
+    log-uniform down to 1e-5 or Pareto-like) against the oracle at the fp32-mode bar."""
+    rng = np.random.default_rng(4000 + case)
+    h = int(rng.integers(257, 1500))
+    w = int(rng.integers(h, min(4096, 3 * h)))
+    tall = rng.random() < 0.6
+    batch = int(rng.choice([1, 1, 2]))
+    dtype = {0: torch.float32, 1: torch.float32, 2: torch.float64, 3: torch.bfloat16}[int(rng.integers(0, 4))]
+    scaling = str(rng.choice(["gram", "gram", "plain"]))
+    ms = []
+    for i in range(batch):
+        if rng.random() < 0.5:
+            s = np.exp(rng.uniform(np.log(1e-5), 0.0, h))
+        else:
+            s = 1.0 + rng.pareto(1.5, h)
+            s = 1e-6 + (s - s.min()) / (s.max() - s.min())
+        m = O.controlled_spectrum_matrix(w, h, s, 100 * case + i) if tall else \
+            O.controlled_spectrum_matrix(h, w, s, 100 * case + i)
+        ms.append(m)
+    x = torch.from_numpy(np.stack(ms)).to(dtype).to(DEV)
+    xin = x[0] if batch == 1 else x
+    res = U.orthogonalize(xin, spec(scaling=scaling), precision="fp32")
+    torch.cuda.synchronize()
+    y = res.y.reshape(x.shape).double().cpu().numpy()
+    src = x.double().cpu().numpy()
+    worst = 0.0
+    for i in range(batch):
+        ref = O.run(src[i], "unso", scaling=scaling)["y"]
+        worst = max(worst, rel(y[i], ref))
+    tol = 1e-5 + (2.0 ** -9 if dtype == torch.bfloat16 else 0.0)
+    print(f"case {case}: {x.shape} {str(dtype)[6:]} {scaling}: {worst:.2e}")
+    assert worst <= tol
