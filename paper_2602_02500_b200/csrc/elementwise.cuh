@@ -132,15 +132,17 @@ __global__ void gram_norms_kernel(const T* __restrict__ G, int h, int64_t ld, do
   const int b = blockIdx.y;
   const T* g = G + static_cast<int64_t>(b) * h * ld;
   double tr = 0.0, fr = 0.0, dv = 0.0;
-  const int64_t total = static_cast<int64_t>(h) * h;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / h, c = i - r * h;
-    const double v = static_cast<double>(g[r * ld + c]);
-    const double d = (r == c) ? v - 1.0 : v;
-    if (r == c) tr += v;
-    fr += v * v;
-    dv += d * d;
+  // rows strided over the blocks, columns over the threads: no 64-bit division per element (the
+  // flat-index form spent most of its time in the emulated int64 divide)
+  for (int r = blockIdx.x; r < h; r += gridDim.x) {
+    const T* gr = g + static_cast<int64_t>(r) * ld;
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+      const double v = static_cast<double>(gr[c]);
+      const double d = (r == c) ? v - 1.0 : v;
+      if (r == c) tr += v;
+      fr += v * v;
+      dv += d * d;
+    }
   }
   tr = block_sum(tr, scratch);
   if (threadIdx.x == 0) blk[(static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * 3 + 0] = tr;
