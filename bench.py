@@ -1035,9 +1035,46 @@ def shard_projection(work, U, N, dev, ms_full):
                 t_f += e2.elapsed_time(e3) / reps
         t_ar = 1e3 * (2.0 * (n - 1) / n * ar_bytes / 700e9) + 0.015
         t_n = t_g + t_f + t_ar
-        out[str(n)] = {"rows_per_rank": rows // n, "gram_ms": t_g, "chain_and_apply_ms": t_f,
-                       "allreduce_ms_assumed": t_ar, "critical_path_ms": t_n,
-                       "projected_efficiency": ms_full / (n * t_n)}
+        # the same two stages replayed as CUDA graphs: the GPU-side critical path without the host
+        # launch gaps of ~0.1 ms stages (a rank would capture gram -> all-reduce -> finish the same way)
+        t_gg = t_fg = None
+        try:
+            gg, gf = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                for _ in range(2):  # warm-up on the capture stream (workspace, attributes)
+                    D.native_gram(xs, work.spec, None)
+                    D.native_finish(xs, gbuf, work.spec, None, ys)
+                with torch.cuda.graph(gg, stream=side):
+                    D.native_gram(xs, work.spec, None)
+                with torch.cuda.graph(gf, stream=side):
+                    D.native_finish(xs, gbuf, work.spec, None, ys)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            torch.cuda.synchronize()
+            for graph, key in ((gg, "g"), (gf, "f")):
+                graph.replay()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    graph.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                if key == "g":
+                    t_gg = e0.elapsed_time(e1) / reps
+                else:
+                    t_fg = e0.elapsed_time(e1) / reps
+        except Exception as exc:  # graph capture unavailable: report the event-timed path only
+            print(f"bench.py: graphed shard projection skipped: {exc}", file=sys.stderr)
+        rec = {"rows_per_rank": rows // n, "gram_ms": t_g, "chain_and_apply_ms": t_f,
+               "allreduce_ms_assumed": t_ar, "critical_path_ms": t_n,
+               "projected_efficiency": ms_full / (n * t_n)}
+        if t_gg is not None and t_fg is not None:
+            t_ng = t_gg + t_fg + t_ar
+            rec.update({"gram_ms_graphed": t_gg, "chain_and_apply_ms_graphed": t_fg,
+                        "critical_path_ms_graphed": t_ng, "projected_efficiency_graphed": ms_full / (n * t_ng)})
+        out[str(n)] = rec
     return out
 
 
