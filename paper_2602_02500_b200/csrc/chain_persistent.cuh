@@ -427,6 +427,67 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       tc_fence_after();
       const bool want_e2 = p.trunc_tau > 0.0 && !last;
       float e2 = 0.f;  // ||I - C_{k+1}||_F^2 over this thread's part of the tile (weighted below)
+      if (!last) {
+        // Critical path first: C_{k+1} to TMEM and to its global hi/lo copies, the barrier arrival;
+        // the P update (not read by any other tile) follows while the next squaring's MMAs run.
+        for (int c = 0; c < 4; ++c) {
+          const int gc0 = tj * 128 + c * 32;
+          uint32_t ua[32], uc[32];
+          tmem_ld32(lane_base + CH_ACC + c * 32, ua);
+          tmem_ld32(lane_base + CH_C + c * 32, uc);
+          tmem_wait_ld();
+          __align__(16) __nv_bfloat16 hi[32];
+          __align__(16) __nv_bfloat16 lo[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const bool ok = row_ok && gc0 + j < p.h;
+            const float cn = ok ? 2.0f * __uint_as_float(uc[j]) - __uint_as_float(ua[j]) : 0.f;
+            uc[j] = __float_as_uint(cn);
+            split_bf16(cn, hi[j], lo[j]);
+            if (want_e2) {
+              const float dv = ok ? cn - (gc0 + j == gr ? 1.f : 0.f) : 0.f;
+              e2 = fmaf(dv, dv, e2);
+            }
+          }
+          tmem_st32(lane_base + CH_C + c * 32, uc);
+          if (row_ok) {
+            const int nb = k & 1;
+            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 16) {  // 256-bit stores: whole sectors (ld % 256 == 0)
+              st_global_v8(p.chi[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(hi + j));
+              st_global_v8(p.clo[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(lo + j));
+            }
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(tempty);
+        if (want_e2) {
+          const double e2w = warp_sum(wgt * static_cast<double>(e2));
+          if (lane == 0) red[0][ew] = e2w;
+        }
+        fence_proxy_async_global();
+        named_bar_sync(1, 128);
+        if (tid == 0) {
+          CHAIN_TRACE(k, 4);
+          const double part = p.trunc_tau > 0.0 ? red[0][0] + red[0][1] + red[0][2] + red[0][3] : 0.0;
+          grid_arrive(p.gbar, k + 1, part);  // C_{k+1} published, with its ||I - C||_F^2 partial
+        }
+        last_round = static_cast<unsigned>(k + 1);
+        // P -= c_{k+1} C_{k+1}, off the critical path (the TMEM C region is not touched by the MMAs)
+        for (int c = 0; c < 4; ++c) {
+          uint32_t uc[32], up[32];
+          tmem_ld32(lane_base + CH_C + c * 32, uc);
+          tmem_ld32(lane_base + CH_P + c * 32, up);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) up[j] = __float_as_uint(__uint_as_float(up[j]) - coef * __uint_as_float(uc[j]));
+          tmem_st32(lane_base + CH_P + c * 32, up);
+        }
+        tmem_wait_st();
+        continue;
+      }
       for (int c = 0; c < 4; ++c) {
         const int gc0 = tj * 128 + c * 32;
         uint32_t ua[32], uc[32], up[32];
