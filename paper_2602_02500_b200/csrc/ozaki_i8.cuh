@@ -391,6 +391,45 @@ struct OzEpiSym {
   }
 };
 
+// NS quintic operator B = bq G + cq G^2 (ortho.py:226-230 regrouped) from the SYRK of G: upper row
+// segment and its mirror (B is symmetric; the mirror reuses G(row, n) = G(n, row)).
+struct OzEpiQuinticB {
+  const double* G;
+  double* Bm;
+  int64_t ld, bs;
+  double bq, cq;
+  __device__ void rows(int b, int, int row, int n0, const double (&v)[32], int M, int N, bool syrk) const {
+    if (row >= M) return;
+    const int64_t base = static_cast<int64_t>(b) * bs;
+    const double* g = G + base + static_cast<int64_t>(row) * ld + n0;
+    double o[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = (n0 + j < N) ? fma(bq, __ldg(g + j), cq * v[j]) : 0.0;
+    oz_store_row_f64(Bm + base + static_cast<int64_t>(row) * ld + n0, row, n0, o, M, N, syrk);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = n0 + j;
+      if (n > row && n < N) Bm[base + static_cast<int64_t>(n) * ld + row] = o[j];
+    }
+  }
+};
+
+// NS state update out = alpha * (X B or B X) + beta * old, fp64 state (ortho.py:215-217, 226-230).
+struct OzEpiAxpy {
+  double* out;
+  const double* old;
+  int64_t ld, bs;
+  double alpha, beta;
+  __device__ void rows(int b, int, int row, int n0, const double (&v)[32], int M, int N, bool) const {
+    if (row >= M) return;
+    const int64_t o = static_cast<int64_t>(b) * bs + static_cast<int64_t>(row) * ld + n0;
+    double r[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) r[j] = (n0 + j < N) ? fma(alpha, v[j], beta * __ldg(old + o + j)) : 0.0;
+    oz_store_row_f64(out + o, row, n0, r, M, N, false);
+  }
+};
+
 // Output in the caller's dtype (the apply).
 struct OzEpiOut {
   void* out;

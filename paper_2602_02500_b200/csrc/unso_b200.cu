@@ -545,7 +545,7 @@ static int pick_splits(int64_t tiles, int64_t ktiles, int64_t slots) {
 // FP32 mode on the int8 tensor cores (ozaki_i8.cuh): UNSO with h > 256 (smaller h runs the
 // one-launch fp64 chain, latency-bound) unless UNSO_FLAG_FP32_DMMA asks for the fp64 DMMA engine.
 static bool use_oz(const Problem& p) {
-  return p.prec == UNSO_PREC_FP32 && p.method == UNSO_METHOD_UNSO && p.h > 256 && (p.flags & UNSO_FLAG_FP32_DMMA) == 0;
+  return p.prec == UNSO_PREC_FP32 && p.h > 256 && (p.flags & UNSO_FLAG_FP32_DMMA) == 0;
 }
 static int64_t oz_syrk_tiles(int64_t h) {  // pair tiles of oz_decode's SYRK order
   const int64_t tm = (h + OZ_BM - 1) / OZ_BM, tn = (h + OZ_BN - 1) / OZ_BN;
@@ -569,6 +569,21 @@ static int gram_splits(const Problem& p, bool for_error = false) {
   }
   const int64_t t = (p.h + SIMT_BM - 1) / SIMT_BM;
   return simt_pick_splits(static_cast<int>(t * (t + 1) / 2), static_cast<int>(p.batch), static_cast<int>(p.w));
+}
+
+// int8 digit-engine buffers (fp32 mode, h > 256): X digit planes [S][B][h][round_up(w, 64)] (Gram
+// operand) or [S][B][w][round_up(h, 64)] (apply / NS update operand) -- one buffer, used in turn; the
+// h x h digit planes (C_k, P, G or the NS operator); per-row maxima of both operands.
+static void take_oz(Plan& pl, const Problem& p) {
+  const int64_t B = p.batch;
+  const int64_t xa = p.h * round_up(p.w, 64), xb = p.w * round_up(p.h, 64);
+  pl.ozX_plane = B * std::max(xa, xb);
+  pl.ozX = take(pl, static_cast<size_t>(OZ_S * pl.ozX_plane));
+  pl.ozC_plane = B * pl.hh;
+  pl.ozC = take(pl, static_cast<size_t>(OZ_S * pl.ozC_plane));
+  pl.ozMaxA_bs = std::max(p.w, p.h);
+  pl.ozMaxA = take(pl, static_cast<size_t>(B * pl.ozMaxA_bs) * 8);
+  pl.ozMaxB = take(pl, static_cast<size_t>(B * p.h) * 8);
 }
 
 static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) {
@@ -629,18 +644,7 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
       pl.gbar = take(pl, CHAIN_ROUNDS * 8);  // chain_f64_kernel rounds and phase-A partials
       const int64_t nt16 = (p.h + 15) / 16;
       pl.normbuf = take(pl, static_cast<size_t>(nt16 * (nt16 + 1) / 2 * B) * 2 * 8);
-      if (use_oz(p)) {
-        // X digit planes: [S][B][h][round_up(w, 64)] (Gram operand) or [S][B][w][round_up(h, 64)]
-        // (apply operand) -- one buffer, the Gram's planes are dead before the apply's are written.
-        const int64_t xa = p.h * round_up(p.w, 64), xb = p.w * round_up(p.h, 64);
-        pl.ozX_plane = B * std::max(xa, xb);
-        pl.ozX = take(pl, static_cast<size_t>(OZ_S * pl.ozX_plane));
-        pl.ozC_plane = B * pl.hh;  // C_k digit planes, then P's
-        pl.ozC = take(pl, static_cast<size_t>(OZ_S * pl.ozC_plane));
-        pl.ozMaxA_bs = std::max(p.w, p.h);
-        pl.ozMaxA = take(pl, static_cast<size_t>(B * pl.ozMaxA_bs) * 8);
-        pl.ozMaxB = take(pl, static_cast<size_t>(B * p.h) * 8);
-      }
+      if (use_oz(p)) take_oz(pl, p);
     }
   } else if (bf) {
     // NS in BF16: fp32 state ping-pong + bf16 operand copy (always), G hi/lo, operator B (P), B hi/lo
@@ -666,6 +670,7 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
     pl.Xs[0] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 8);
     pl.Xs[1] = take(pl, static_cast<size_t>(B * p.rows * p.cols) * 8);
     pl.C[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);  // quintic operator B
+    if (use_oz(p)) take_oz(pl, p);
   }
   return pl;
 }
@@ -850,13 +855,20 @@ static int32_t oz_gemm(const OzOperand& A, const OzOperand& B, int64_t M, int64_
   return UNSO_OK;
 }
 
-// Gram split-K partials of X on the int8 engine (the fp64 partial layout of gram_simt).
-static int32_t gram_oz(const Problem& p, const void* x, const Plan& pl, void* ws, int splits, cudaStream_t st) {
+// Gram split-K partials of X on the int8 engine (the fp64 partial layout of gram_simt); the source
+// may be the input (dt, ld, bs of the problem) or an fp64 NS state.
+static int32_t gram_oz(const Problem& p, const void* x, const Plan& pl, void* ws, int splits, cudaStream_t st,
+                       int dt = -1, int64_t ld = -1, int64_t bs = -1) {
+  if (dt < 0) {
+    dt = p.dt;
+    ld = p.ld;
+    bs = p.bs;
+  }
   int8_t* planes = at<int8_t>(ws, pl.ozX);
   unsigned long long* mx = at<unsigned long long>(ws, pl.ozMaxA);
   const int64_t ldd = round_up(p.w, 64), dbs = p.h * ldd;
   // operand rows = the h short-side vectors: columns of a tall X, rows of a wide one
-  UNSO_TRY(oz_slice(x, p.dt, p.ld, p.bs, p.rows, p.cols, p.batch, p.tall, mx, pl.ozMaxA_bs, planes, ldd, dbs,
+  UNSO_TRY(oz_slice(x, dt, ld, bs, p.rows, p.cols, p.batch, p.tall, mx, pl.ozMaxA_bs, planes, ldd, dbs,
                     pl.ozX_plane, st));
   const OzOperand X{planes, ldd, dbs, pl.ozX_plane, mx, pl.ozMaxA_bs};
   OzEpiPartial epi{at<double>(ws, pl.part), pl.hh, pl.ldc, static_cast<int>(p.batch)};
@@ -1631,7 +1643,7 @@ static int32_t ns_fp32(const Problem& p, const Plan& pl, void* ws, const void* x
                                                             at<double>(ws, pl.scal), status);
     UNSO_CHECK_LAUNCH();
   } else {
-    UNSO_TRY(gram_simt(p, x, p.dt, p.ld, p.bs, pl, ws, pl.splits, st));
+    UNSO_TRY(gram_fp32(p, x, pl, ws, pl.splits, st));
     UNSO_TRY(finalize_gram<double>(p, pl, ws, pl.splits, at<double>(ws, pl.G), st));
     UNSO_TRY(norms_and_scalars<double>(p, pl, ws, at<double>(ws, pl.G), SM_GRAM, status, st));
     if (p.scaling == UNSO_SCALING_GELFAND)
@@ -1644,6 +1656,44 @@ static int32_t ns_fp32(const Problem& p, const Plan& pl, void* ws, const void* x
   const int iters = p.steps;
   for (int it = 0; it < iters; ++it) {
     const double* X = at<double>(ws, pl.Xs[cur]);
+    if (use_oz(p)) {  // the same three products on the int8 digit engine (fp32 mode, h > 256)
+      UNSO_TRY(gram_oz(p, X, pl, ws, pl.splits, st, DT_F64, p.cols, xsz));
+      UNSO_TRY(finalize_gram<double>(p, pl, ws, pl.splits, at<double>(ws, pl.G), st));
+      int8_t* cp = at<int8_t>(ws, pl.ozC);
+      unsigned long long* cm = at<unsigned long long>(ws, pl.ozMaxB);
+      const double* Bop = at<double>(ws, pl.G);
+      double a_c, alpha;
+      if (p.method == UNSO_METHOD_ORIGINAL_NS) {  // X <- 1.5 X - 0.5 G X (ortho.py:215-217)
+        a_c = 1.5;
+        alpha = -0.5;
+      } else {  // X <- a X + (b G + c G^2) X (ortho.py:226-230)
+        a_c = p.co[3 * it + 0];
+        alpha = 1.0;
+        UNSO_TRY(oz_slice(at<double>(ws, pl.G), DT_F64, pl.ldc, pl.hh, h, h, B, false, cm, h, cp, pl.ldc, pl.hh,
+                          pl.ozC_plane, st));
+        const OzOperand Gd{cp, pl.ldc, pl.hh, pl.ozC_plane, cm, h};
+        const OzEpiQuinticB qe{at<double>(ws, pl.G), at<double>(ws, pl.C[0]), pl.ldc, pl.hh, p.co[3 * it + 1],
+                               p.co[3 * it + 2]};
+        UNSO_TRY(oz_gemm(Gd, Gd, h, h, h, B, true, 1, qe, st));
+        Bop = at<double>(ws, pl.C[0]);
+      }
+      UNSO_TRY(oz_slice(Bop, DT_F64, pl.ldc, pl.hh, h, h, B, false, cm, h, cp, pl.ldc, pl.hh, pl.ozC_plane, st));
+      const OzOperand Bd{cp, pl.ldc, pl.hh, pl.ozC_plane, cm, h};
+      int8_t* xp = at<int8_t>(ws, pl.ozX);
+      unsigned long long* xm = at<unsigned long long>(ws, pl.ozMaxA);
+      const int64_t ldd = round_up(p.h, 64), dbs = p.w * ldd;
+      // operand rows = the w long-side vectors of the state: rows of a tall X, columns of a wide one
+      UNSO_TRY(oz_slice(X, DT_F64, p.cols, xsz, p.rows, p.cols, B, !p.tall, xm, pl.ozMaxA_bs, xp, ldd, dbs,
+                        pl.ozX_plane, st));
+      const OzOperand Xd{xp, ldd, dbs, pl.ozX_plane, xm, pl.ozMaxA_bs};
+      const OzEpiAxpy ae{at<double>(ws, pl.Xs[cur ^ 1]), X, p.cols, xsz, alpha, a_c};
+      if (p.tall)
+        UNSO_TRY(oz_gemm(Xd, Bd, p.w, h, h, B, false, 1, ae, st));
+      else
+        UNSO_TRY(oz_gemm(Bd, Xd, h, p.w, h, B, false, 1, ae, st));
+      cur ^= 1;
+      continue;
+    }
     UNSO_TRY(gram_simt(p, X, DT_F64, p.cols, xsz, pl, ws, pl.splits, st));
     UNSO_TRY(finalize_gram<double>(p, pl, ws, pl.splits, at<double>(ws, pl.G), st));
     const double* Bop = at<double>(ws, pl.G);

@@ -151,3 +151,32 @@ def test_int8_engine_random_sweep(case):
     tol = 1e-5 + (2.0 ** -9 if dtype == torch.bfloat16 else 0.0)
     print(f"case {case}: {x.shape} {str(dtype)[6:]} {scaling}: {worst:.2e}")
     assert worst <= tol
+
+
+NS_CASES = [
+    # (shape, method, iterations, dtype): the NS comparison path (ortho.py:209-233) in fp32 mode, h > 256
+    ((1000, 333), "muon", 5, torch.float32),      # tall, ragged h
+    ((300, 700), "muon", 5, torch.float64),       # wide, fp64 I/O
+    ((2048, 512), "muon", 5, torch.float32),      # configs[1] matrix
+    ((700, 300), "original", 6, torch.float32),   # cubic NS, tall
+    ((520, 1100), "original", 8, torch.float32),  # cubic NS, wide
+]
+
+
+@pytest.mark.parametrize("case", range(len(NS_CASES)))
+def test_int8_engine_ns_matches_oracle(case):
+    """Newton-Schulz on the int8 digit engine: Gram of the state, the quintic operator b G + c G^2 and
+    the state update per iteration, against the oracle's NS loop and against the fp64 DMMA engine."""
+    shape, method, iters, dtype = NS_CASES[case]
+    kind = U.MethodKind.MUON_NS if method == "muon" else U.MethodKind.ORIGINAL_NS
+    m = controlled(*shape, 0.05, 70 + case)
+    x = torch.from_numpy(m).to(dtype).to(DEV)
+    res = U.orthogonalize(x, U.MethodSpec(kind, iterations=iters), precision="fp32")
+    dm = U.orthogonalize(x, U.MethodSpec(kind, iterations=iters, fp32_engine="dmma"), precision="fp32")
+    torch.cuda.synchronize()
+    ref = O.run(x.double().cpu().numpy(), method, iterations=iters)["y"]
+    y = res.y.double().cpu().numpy()
+    e_or, e_dm = rel(y, ref), rel(y, dm.y.double().cpu().numpy())
+    print(f"{shape} {method}-{iters}: vs oracle {e_or:.2e}, vs fp64 DMMA {e_dm:.2e}")
+    assert e_or <= 1e-5
+    assert e_dm <= 2e-6

@@ -44,7 +44,10 @@ ROUTES = [
     ((3, 600, 520), "unso", "fp32", torch.float32, {}),        # int8 digit engine, batch
     ((1000, 333), "unso", "fp32", torch.float32, {"fp32_engine": "dmma"}),
     ((1000, 300), "muon", "bf16", torch.bfloat16, {}),         # NS comparison path, bf16
-    ((700, 300), "original", "fp32", torch.float32, {}),       # NS comparison path, fp32
+    ((700, 300), "original", "fp32", torch.float32, {}),       # NS comparison path, fp32, int8 engine
+    ((333, 1000), "muon", "fp32", torch.float64, {}),          # NS quintic, int8 engine, wide ragged
+    ((2, 600, 520), "muon", "fp32", torch.float32, {}),        # NS quintic, int8 engine, batch
+    ((700, 300), "muon", "fp32", torch.float32, {"fp32_engine": "dmma"}),
 ]
 
 
