@@ -55,7 +55,6 @@ struct ChainF64Params {
   double trunc_tau;          // 0 disables truncation
   double coef[CHAIN_MAX_ORDER];
   double tail[CHAIN_MAX_ORDER];
-  double tail_abs[CHAIN_MAX_ORDER];
 };
 
 __device__ __forceinline__ void cf_arrive(unsigned long long* gbar, int round, double partial) {
@@ -185,7 +184,7 @@ __global__ void __launch_bounds__(128, 1) chain_f64_kernel(const __grid_constant
       if (threadIdx.x == 0) {
         const uint64_t sum = grid_wait(p.gbar, k);  // C_k published, with its ||I - C_k||_F^2 partials
         s_stop = p.trunc_tau > 0.0 && k >= 2 &&
-                 p.tail_abs[k] * (static_cast<double>(sum) / CF_FIX) <= p.trunc_tau;
+                 chain_tail_bound(p.coef, p.order, k, static_cast<double>(sum) / CF_FIX) <= p.trunc_tau;
       }
       __syncthreads();
       if (s_stop) {  // C_j = I for j > k

@@ -18,9 +18,9 @@
 //
 // Data-dependent truncation: each step also reduces ||I - C_{k+1}||_F^2 per tile.
 // Before step k every role sums those partials (fixed order, so all CTAs agree) and, once every
-// matrix of the launch has tail_abs[k] * ||I - C_k||_F^2 <= trunc_tau, stops: the remaining
-// C_j (j > k) equal I up to ||B_k||_2^(2^(j-k)) <= ||I - C_k||_F^2, so P -= tail[k] I replaces them
-// (tail[k] = sum_{j>k} c_j; the dropped terms are bounded by tail_abs[k] ||I - C_k||_F^2).
+// matrix of the launch has sum_{j>k} |c_j| (||I - C_k||_F^2)^(2^(j-k-1)) <= trunc_tau, stops: the
+// remaining C_j (j > k) equal I up to ||B_k||_2^(2^(j-k)), so P -= tail[k] I replaces them
+// (tail[k] = sum_{j>k} c_j; chain_tail_bound() below bounds the dropped terms).
 #pragma once
 #include "common.cuh"
 #include "ptx_sm100.cuh"
@@ -84,7 +84,6 @@ struct ChainParams {
   double trunc_tau;    // 0 disables truncation
   int hi_only;         // squarings k <= hi_only take the hi*hi product alone (lo tiles not loaded)
   float tail[CHAIN_MAX_ORDER];      // tail[k] = sum_{j > k} coef[j-1]
-  float tail_abs[CHAIN_MAX_ORDER];  // tail_abs[k] = sum_{j > k} |coef[j-1]|
 };
 
 // Grid barrier, one 64-bit word per round r: every CTA adds (1 << 48) + a fixed-point (2^-33, clamped
@@ -107,11 +106,24 @@ __device__ __forceinline__ uint64_t grid_wait(const unsigned long long* gbar, in
   }
   return v & ((1ull << 48) - 1);
 }
+// Bound on the terms dropped by stopping before step k, from x = ||I - C_k||_F^2 = ||B_k||_F^2:
+// ||B_j||_2 = ||B_k||_2^(2^(j-k)) <= x^(2^(j-k-1)), so || sum_{j>k} c_j B_j ||_2 <= sum_{j>k} |c_j| x^(2^(j-k-1))
+// (coef[j-1] multiplies C_j).  Only the first term matters once x is small: one squaring fewer than
+// the uniform bound (sum_{j>k} |c_j|) x on configs[3].
+template <typename T>
+__device__ __forceinline__ double chain_tail_bound(const T* coef, int order, int k, double x) {
+  double s = 0.0, xp = x;
+  for (int j = k + 1; j <= order; ++j) {
+    s += fabs(static_cast<double>(coef[j - 1])) * xp;
+    xp = xp < 1.0 ? xp * xp : xp;  // x >= 1 never passes; keep the sum finite
+  }
+  return s;
+}
 // After round k (C_k published, `sum` = that round's partials = sum over the launch's matrices of
 // ||I - C_k||_F^2): every role takes the same decision whether the chain stops before step k.
 __device__ __forceinline__ bool chain_truncate_before(const ChainParams& p, int k, uint64_t sum) {
   if (p.trunc_tau <= 0.0 || k < 2) return false;
-  return static_cast<double>(p.tail_abs[k]) * (static_cast<double>(sum) / CHAIN_FIX) <= p.trunc_tau;
+  return chain_tail_bound(p.coef, p.order, k, static_cast<double>(sum) / CHAIN_FIX) <= p.trunc_tau;
 }
 
 // Sum of the launch-wide per-tile (x, y) partials of matrix `lb` by the 128 epilogue threads after the

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) chain_small_kernel(const __grid
       reduce2(static_cast<double>(e2), 0.0);
       const double e2s = total(0);
       const bool stop = p.trunc_tau > 0.0 && k + 1 >= 2 &&
-                        static_cast<double>(p.tail_abs[k + 1]) * e2s <= p.trunc_tau;
+                        chain_tail_bound(p.coef, p.order, k + 1, e2s) <= p.trunc_tau;
       if (tid == 0) s_stop = stop ? 1 : 0;
       fence_proxy_async_shared();
       tc_fence_before();

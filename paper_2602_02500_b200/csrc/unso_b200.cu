@@ -935,7 +935,6 @@ static bool chain_f64_persistent(const Problem& p, const Plan& pl, void* ws, con
   for (int k = 0; k <= p.order && k < CHAIN_MAX_ORDER; ++k) {
     for (int j = k + 1; j <= p.order; ++j) {
       cp.tail[k] += p.co[j - 1];
-      cp.tail_abs[k] += std::fabs(p.co[j - 1]);
     }
   }
   const int cap = std::min(per_sm * device_sm_count(), CF_MAX_GRID);
@@ -1451,13 +1450,9 @@ static ChainParams chain_params(const Problem& p, const Plan& pl, void* ws, cons
     cp.hi_only = f ? std::max(0, std::min(std::atoi(f), p.order - 1)) : dflt;
   }
   for (int k = 0; k <= p.order && k < CHAIN_MAX_ORDER; ++k) {
-    double t = 0.0, ta = 0.0;
-    for (int j = k + 1; j <= p.order; ++j) {
-      t += p.co[j - 1];
-      ta += std::fabs(p.co[j - 1]);
-    }
+    double t = 0.0;
+    for (int j = k + 1; j <= p.order; ++j) t += p.co[j - 1];
     cp.tail[k] = static_cast<float>(t);
-    cp.tail_abs[k] = static_cast<float>(ta);
   }
   return cp;
 }
