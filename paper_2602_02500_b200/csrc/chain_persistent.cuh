@@ -1,20 +1,25 @@
-// Fused persistent "scale + squaring chain" kernel (BF16 precision), one CTA per
-// 128x128 upper tile of the h x h state, all tiles co-resident (cooperative launch).
+// Fused persistent "scale + squaring chain" kernel (BF16 precision) over the 128x128 upper tiles
+// of the h x h state(s), all tiles co-resident (cooperative launch, one or two tiles per CTA).
 //
 // Replaces, for the reference's ortho.py:156-167 + 197-204:
 //   split-K finalize -> ||G||_F / trace -> s^2, status -> C_1 = G/s^2, P = alpha I - a_1 C_1
 //   -> N-1 squarings C_{k+1} = 2 C_k - C_k^2 with P -= c_{k+1} C_{k+1} -> P/s split bf16 hi/lo.
 // (C-form of B_{k+1} = B_k^2 with B = I - C; P = I + sum a_k B_k + b B_N = alpha I - sum c_k C_k.)
 //
-// Per CTA (tile (ti, tj), ti <= tj):
-//   TMEM  cols [0,128)   accumulator of C_k^2 for the tile (bf16x3: hi*hi + hi*lo + lo*hi)
-//         cols [128,256) P tile (fp32), resident for the whole chain
-//         cols [256,384) C_k tile (fp32), resident for the whole chain
-//   global: only the CTA's own upper tile of C_{k+1} (bf16 hi/lo, ping-pong buffers) is
+// Per CTA: up to two upper tiles (ti, tj), ti <= tj ("slots": tile ids blockIdx.x and blockIdx.x +
+// gridDim.x of the launch, so a batch with up to 2 x #SM tiles runs in ONE co-resident launch).  The
+// host sizes the grid to whole matrices, so slot s of every CTA belongs to matrix group s, and each
+// group has its own barrier rounds: while group 0's tiles drain, publish, synchronise and fetch their
+// first operands, the tensor pipe runs group 1's MMAs (and vice versa).  Per slot s:
+//   TMEM  cols [256 s, 256 s + 128)        D: holds 2 C_k when step k starts; the MMAs run with the A
+//                                          operand negated and accumulate into it (bf16x3: hi*hi + hi*lo +
+//                                          lo*hi), so afterwards D = 2 C_k - C_k^2 = C_{k+1} in fp32
+//         cols [256 s + 128, 256 s + 256)  P tile (fp32), resident for the whole chain
+//   global: only the CTA's own upper tiles of C_{k+1} (bf16 hi/lo, ping-pong buffers) are
 //   written per step.  Operand row-blocks are assembled from upper tiles: block (i, kb)
 //   with kb < i is read through an MN-major (transposed) TMA map of tile (kb, i), and the
 //   tcgen05 instruction descriptor's A/B major bits are switched per k-block.
-//   A grid barrier (gpu-scope release/acquire counter) separates the steps.
+//   A per-group grid barrier (gpu-scope release/acquire counter) separates the steps.
 //
 // Data-dependent truncation: each step also reduces ||I - C_{k+1}||_F^2 per tile.
 // Before step k every role sums those partials (fixed order, so all CTAs agree) and, once every
@@ -65,6 +70,7 @@ struct ChainParams {
   int splits;
   int h, nt, tiles_per_mat, batch;  // batch = TOTAL batch (split-K partial layout)
   int b0;                            // first matrix of this launch's chunk
+  int nb;                            // matrices in this launch's chunk (persistent chain)
   int64_t ld, mat;     // padded leading dim / per-matrix elements of every h x h buffer
   __nv_bfloat16* chi[2];
   __nv_bfloat16* clo[2];
@@ -76,7 +82,7 @@ struct ChainParams {
   double tau;          // bound threshold for that decision
   double* scal;        // [batch][SCAL_STRIDE]
   int32_t* status;     // [batch]
-  unsigned long long* gbar;  // [CHAIN_ROUNDS] per-round barrier words, zeroed before launch
+  unsigned long long* gbar;  // [CH_SLOTS][CHAIN_ROUNDS] per-group, per-round barrier words, zeroed before launch
   int order;
   int scal_mode;       // SM_GRAM / SM_PLAIN / SM_NONE
   double alpha;        // 1 + sum a + b
@@ -96,9 +102,9 @@ __device__ __forceinline__ void grid_arrive(unsigned long long* gbar, int round,
   __threadfence();
   red_release_gpu_add_u64(gbar + round, (1ull << 48) + static_cast<uint64_t>(c * CHAIN_FIX));
 }
-__device__ __forceinline__ uint64_t grid_wait(const unsigned long long* gbar, int round) {
+__device__ __forceinline__ uint64_t grid_wait(const unsigned long long* gbar, int round, unsigned count = 0) {
   const long long t0 = clock64();
-  const uint64_t T = gridDim.x;
+  const uint64_t T = count ? count : gridDim.x;
   uint64_t v;
   while (((v = ld_acquire_gpu_u64(gbar + round)) >> 48) < T) {
     __nanosleep(64);
@@ -149,7 +155,9 @@ constexpr int CH_STAGES = 3;
 constexpr int CH_TILE = 128 * 64 * 2;          // 16 KB operand tile
 constexpr int CH_STAGE_BYTES = 4 * CH_TILE;    // A hi, A lo, B hi, B lo
 constexpr int CH_SMEM = CH_STAGES * CH_STAGE_BYTES + 256 + 1024;
-constexpr uint32_t CH_ACC = 0, CH_P = 128, CH_C = 256;
+// TMEM columns of tile slot s: [256 s, 256 s + 128) the state D, [256 s + 128, 256 s + 256) P.
+constexpr uint32_t CH_SLOT = 256, CH_D = 0, CH_P = 128;
+constexpr int CH_SLOTS = 2;
 
 __device__ __forceinline__ void ch_load_block(const ChainMaps& maps, int buf, int hl, uint64_t* bar, uint8_t* dst,
                                               int blk, int kt, int b) {
@@ -162,24 +170,49 @@ __device__ __forceinline__ void ch_load_block(const ChainMaps& maps, int buf, in
   }
 }
 
+// One CTA owns up to CH_SLOTS upper tiles of the launch (tile ids blockIdx.x and blockIdx.x + gridDim.x,
+// possibly of different matrices).  The state of slot s lives in TMEM: D_s holds 2 C_k when step k's
+// MMAs start; they run with the A operand negated and accumulate into it, D_s -= C_k C_k, so the
+// accumulator IS C_{k+1} = 2 C_k - C_k^2 (no separate C copy), and the epilogue writes 2 C_{k+1} back.
+// With two slots the epilogue of slot 0 runs under the MMAs of slot 1.
 __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_constant__ ChainMaps maps,
                                                                   const __grid_constant__ ChainParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CH_STAGES * CH_STAGE_BYTES);
   uint64_t* empty = full + CH_STAGES;
-  uint64_t* tfull = empty + CH_STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tfull = empty + CH_STAGES;   // [CH_SLOTS]
+  uint64_t* tempty = tfull + CH_SLOTS;   // [CH_SLOTS]
+  uint64_t* decbar = tempty + CH_SLOTS;  // [CH_SLOTS] the producer's per-step go / stop decision is posted
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(decbar + CH_SLOTS);
+  // Only the producer polls the global barrier words; it posts each step's decision (0 = run step k,
+  // 1 = the chain of this slot's group stops before step k) for the MMA and epilogue roles.
+  __shared__ int s_dec[CH_SLOTS][2];
   __shared__ double red[2][4];
-  __shared__ double s_scale[2];  // inv_s2, inv_s
+  __shared__ double s_scale[CH_SLOTS][2];  // per slot: inv_s2 (later the shift d), inv_s
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int lb = blockIdx.x / p.tiles_per_mat;  // matrix within this chunk
-  const int b = p.b0 + lb;
-  const int t = blockIdx.x % p.tiles_per_mat;
-  int ti, tj;
-  simt_tile_coords(t, p.nt, p.nt, 1, ti, tj);
+  const int total_tiles = p.tiles_per_mat * p.nb;
+  const int ns = (static_cast<int>(blockIdx.x + gridDim.x) < total_tiles) ? 2 : 1;
+  // Slot s of every CTA belongs to matrix group s (the host sizes the grid to whole matrices), and each
+  // group has its own barrier words: group 1's MMAs cover group 0's epilogue + barrier + first loads.
+  const unsigned cnt0 = gridDim.x, cnt1 = static_cast<unsigned>(max(total_tiles - static_cast<int>(gridDim.x), 1));
+  auto cnt = [&](int s) { return s ? cnt1 : cnt0; };
+  // Slot coordinates, computed from blockIdx (warp-uniform values: the MMA issuer's descriptors and
+  // instruction descriptor then stay in uniform registers) and selected per slot.
+  int g_[CH_SLOTS], ti_[CH_SLOTS], tj_[CH_SLOTS];
+#pragma unroll
+  for (int s = 0; s < CH_SLOTS; ++s) {
+    g_[s] = min(static_cast<int>(blockIdx.x + s * gridDim.x), total_tiles - 1);
+    simt_tile_coords(g_[s] % p.tiles_per_mat, p.nt, p.nt, 1, ti_[s], tj_[s]);
+  }
+  const int g0 = g_[0], g1 = g_[1], ti0 = ti_[0], ti1 = ti_[1], tj0 = tj_[0], tj1 = tj_[1];
+  auto s_g = [&](int s) { return s ? g1 : g0; };                                   // tile id in the launch
+  auto s_lb = [&](int s) { return (s ? g1 : g0) / p.tiles_per_mat; };              // matrix within the chunk
+  auto s_b = [&](int s) { return p.b0 + (s ? g1 : g0) / p.tiles_per_mat; };        // matrix in the batch
+  auto s_t = [&](int s) { return (s ? g1 : g0) % p.tiles_per_mat; };               // tile within the matrix
+  auto s_ti = [&](int s) { return s ? ti1 : ti0; };
+  auto s_tj = [&](int s) { return s ? tj1 : tj0; };
   const int N = p.order;
   const int KT = (p.h + 63) / 64;
 
@@ -191,8 +224,11 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 128);
+    for (int s = 0; s < CH_SLOTS; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+      mbar_init(&decbar[s], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -206,25 +242,36 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       // ---------------------------------------------------------------- producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int k = 1; k < N; ++k) {
-        const uint64_t e2 = grid_wait(p.gbar, k);  // C_k published (round k)
-        if (chain_truncate_before(p, k, e2)) break;
-        CHAIN_TRACE(k, 0);
-        fence_proxy_async_global();
+      unsigned done = ns < 2 ? 2u : 0u;  // bit s: slot s's chain has stopped (truncated)
+      for (int k = 1; k < N && done != 3u; ++k) {
         const int buf = (k - 1) & 1;
-        for (int kt = 0; kt < KT; ++kt) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          CHAIN_KB(k, 1, kt);
-          uint8_t* st = smem + stage * CH_STAGE_BYTES;
-          const bool hi_only = k <= p.hi_only;
-          mbar_arrive_expect_tx(&full[stage], hi_only ? 2 * CH_TILE : CH_STAGE_BYTES);
-          ch_load_block(maps, buf, 0, &full[stage], st, ti, kt, b);
-          if (!hi_only) ch_load_block(maps, buf, 1, &full[stage], st + CH_TILE, ti, kt, b);
-          ch_load_block(maps, buf, 0, &full[stage], st + 2 * CH_TILE, tj, kt, b);
-          if (!hi_only) ch_load_block(maps, buf, 1, &full[stage], st + 3 * CH_TILE, tj, kt, b);
-          if (++stage == CH_STAGES) {
-            stage = 0;
-            phase ^= 1;
+        const bool hi_only = k <= p.hi_only;
+        for (int s = 0; s < CH_SLOTS; ++s) {
+          if ((done >> s) & 1u) continue;
+          const uint64_t e2 = grid_wait(p.gbar + s * CHAIN_ROUNDS, k, cnt(s));  // group s: C_k published (round k)
+          const bool stop = chain_truncate_before(p, k, e2);
+          *reinterpret_cast<volatile int*>(&s_dec[s][k & 1]) = stop ? 1 : 0;
+          mbar_arrive(&decbar[s]);  // release: the decision is visible to whoever sees phase k - 1 complete
+          if (stop) {
+            done |= 1u << s;
+            continue;
+          }
+          if (s == 0) CHAIN_TRACE(k, 0);
+          fence_proxy_async_global();
+          const int ti = s_ti(s), tj = s_tj(s), b = s_b(s);
+          for (int kt = 0; kt < KT; ++kt) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (s == 0) CHAIN_KB(k, 1, kt);
+            uint8_t* st = smem + stage * CH_STAGE_BYTES;
+            mbar_arrive_expect_tx(&full[stage], hi_only ? 2 * CH_TILE : CH_STAGE_BYTES);
+            ch_load_block(maps, buf, 0, &full[stage], st, ti, kt, b);
+            if (!hi_only) ch_load_block(maps, buf, 1, &full[stage], st + CH_TILE, ti, kt, b);
+            ch_load_block(maps, buf, 0, &full[stage], st + 2 * CH_TILE, tj, kt, b);
+            if (!hi_only) ch_load_block(maps, buf, 1, &full[stage], st + 3 * CH_TILE, tj, kt, b);
+            if (++stage == CH_STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -234,473 +281,469 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     // ---------------------------------------------------------------- MMA issuer (whole warp, one
     // elected lane issues: warp-uniform control flow keeps the descriptors in uniform registers)
     int stage = 0;
-    uint32_t phase = 0, acc_phase = 0;
-    for (int k = 1; k < N; ++k) {
-      if (k >= 2 && p.trunc_tau > 0.0 && chain_truncate_before(p, k, grid_wait(p.gbar, k))) break;
-      mbar_wait(tempty, acc_phase ^ 1);
-      tc_fence_after();
-      for (int kt = 0; kt < KT; ++kt) {
-        mbar_wait(&full[stage], phase);
-        CHAIN_KB(k, 0, kt);
-        if (kt == 0) CHAIN_TRACE(k, 1);
-        tc_fence_after();
-        const int kb = kt >> 1;
-        const bool a_mn = kb < ti, b_mn = kb < tj;
-        const uint32_t idesc = idesc_bf16(128, 128, a_mn ? 1 : 0, b_mn ? 1 : 0);
-        const uint32_t st = smem_u32(smem + stage * CH_STAGE_BYTES);
+    uint32_t phase = 0;
+    uint32_t st_phase[CH_SLOTS] = {0, 0};
+    unsigned done = ns < 2 ? 2u : 0u;
+    for (int k = 1; k < N && done != 3u; ++k) {
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t ah = a_mn ? operand_desc<true>(st, ks) : operand_desc<false>(st, ks);
-          const uint64_t al = a_mn ? operand_desc<true>(st + CH_TILE, ks) : operand_desc<false>(st + CH_TILE, ks);
-          const uint64_t bh = b_mn ? operand_desc<true>(st + 2 * CH_TILE, ks)
-                                   : operand_desc<false>(st + 2 * CH_TILE, ks);
-          const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * CH_TILE, ks)
-                                   : operand_desc<false>(st + 3 * CH_TILE, ks);
-          umma_bf16_warp(tmem + CH_ACC, ah, bh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
-          if (k > p.hi_only) {
-            umma_bf16_warp(tmem + CH_ACC, ah, bl, idesc, 1u);
-            umma_bf16_warp(tmem + CH_ACC, al, bh, idesc, 1u);
+      for (int s = 0; s < CH_SLOTS; ++s) {
+        if ((done >> s) & 1u) continue;
+        mbar_wait(&decbar[s], (k - 1) & 1);
+        if (*reinterpret_cast<volatile int*>(&s_dec[s][k & 1])) {
+          done |= 1u << s;
+          continue;
+        }
+        const int ti = s_ti(s), tj = s_tj(s);
+        mbar_wait(&tempty[s], st_phase[s]);  // D_s holds 2 C_k (phase A / the previous step's epilogue)
+        st_phase[s] ^= 1;
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + s * CH_SLOT + CH_D;
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(&full[stage], phase);
+          if (s == 0) CHAIN_KB(k, 0, kt);
+          if (kt == 0 && s == 0) CHAIN_TRACE(k, 1);
+          tc_fence_after();
+          const int kb = kt >> 1;
+          const bool a_mn = kb < ti, b_mn = kb < tj;
+          const uint32_t idesc = idesc_bf16(128, 128, a_mn ? 1 : 0, b_mn ? 1 : 0) | IDESC_NEGATE_A;
+          const uint32_t st = smem_u32(smem + stage * CH_STAGE_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t ah = a_mn ? operand_desc<true>(st, ks) : operand_desc<false>(st, ks);
+            const uint64_t al = a_mn ? operand_desc<true>(st + CH_TILE, ks) : operand_desc<false>(st + CH_TILE, ks);
+            const uint64_t bh = b_mn ? operand_desc<true>(st + 2 * CH_TILE, ks)
+                                     : operand_desc<false>(st + 2 * CH_TILE, ks);
+            const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * CH_TILE, ks)
+                                     : operand_desc<false>(st + 3 * CH_TILE, ks);
+            umma_bf16_warp(d_tmem, ah, bh, idesc, 1u);
+            if (k > p.hi_only) {
+              umma_bf16_warp(d_tmem, ah, bl, idesc, 1u);
+              umma_bf16_warp(d_tmem, al, bh, idesc, 1u);
+            }
+          }
+          umma_commit_warp(&empty[stage]);
+          if (++stage == CH_STAGES) {
+            stage = 0;
+            phase ^= 1;
           }
         }
-        umma_commit_warp(&empty[stage]);
-        if (++stage == CH_STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
+        umma_commit_warp(&tfull[s]);
+        if (s == 0) CHAIN_TRACE(k, 2);
       }
-      umma_commit_warp(tfull);
-      CHAIN_TRACE(k, 2);
-      acc_phase ^= 1;
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue warps
     const int ew = warp - 4;
     const int r = ew * 32 + lane;
-    const int gr = ti * 128 + r;
-    const bool row_ok = gr < p.h;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(ew * 32) << 16);
-    const int64_t mbase = static_cast<int64_t>(b) * p.mat;
     const int tid = threadIdx.x - 128;
 
-    // ---- phase A: G tile = sum of split-K partials -> TMEM C region; tile norms
+    // ---- phase A: G tile = sum of split-K partials -> TMEM D region; tile norms
     if (tid == 0) CHAIN_TRACE(0, 0);
-    double tr = 0.0, fr = 0.0;
-    const double wgt = (ti == tj) ? 1.0 : 2.0;
-    // all four 32-column chunks of a split-K slice are loaded before any is summed: 32 independent
-    // 16-byte loads in flight per thread (the phase was load-latency-bound chunk by chunk)
-    float g4[4][32];
+    for (int s = 0; s < ns; ++s) {
+      const int ti = s_ti(s), tj = s_tj(s), b = s_b(s);
+      const int gr = ti * 128 + r;
+      const bool row_ok = gr < p.h;
+      double tr = 0.0, fr = 0.0;
+      const double wgt = (ti == tj) ? 1.0 : 2.0;
+      // all four 32-column chunks of a split-K slice are loaded before any is summed: 32 independent
+      // 16-byte loads in flight per thread (the phase was load-latency-bound chunk by chunk)
+      float g4[4][32];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int j = 0; j < 32; ++j) g4[c][j] = 0.f;
-    if (row_ok) {
-      for (int sp = 0; sp < p.splits; ++sp) {
-        const float* src = p.part + (static_cast<int64_t>(sp) * p.batch + b) * p.part_mat +
-                           static_cast<int64_t>(gr) * p.part_ld + tj * 128;
-        float4 v[32];
+        for (int j = 0; j < 32; ++j) g4[c][j] = 0.f;
+      if (row_ok) {
+        for (int sp = 0; sp < p.splits; ++sp) {
+          const float* src = p.part + (static_cast<int64_t>(sp) * p.batch + b) * p.part_mat +
+                             static_cast<int64_t>(gr) * p.part_ld + tj * 128;
+          float4 v[32];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = __ldcg(reinterpret_cast<const float4*>(src) + q);
+          for (int q = 0; q < 32; ++q) v[q] = __ldcg(reinterpret_cast<const float4*>(src) + q);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          float* gq = &g4[q >> 3][(q & 7) * 4];
-          gq[0] += v[q].x;
-          gq[1] += v[q].y;
-          gq[2] += v[q].z;
-          gq[3] += v[q].w;
+          for (int q = 0; q < 32; ++q) {
+            float* gq = &g4[q >> 3][(q & 7) * 4];
+            gq[0] += v[q].x;
+            gq[1] += v[q].y;
+            gq[2] += v[q].z;
+            gq[3] += v[q].w;
+          }
         }
       }
-    }
-    for (int c = 0; c < 4; ++c) {
-      const int gc0 = tj * 128 + c * 32;
-      float g[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) g[j] = g4[c][j];
-      uint32_t u[32];
-      float frc = 0.f;  // fp32 partial over the 32 columns, accumulated in fp64 across chunks
+      for (int c = 0; c < 4; ++c) {
+        const int gc0 = tj * 128 + c * 32;
+        uint32_t u[32];
+        float frc = 0.f;  // fp32 partial over the 32 columns, accumulated in fp64 across chunks
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const bool ok = row_ok && (gc0 + j) < p.h;
-        const float v = ok ? g[j] : 0.f;
-        if (ok && gc0 + j == gr) tr += v;
-        frc = fmaf(v, v, frc);
-        u[j] = __float_as_uint(v);
+        for (int j = 0; j < 32; ++j) {
+          const bool ok = row_ok && (gc0 + j) < p.h;
+          const float v = ok ? g4[c][j] : 0.f;
+          if (ok && gc0 + j == gr) tr += v;
+          frc = fmaf(v, v, frc);
+          u[j] = __float_as_uint(v);
+        }
+        fr += wgt * static_cast<double>(frc);
+        tmem_st32(lane_base + s * CH_SLOT + CH_D + c * 32, u);
       }
-      fr += wgt * static_cast<double>(frc);
-      tmem_st32(lane_base + CH_C + c * 32, u);
+      tmem_wait_st();
+      tr = warp_sum(tr);
+      fr = warp_sum(fr);
+      named_bar_sync(1, 128);  // red[] free (slot 0's sums were consumed)
+      if (lane == 0) {
+        red[0][ew] = tr;
+        red[1][ew] = fr;
+      }
+      named_bar_sync(1, 128);
+      if (tid == 0) {
+        p.normbuf[s_g(s) * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+        p.normbuf[s_g(s) * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+      }
     }
-    tmem_wait_st();
-    tr = warp_sum(tr);
-    fr = warp_sum(fr);
-    if (lane == 0) {
-      red[0][ew] = tr;
-      red[1][ew] = fr;
-    }
-    named_bar_sync(1, 128);
     if (tid == 0) {
-      p.normbuf[blockIdx.x * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
-      p.normbuf[blockIdx.x * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
       CHAIN_TRACE(0, 1);
-      grid_arrive(p.gbar, 0);
-      grid_wait(p.gbar, 0);
+      for (int s = 0; s < ns; ++s) grid_arrive(p.gbar + s * CHAIN_ROUNDS, 0);
+      for (int s = 0; s < ns; ++s) grid_wait(p.gbar + s * CHAIN_ROUNDS, 0, cnt(s));
       CHAIN_TRACE(0, 2);
     }
     named_bar_sync(1, 128);  // every epilogue thread is past the grid barrier
-    sum_tile_partials(p.normbuf, lb * p.tiles_per_mat, p.tiles_per_mat, tid, red);
-    if (tid == 0) {
-      const double s0 = red[0][0] + red[0][1] + red[0][2] + red[0][3];
-      const double s1 = red[1][0] + red[1][1] + red[1][2] + red[1][3];
-      CHAIN_TRACE(0, 4);
-      double s2 = p.scal_mode == SM_PLAIN ? s0 : sqrt(s1);
-      if (p.scal_mode == SM_NONE) s2 = 1.0;
-      const double inv_s = 1.0 / sqrt(s2);
-      const bool bad = p.scal_mode != SM_NONE &&
-                       (!(s0 > 0.0) || !isfinite(s0) || !(s2 > 0.0) || !isfinite(s2) || !isfinite(inv_s));
-      s_scale[0] = 1.0 / s2;
-      s_scale[1] = inv_s;
-      if (t == 0) {
-        double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
-        o[S_TRACE] = s0;
-        o[S_FRO2] = s1;
-        o[S_S2] = s2;
-        o[S_INV_S] = inv_s;
-        if (p.status) p.status[b] = bad ? 2 : 0;
-      }
-    }
-    named_bar_sync(1, 128);
-    const float inv_s2 = static_cast<float>(s_scale[0]);
-    const float alpha_f = static_cast<float>(p.alpha);
-
-    // ---- C_1 = G / s^2 (TMEM + global buffer 0), P = alpha I - coef_1 C_1 (TMEM)
-    for (int c = 0; c < 4; ++c) {
-      const int gc0 = tj * 128 + c * 32;
-      uint32_t u[32], pu[32];
-      tmem_ld32(lane_base + CH_C + c * 32, u);
-      tmem_wait_ld();
-      __align__(16) __nv_bfloat16 hi[32];
-      __align__(16) __nv_bfloat16 lo[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float cv = __uint_as_float(u[j]) * inv_s2;  // fp32 arithmetic: the state is fp32 anyway
-        u[j] = __float_as_uint(cv);
-        const float pv = fmaf(-p.coef[0], cv, (gr == gc0 + j && row_ok) ? alpha_f : 0.f);
-        pu[j] = __float_as_uint(pv);
-        split_bf16(cv, hi[j], lo[j]);
-      }
-      tmem_st32(lane_base + CH_C + c * 32, u);
-      tmem_st32(lane_base + CH_P + c * 32, pu);
-      if (row_ok && N > 1) {
-        const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
-#pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          *reinterpret_cast<uint4*>(p.chi[0] + o + j) = *reinterpret_cast<const uint4*>(hi + j);
-          *reinterpret_cast<uint4*>(p.clo[0] + o + j) = *reinterpret_cast<const uint4*>(lo + j);
+    for (int s = 0; s < ns; ++s) {
+      const int b = s_b(s);
+      sum_tile_partials(p.normbuf, s_lb(s) * p.tiles_per_mat, p.tiles_per_mat, tid, red);
+      if (tid == 0) {
+        const double s0 = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+        const double s1 = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+        if (s == 0) CHAIN_TRACE(0, 4);
+        double s2 = p.scal_mode == SM_PLAIN ? s0 : sqrt(s1);
+        if (p.scal_mode == SM_NONE) s2 = 1.0;
+        const double inv_s = 1.0 / sqrt(s2);
+        const bool bad = p.scal_mode != SM_NONE &&
+                         (!(s0 > 0.0) || !isfinite(s0) || !(s2 > 0.0) || !isfinite(s2) || !isfinite(inv_s));
+        s_scale[s][0] = 1.0 / s2;
+        s_scale[s][1] = inv_s;
+        if (s_t(s) == 0) {
+          double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
+          o[S_TRACE] = s0;
+          o[S_FRO2] = s1;
+          o[S_S2] = s2;
+          o[S_INV_S] = inv_s;
+          if (p.status) p.status[b] = bad ? 2 : 0;
         }
       }
     }
-    tmem_wait_st();
-    fence_proxy_async_global();
     named_bar_sync(1, 128);
-    if (tid == 0) {
-      CHAIN_TRACE(0, 3);
-      grid_arrive(p.gbar, 1);  // C_1 published
+    const float alpha_f = static_cast<float>(p.alpha);
+
+    // ---- C_1 = G / s^2 (global buffer 0), D = 2 C_1, P = alpha I - coef_1 C_1 (TMEM)
+    for (int s = 0; s < ns; ++s) {
+      const int ti = s_ti(s), tj = s_tj(s);
+      const int gr = ti * 128 + r;
+      const bool row_ok = gr < p.h;
+      const int64_t mbase = static_cast<int64_t>(s_b(s)) * p.mat;
+      const float inv_s2 = static_cast<float>(s_scale[s][0]);
+      for (int c = 0; c < 4; ++c) {
+        const int gc0 = tj * 128 + c * 32;
+        uint32_t u[32], pu[32];
+        tmem_ld32(lane_base + s * CH_SLOT + CH_D + c * 32, u);
+        tmem_wait_ld();
+        __align__(16) __nv_bfloat16 hi[32];
+        __align__(16) __nv_bfloat16 lo[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float cv = __uint_as_float(u[j]) * inv_s2;  // fp32 arithmetic: the state is fp32 anyway
+          u[j] = __float_as_uint(2.0f * cv);
+          const float pv = fmaf(-p.coef[0], cv, (gr == gc0 + j && row_ok) ? alpha_f : 0.f);
+          pu[j] = __float_as_uint(pv);
+          split_bf16(cv, hi[j], lo[j]);
+        }
+        tmem_st32(lane_base + s * CH_SLOT + CH_D + c * 32, u);
+        tmem_st32(lane_base + s * CH_SLOT + CH_P + c * 32, pu);
+        if (row_ok && N > 1) {
+          const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            *reinterpret_cast<uint4*>(p.chi[0] + o + j) = *reinterpret_cast<const uint4*>(hi + j);
+            *reinterpret_cast<uint4*>(p.clo[0] + o + j) = *reinterpret_cast<const uint4*>(lo + j);
+          }
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&tempty[s]);  // D_s = 2 C_1 is in place for step 1's MMAs
+      fence_proxy_async_global();
+      named_bar_sync(1, 128);
+      if (tid == 0) {
+        if (s == 0) CHAIN_TRACE(0, 3);
+        grid_arrive(p.gbar + s * CHAIN_ROUNDS, 1);  // group s: C_1 published
+      }
     }
 
     // ---- phase B: squaring steps
-    __shared__ int s_stop;
-    uint32_t acc_phase = 0;
-    int steps = 0;
-    unsigned last_round = 1;  // rounds published so far: 0 (norms), 1 (C_1), then k+1 per step k
-    for (int k = 1; k < N; ++k) {
-      if (k >= 2 && p.trunc_tau > 0.0) {
-        if (tid == 0) s_stop = chain_truncate_before(p, k, grid_wait(p.gbar, k)) ? 1 : 0;
-        named_bar_sync(1, 128);
-        if (s_stop) {  // C_j = I for j > k: P -= tail[k] I on the diagonal; P stays in TMEM
-          const float tl = p.tail[k];
-          for (int c = 0; c < 4; ++c) {
-            const int gc0 = tj * 128 + c * 32;
-            uint32_t up[32];
-            tmem_ld32(lane_base + CH_P + c * 32, up);  // warp-collective: every lane
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (row_ok && gc0 + j == gr) up[j] = __float_as_uint(__uint_as_float(up[j]) - tl);
-            tmem_st32(lane_base + CH_P + c * 32, up);
-          }
-          tmem_wait_st();
-          break;
-        }
-      }
+    uint32_t acc_phase[CH_SLOTS] = {0, 0};
+    int steps[CH_SLOTS] = {0, 0};
+    unsigned last_round[CH_SLOTS] = {1, 1};  // rounds published so far: 0 (norms), 1 (C_1), then k+1 per step k
+    unsigned done = ns < 2 ? 2u : 0u;        // bit s: slot s's chain has stopped (truncated)
+    for (int k = 1; k < N && done != 3u; ++k) {
       const bool last = (k == N - 1);
       const float coef = p.coef[k];  // multiplies C_{k+1}
-      ++steps;
-      mbar_wait(tfull, acc_phase);
-      if (tid == 0) CHAIN_TRACE(k, 3);
-      acc_phase ^= 1;
-      tc_fence_after();
       const bool want_e2 = p.trunc_tau > 0.0 && !last;
-      float e2 = 0.f;  // ||I - C_{k+1}||_F^2 over this thread's part of the tile (weighted below)
-      if (!last) {
-        // Critical path first: C_{k+1} to TMEM and to its global hi/lo copies, the barrier arrival;
-        // the P update (not read by any other tile) follows while the next squaring's MMAs run.
+#pragma unroll
+      for (int s = 0; s < CH_SLOTS; ++s) {
+        if ((done >> s) & 1u) continue;
+        const int ti = s_ti(s), tj = s_tj(s);
+        const int gr = ti * 128 + r;
+        const bool row_ok = gr < p.h;
+        {
+          mbar_wait(&decbar[s], (k - 1) & 1);
+          const int stop = *reinterpret_cast<volatile int*>(&s_dec[s][k & 1]);
+          if (stop) {  // C_j = I for j > k: P -= tail[k] I on the diagonal; P stays in TMEM
+            done |= 1u << s;
+            if (ti == tj) {  // warp-uniform: only diagonal tiles hold diagonal entries
+              const float tl = p.tail[k];
+              for (int c = 0; c < 4; ++c) {
+                const int gc0 = tj * 128 + c * 32;
+                uint32_t up[32];
+                tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);  // warp-collective: every lane
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (row_ok && gc0 + j == gr) up[j] = __float_as_uint(__uint_as_float(up[j]) - tl);
+                tmem_st32(lane_base + s * CH_SLOT + CH_P + c * 32, up);
+              }
+              tmem_wait_st();
+            }
+            continue;
+          }
+        }
+        ++steps[s];
+        const int64_t mbase = static_cast<int64_t>(s_b(s)) * p.mat;
+        mbar_wait(&tfull[s], acc_phase[s]);
+        acc_phase[s] ^= 1;
+        if (tid == 0 && s == 0) CHAIN_TRACE(k, 3);
+        tc_fence_after();
+        float e2 = 0.f;  // ||I - C_{k+1}||_F^2 over this thread's part of the tile (weighted below)
+        // D_s = C_{k+1} (the MMAs subtracted C_k C_k from 2 C_k).  Per 32-column chunk: C_{k+1} to its
+        // global bf16 hi/lo copies, 2 C_{k+1} back into D_s, P -= c_{k+1} C_{k+1} (one TMEM pass; a
+        // separate P pass after the barrier arrival measured slower in both the one- and two-slot forms).
         for (int c = 0; c < 4; ++c) {
           const int gc0 = tj * 128 + c * 32;
-          uint32_t ua[32], uc[32];
-          tmem_ld32(lane_base + CH_ACC + c * 32, ua);
-          tmem_ld32(lane_base + CH_C + c * 32, uc);
+          uint32_t ud[32], up[32];
+          tmem_ld32(lane_base + s * CH_SLOT + CH_D + c * 32, ud);
+          tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);
           tmem_wait_ld();
           __align__(16) __nv_bfloat16 hi[32];
           __align__(16) __nv_bfloat16 lo[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const bool ok = row_ok && gc0 + j < p.h;
-            const float cn = ok ? 2.0f * __uint_as_float(uc[j]) - __uint_as_float(ua[j]) : 0.f;
-            uc[j] = __float_as_uint(cn);
+            const float cn = ok ? __uint_as_float(ud[j]) : 0.f;
+            ud[j] = __float_as_uint(2.0f * cn);
+            up[j] = __float_as_uint(fmaf(-coef, cn, __uint_as_float(up[j])));
             split_bf16(cn, hi[j], lo[j]);
             if (want_e2) {
               const float dv = ok ? cn - (gc0 + j == gr ? 1.f : 0.f) : 0.f;
               e2 = fmaf(dv, dv, e2);
             }
           }
-          tmem_st32(lane_base + CH_C + c * 32, uc);
-          if (row_ok) {
-            const int nb = k & 1;
-            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
+          if (!last) {
+            if (row_ok) {
+              const int nb = k & 1;
+              const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
 #pragma unroll
-            for (int j = 0; j < 32; j += 16) {  // 256-bit stores: whole sectors (ld % 256 == 0)
-              st_global_v8(p.chi[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(hi + j));
-              st_global_v8(p.clo[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(lo + j));
+              for (int j = 0; j < 32; j += 16) {  // 256-bit stores: whole sectors (ld % 256 == 0)
+                st_global_v8(p.chi[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(hi + j));
+                st_global_v8(p.clo[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(lo + j));
+              }
             }
+            tmem_st32(lane_base + s * CH_SLOT + CH_D + c * 32, ud);
           }
+          tmem_st32(lane_base + s * CH_SLOT + CH_P + c * 32, up);  // the final P stays in TMEM for the shifted split
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(tempty);
-        if (want_e2) {
-          const double e2w = warp_sum(wgt * static_cast<double>(e2));
-          if (lane == 0) red[0][ew] = e2w;
-        }
-        fence_proxy_async_global();
-        named_bar_sync(1, 128);
-        if (tid == 0) {
-          CHAIN_TRACE(k, 4);
-          const double part = p.trunc_tau > 0.0 ? red[0][0] + red[0][1] + red[0][2] + red[0][3] : 0.0;
-          grid_arrive(p.gbar, k + 1, part);  // C_{k+1} published, with its ||I - C||_F^2 partial
-        }
-        last_round = static_cast<unsigned>(k + 1);
-        // P -= c_{k+1} C_{k+1}, off the critical path (the TMEM C region is not touched by the MMAs)
-        for (int c = 0; c < 4; ++c) {
-          uint32_t uc[32], up[32];
-          tmem_ld32(lane_base + CH_C + c * 32, uc);
-          tmem_ld32(lane_base + CH_P + c * 32, up);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) up[j] = __float_as_uint(__uint_as_float(up[j]) - coef * __uint_as_float(uc[j]));
-          tmem_st32(lane_base + CH_P + c * 32, up);
-        }
-        tmem_wait_st();
-        continue;
-      }
-      for (int c = 0; c < 4; ++c) {
-        const int gc0 = tj * 128 + c * 32;
-        uint32_t ua[32], uc[32], up[32];
-        tmem_ld32(lane_base + CH_ACC + c * 32, ua);
-        tmem_ld32(lane_base + CH_C + c * 32, uc);
-        tmem_ld32(lane_base + CH_P + c * 32, up);
-        tmem_wait_ld();
-        __align__(16) __nv_bfloat16 hi[32];
-        __align__(16) __nv_bfloat16 lo[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const bool ok = row_ok && gc0 + j < p.h;
-          const float cn = ok ? 2.0f * __uint_as_float(uc[j]) - __uint_as_float(ua[j]) : 0.f;
-          const float pv = __uint_as_float(up[j]) - coef * cn;
-          uc[j] = __float_as_uint(cn);
-          up[j] = __float_as_uint(pv);
-          split_bf16(cn, hi[j], lo[j]);
-          if (want_e2) {
-            const float dv = ok ? cn - (gc0 + j == gr ? 1.f : 0.f) : 0.f;
-            e2 = fmaf(dv, dv, e2);
-          }
-        }
+        mbar_arrive(&tempty[s]);
         if (!last) {
-          tmem_st32(lane_base + CH_C + c * 32, uc);
-          tmem_st32(lane_base + CH_P + c * 32, up);
-          if (row_ok) {
-            const int nb = k & 1;
-            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
-#pragma unroll
-            for (int j = 0; j < 32; j += 16) {  // 256-bit stores: whole sectors (ld % 256 == 0)
-              st_global_v8(p.chi[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(hi + j));
-              st_global_v8(p.clo[nb] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(lo + j));
-            }
+          if (want_e2) {
+            const double e2w = warp_sum(((ti == tj) ? 1.0 : 2.0) * static_cast<double>(e2));
+            if (lane == 0) red[0][ew] = e2w;
           }
-        } else {
-          tmem_st32(lane_base + CH_P + c * 32, up);  // final P stays in TMEM for the shifted split
+          fence_proxy_async_global();
+          named_bar_sync(1, 128);
+          if (tid == 0) {
+            if (s == 0) CHAIN_TRACE(k, 4);
+            const double part = p.trunc_tau > 0.0 ? red[0][0] + red[0][1] + red[0][2] + red[0][3] : 0.0;
+            // group s: C_{k+1} published, with its ||I - C||_F^2 partial
+            grid_arrive(p.gbar + s * CHAIN_ROUNDS, k + 1, part);
+          }
+          last_round[s] = static_cast<unsigned>(k + 1);
+          named_bar_sync(1, 128);  // red[] consumed before the next slot / step rewrites it
         }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(tempty);
-      if (!last) {
-        if (want_e2) {
-          const double e2w = warp_sum(wgt * static_cast<double>(e2));
-          if (lane == 0) red[0][ew] = e2w;
-        }
-        fence_proxy_async_global();
-        named_bar_sync(1, 128);
-        if (tid == 0) {
-          CHAIN_TRACE(k, 4);
-          const double part = p.trunc_tau > 0.0 ? red[0][0] + red[0][1] + red[0][2] + red[0][3] : 0.0;
-          grid_arrive(p.gbar, k + 1, part);  // C_{k+1} published, with its ||I - C||_F^2 partial
-        }
-        last_round = static_cast<unsigned>(k + 1);
       }
     }
     // ---- final P: statistics -> identity shift d and the adaptive apply decision, then
     //      R/s = (P - d I)/s split into bf16 hi/lo, written symmetric for the apply.
     {
       if (tid == 0) CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 0);
-      double trp = 0.0, sp2 = 0.0;
-      for (int c = 0; c < 4; ++c) {
-        const int gc0 = tj * 128 + c * 32;
-        uint32_t up[32];
-        tmem_ld32(lane_base + CH_P + c * 32, up);
-        tmem_wait_ld();
-        float s2c = 0.f;  // fp32 partial over 32 columns, fp64 across chunks
+      for (int s = 0; s < ns; ++s) {
+        const int ti = s_ti(s), tj = s_tj(s);
+        const int gr = ti * 128 + r;
+        const bool row_ok = gr < p.h;
+        const double wgt = (ti == tj) ? 1.0 : 2.0;
+        double trp = 0.0, sp2 = 0.0;
+        for (int c = 0; c < 4; ++c) {
+          const int gc0 = tj * 128 + c * 32;
+          uint32_t up[32];
+          tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);
+          tmem_wait_ld();
+          float s2c = 0.f;  // fp32 partial over 32 columns, fp64 across chunks
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const bool ok = row_ok && gc0 + j < p.h;
-          const float v = ok ? __uint_as_float(up[j]) : 0.f;
-          if (ok && gc0 + j == gr) trp += v;
-          s2c = fmaf(v, v, s2c);
+          for (int j = 0; j < 32; ++j) {
+            const bool ok = row_ok && gc0 + j < p.h;
+            const float v = ok ? __uint_as_float(up[j]) : 0.f;
+            if (ok && gc0 + j == gr) trp += v;
+            s2c = fmaf(v, v, s2c);
+          }
+          sp2 += wgt * static_cast<double>(s2c);
         }
-        sp2 += wgt * static_cast<double>(s2c);
+        trp = warp_sum(trp);
+        sp2 = warp_sum(sp2);
+        named_bar_sync(1, 128);  // red[] free
+        if (lane == 0) {
+          red[0][ew] = trp;
+          red[1][ew] = sp2;
+        }
+        named_bar_sync(1, 128);
+        if (tid == 0) {
+          p.pstat[s_g(s) * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+          p.pstat[s_g(s) * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+        }
       }
-      trp = warp_sum(trp);
-      sp2 = warp_sum(sp2);
-      if (lane == 0) {
-        red[0][ew] = trp;
-        red[1][ew] = sp2;
-      }
-      named_bar_sync(1, 128);
       if (tid == 0) {
-        p.pstat[blockIdx.x * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
-        p.pstat[blockIdx.x * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
-        const int round = static_cast<int>(last_round) + 1;
         CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 1);
-        grid_arrive(p.gbar, round);
-        grid_wait(p.gbar, round);
+        grid_arrive(p.gbar, static_cast<int>(last_round[0]) + 1);
+        if (ns > 1) grid_arrive(p.gbar + CHAIN_ROUNDS, static_cast<int>(last_round[1]) + 1);
+        grid_wait(p.gbar, static_cast<int>(last_round[0]) + 1, cnt(0));
+        if (ns > 1) grid_wait(p.gbar + CHAIN_ROUNDS, static_cast<int>(last_round[1]) + 1, cnt(1));
         CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 2);
       }
       named_bar_sync(1, 128);
-      sum_tile_partials(p.pstat, lb * p.tiles_per_mat, p.tiles_per_mat, tid, red);
-      if (tid == 0) {
-        const double tp = red[0][0] + red[0][1] + red[0][2] + red[0][3];
-        const double s2p = red[1][0] + red[1][1] + red[1][2] + red[1][3];
-        const double d = tp / p.h;
-        const double r2 = fmax(s2p - tp * tp / p.h, 0.0);
-        // ||X (R_hat - R)||_F <= ||X||_2 2^-9 ||R||_F with ||X||_2 <= 1 (gram/plain scaling), and
-        // ||Y||_F >= min_sigma f(sigma)/sigma * ||X||_F = sqrt(tr C_1) (min f(s)/s = f(1) = 1).
-        const double trc = fmax(s_scale[0] * __ldcg(&p.scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_TRACE]), 0.0);
-        const double bound = ldexp(sqrt(r2), -9) / fmax(sqrt(trc), 1e-300);
-        const bool single = p.adaptive && bound <= p.tau;
-        s_scale[0] = d;
-        if (t == 0) {
-          double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
-          o[S_SHIFT] = static_cast<double>(static_cast<float>(d)) * s_scale[1];  // the shift R was formed with
-          o[S_MODE] = single ? 1.0 : 0.0;
-          o[S_BOUND] = bound;
-          o[S_STEPS] = steps;
+      for (int s = 0; s < ns; ++s) {
+        const int b = s_b(s);
+        sum_tile_partials(p.pstat, s_lb(s) * p.tiles_per_mat, p.tiles_per_mat, tid, red);
+        if (tid == 0) {
+          const double tp = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+          const double s2p = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+          const double d = tp / p.h;
+          const double r2 = fmax(s2p - tp * tp / p.h, 0.0);
+          // ||X (R_hat - R)||_F <= ||X||_2 2^-9 ||R||_F with ||X||_2 <= 1 (gram/plain scaling), and
+          // ||Y||_F >= min_sigma f(sigma)/sigma * ||X||_F = sqrt(tr C_1) (min f(s)/s = f(1) = 1).
+          const double trc =
+              fmax(s_scale[s][0] * __ldcg(&p.scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_TRACE]), 0.0);
+          const double bound = ldexp(sqrt(r2), -9) / fmax(sqrt(trc), 1e-300);
+          const bool single = p.adaptive && bound <= p.tau;
+          s_scale[s][0] = d;
+          if (s_t(s) == 0) {
+            double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
+            o[S_SHIFT] = static_cast<double>(static_cast<float>(d)) * s_scale[s][1];  // the shift R was formed with
+            o[S_MODE] = single ? 1.0 : 0.0;
+            o[S_BOUND] = bound;
+            o[S_STEPS] = s == 0 ? steps[0] : steps[1];
+          }
         }
       }
       named_bar_sync(1, 128);
-      const double d = s_scale[0];
-      const float d_f = static_cast<float>(d), inv_s_f = static_cast<float>(s_scale[1]);
-      if ((p.h & 31) == 0) {
-        // Whole 32 x 32 blocks: every lane stores its row segment with 16-byte vector stores, and
-        // the mirror block goes through a per-warp shared-memory transpose (the pipeline stages
-        // are idle now), so every global store is a run of whole sectors.
-        uint32_t* tb = reinterpret_cast<uint32_t*>(smem) + ew * 32 * 33;
-        const int gr0 = ti * 128 + ew * 32;
-        for (int c = 0; c < 4; ++c) {
-          const int gc0 = tj * 128 + c * 32;
-          uint32_t up[32];
-          tmem_ld32(lane_base + CH_P + c * 32, up);  // warp-collective: every lane
-          tmem_wait_ld();
-          const bool diag = ti == tj && c == ew;        // block straddling the diagonal
-          if (gr0 >= p.h || gc0 >= p.h || (ti == tj && c < ew)) continue;  // warp-uniform
-          uint32_t hl[32];                              // (hi << 16) | lo of row gr, columns gc0 + j
+      for (int s = 0; s < ns; ++s) {
+        const int ti = s_ti(s), tj = s_tj(s);
+        const int gr = ti * 128 + r;
+        const bool row_ok = gr < p.h;
+        const int64_t mbase = static_cast<int64_t>(s_b(s)) * p.mat;
+        const float d_f = static_cast<float>(s_scale[s][0]), inv_s_f = static_cast<float>(s_scale[s][1]);
+        if ((p.h & 31) == 0) {
+          // Whole 32 x 32 blocks: every lane stores its row segment with 16-byte vector stores, and
+          // the mirror block goes through a per-warp shared-memory transpose (the pipeline stages
+          // are idle now), so every global store is a run of whole sectors.
+          uint32_t* tb = reinterpret_cast<uint32_t*>(smem) + ew * 32 * 33;
+          const int gr0 = ti * 128 + ew * 32;
+          for (int c = 0; c < 4; ++c) {
+            const int gc0 = tj * 128 + c * 32;
+            uint32_t up[32];
+            tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);  // warp-collective: every lane
+            tmem_wait_ld();
+            const bool diag = ti == tj && c == ew;        // block straddling the diagonal
+            if (gr0 >= p.h || gc0 >= p.h || (ti == tj && c < ew)) continue;  // warp-uniform
+            uint32_t hl[32];                              // (hi << 16) | lo of row gr, columns gc0 + j
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float rv = __uint_as_float(up[j]) - (gc0 + j == gr ? d_f : 0.f);
-            __nv_bfloat16 hi, lo;
-            split_bf16(rv * inv_s_f, hi, lo);
-            hl[j] = (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16) | __bfloat16_as_ushort(lo);
-          }
-#pragma unroll
-          for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = hl[j];
-          __syncwarp();
-          if (diag) {  // lower half of the block from the transposed upper half: exact symmetry
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j < lane) hl[j] = tb[j * 33 + lane];
-          }
-          const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            uint4 vh, vl;
-            vh.x = (hl[j] >> 16) | (hl[j + 1] & 0xFFFF0000u);
-            vh.y = (hl[j + 2] >> 16) | (hl[j + 3] & 0xFFFF0000u);
-            vh.z = (hl[j + 4] >> 16) | (hl[j + 5] & 0xFFFF0000u);
-            vh.w = (hl[j + 6] >> 16) | (hl[j + 7] & 0xFFFF0000u);
-            vl.x = (hl[j] & 0xFFFFu) | (hl[j + 1] << 16);
-            vl.y = (hl[j + 2] & 0xFFFFu) | (hl[j + 3] << 16);
-            vl.z = (hl[j + 4] & 0xFFFFu) | (hl[j + 5] << 16);
-            vl.w = (hl[j + 6] & 0xFFFFu) | (hl[j + 7] << 16);
-            *reinterpret_cast<uint4*>(p.phi + o + j) = vh;
-            *reinterpret_cast<uint4*>(p.plo + o + j) = vl;
-          }
-          if (!diag) {  // mirror: lane writes row gc0 + lane, columns gr0 .. gr0 + 31
-            const int64_t om = mbase + static_cast<int64_t>(gc0 + lane) * p.ld + gr0;
-#pragma unroll
-            for (int m = 0; m < 32; m += 8) {
-              uint32_t w[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) w[e] = tb[(m + e) * 33 + lane];
-              uint4 vh, vl;
-              vh.x = (w[0] >> 16) | (w[1] & 0xFFFF0000u);
-              vh.y = (w[2] >> 16) | (w[3] & 0xFFFF0000u);
-              vh.z = (w[4] >> 16) | (w[5] & 0xFFFF0000u);
-              vh.w = (w[6] >> 16) | (w[7] & 0xFFFF0000u);
-              vl.x = (w[0] & 0xFFFFu) | (w[1] << 16);
-              vl.y = (w[2] & 0xFFFFu) | (w[3] << 16);
-              vl.z = (w[4] & 0xFFFFu) | (w[5] << 16);
-              vl.w = (w[6] & 0xFFFFu) | (w[7] << 16);
-              *reinterpret_cast<uint4*>(p.phi + om + m) = vh;
-              *reinterpret_cast<uint4*>(p.plo + om + m) = vl;
-            }
-          }
-          __syncwarp();
-        }
-      } else {
-        for (int c = 0; c < 4; ++c) {
-          const int gc0 = tj * 128 + c * 32;
-          uint32_t up[32];
-          tmem_ld32(lane_base + CH_P + c * 32, up);  // warp-collective: every lane, row_ok or not
-          tmem_wait_ld();
-          if (row_ok) {
             for (int j = 0; j < 32; ++j) {
-              const int gc = gc0 + j;
-              if (gc >= p.h || (ti == tj && gc < gr)) continue;
-              const float rv = __uint_as_float(up[j]) - (gc == gr ? d_f : 0.f);
+              const float rv = __uint_as_float(up[j]) - (gc0 + j == gr ? d_f : 0.f);
               __nv_bfloat16 hi, lo;
               split_bf16(rv * inv_s_f, hi, lo);
-              const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
-              const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
-              p.phi[o] = hi;
-              p.plo[o] = lo;
-              p.phi[om] = hi;
-              p.plo[om] = lo;
+              hl[j] = (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16) | __bfloat16_as_ushort(lo);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = hl[j];
+            __syncwarp();
+            if (diag) {  // lower half of the block from the transposed upper half: exact symmetry
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < lane) hl[j] = tb[j * 33 + lane];
+            }
+            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint4 vh, vl;
+              vh.x = (hl[j] >> 16) | (hl[j + 1] & 0xFFFF0000u);
+              vh.y = (hl[j + 2] >> 16) | (hl[j + 3] & 0xFFFF0000u);
+              vh.z = (hl[j + 4] >> 16) | (hl[j + 5] & 0xFFFF0000u);
+              vh.w = (hl[j + 6] >> 16) | (hl[j + 7] & 0xFFFF0000u);
+              vl.x = (hl[j] & 0xFFFFu) | (hl[j + 1] << 16);
+              vl.y = (hl[j + 2] & 0xFFFFu) | (hl[j + 3] << 16);
+              vl.z = (hl[j + 4] & 0xFFFFu) | (hl[j + 5] << 16);
+              vl.w = (hl[j + 6] & 0xFFFFu) | (hl[j + 7] << 16);
+              *reinterpret_cast<uint4*>(p.phi + o + j) = vh;
+              *reinterpret_cast<uint4*>(p.plo + o + j) = vl;
+            }
+            if (!diag) {  // mirror: lane writes row gc0 + lane, columns gr0 .. gr0 + 31
+              const int64_t om = mbase + static_cast<int64_t>(gc0 + lane) * p.ld + gr0;
+#pragma unroll
+              for (int m = 0; m < 32; m += 8) {
+                uint32_t w[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) w[e] = tb[(m + e) * 33 + lane];
+                uint4 vh, vl;
+                vh.x = (w[0] >> 16) | (w[1] & 0xFFFF0000u);
+                vh.y = (w[2] >> 16) | (w[3] & 0xFFFF0000u);
+                vh.z = (w[4] >> 16) | (w[5] & 0xFFFF0000u);
+                vh.w = (w[6] >> 16) | (w[7] & 0xFFFF0000u);
+                vl.x = (w[0] & 0xFFFFu) | (w[1] << 16);
+                vl.y = (w[2] & 0xFFFFu) | (w[3] << 16);
+                vl.z = (w[4] & 0xFFFFu) | (w[5] << 16);
+                vl.w = (w[6] & 0xFFFFu) | (w[7] << 16);
+                *reinterpret_cast<uint4*>(p.phi + om + m) = vh;
+                *reinterpret_cast<uint4*>(p.plo + om + m) = vl;
+              }
+            }
+            __syncwarp();
+          }
+        } else {
+          for (int c = 0; c < 4; ++c) {
+            const int gc0 = tj * 128 + c * 32;
+            uint32_t up[32];
+            tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);  // warp-collective: every lane, row_ok or not
+            tmem_wait_ld();
+            if (row_ok) {
+              for (int j = 0; j < 32; ++j) {
+                const int gc = gc0 + j;
+                if (gc >= p.h || (ti == tj && gc < gr)) continue;
+                const float rv = __uint_as_float(up[j]) - (gc == gr ? d_f : 0.f);
+                __nv_bfloat16 hi, lo;
+                split_bf16(rv * inv_s_f, hi, lo);
+                const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
+                const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
+                p.phi[o] = hi;
+                p.plo[o] = lo;
+                p.phi[om] = hi;
+                p.plo[om] = lo;
+              }
             }
           }
         }

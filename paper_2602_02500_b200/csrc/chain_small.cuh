@@ -23,6 +23,7 @@
 
 namespace unso {
 
+constexpr uint32_t CH_ACC = 0, CH_C = 256;       // this kernel's TMEM columns: accumulator, C_k (P at CH_P = 128)
 constexpr int CS_EPI_WARPS = 8;                  // two per TMEM lane quarter, each on two 32-column chunks
 constexpr int CS_THREADS = 128 + 32 * CS_EPI_WARPS;  // warp 1 issues MMAs, warp 2 owns TMEM, warps 4.. epilogue
 constexpr int CS_EPI = 32 * CS_EPI_WARPS;

@@ -307,4 +307,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_
          | (static_cast<uint32_t>(M >> 4) << 24);    // M / 16
 }
 
+// kind::f16 / kind::tf32 only: D += (-A) B
+constexpr uint32_t IDESC_NEGATE_A = 1u << 13;
+
 }  // namespace unso

@@ -635,7 +635,7 @@ static Plan make_plan(const Problem& p, bool with_gram, bool for_error = false) 
         pl.C8l[i] = take(pl, static_cast<size_t>(B * pl.hh));
         pl.C8i[i] = take(pl, static_cast<size_t>(B * pl.hh) * 2);
       }
-      pl.gbar = take(pl, CHAIN_ROUNDS * 8);
+      pl.gbar = take(pl, CH_SLOTS * CHAIN_ROUNDS * 8);  // persistent chain: one set of rounds per matrix group
     } else {
       pl.C[0] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
       pl.C[1] = take(pl, static_cast<size_t>(B * pl.hh) * 8);
@@ -1395,9 +1395,9 @@ static bool chain_persistent_fits(const Problem& p) {
   const int64_t tpm = nt * (nt + 1) / 2;
   const int64_t cap = static_cast<int64_t>(max_blocks_per_sm) * device_sm_count();
   if (tpm > cap) return false;
-  // batches run in co-resident chunks; more than ~4 chunks is better served by the
-  // multi-launch pipeline (each launch then covers the whole batch)
-  const int64_t per = cap / tpm;
+  // batches run in co-resident chunks (up to two tiles per CTA); more than ~4 chunks is better
+  // served by the multi-launch pipeline (each launch then covers the whole batch)
+  const int64_t per = CH_SLOTS * (cap / tpm);
   return (p.batch + per - 1) / per <= 4;
 }
 
@@ -1472,17 +1472,26 @@ static int32_t scale_chain_bf16_persistent(const Problem& p, const Plan& pl, voi
   ChainParams cp = chain_params(p, pl, ws, part, splits, part_ld, part_mat, status);
   prof_mark(3, st);
   // co-resident chunks of the batch, one cooperative launch each (same stream: the barrier word
-  // and per-tile buffers are reused after the previous chunk completes)
+  // and per-tile buffers are reused after the previous chunk completes).  A chunk holds up to
+  // CH_SLOTS tiles per CTA; chunks are balanced so no launch runs a nearly empty grid.
   int nb_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb_sm, chain_persistent_kernel, 256, CH_SMEM);
-  const int per = std::max(1, nb_sm * device_sm_count() / cp.tiles_per_mat);
+  const int cap = nb_sm * device_sm_count();
+  const int per_max = std::max(1, CH_SLOTS * (cap / cp.tiles_per_mat));
+  const int nchunks = (static_cast<int>(p.batch) + per_max - 1) / per_max;
+  const int per = (static_cast<int>(p.batch) + nchunks - 1) / nchunks;
   for (int b0 = 0; b0 < static_cast<int>(p.batch); b0 += per) {
     const int nb = std::min(per, static_cast<int>(p.batch) - b0);
     cp.b0 = b0;
-    if (cudaMemsetAsync(cp.gbar, 0, CHAIN_ROUNDS * sizeof(unsigned long long), st) != cudaSuccess)
+    cp.nb = nb;
+    // one wave cannot hold the chunk: two matrix groups, slot s of every CTA in group s (whole matrices
+    // per group: each group runs its own barrier rounds, chain_persistent.cuh)
+    const int tiles = cp.tiles_per_mat * nb;
+    const int grid = tiles <= cap ? tiles : cp.tiles_per_mat * ((nb + 1) / 2);
+    if (cudaMemsetAsync(cp.gbar, 0, CH_SLOTS * CHAIN_ROUNDS * sizeof(unsigned long long), st) != cudaSuccess)
       return UNSO_ERR_CUDA;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(cp.tiles_per_mat * nb));
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = CH_SMEM;
     cfg.stream = st;

@@ -7,7 +7,7 @@
 #include "ptx_sm100.cuh"
 using namespace unso;
 
-template <bool I8>
+template <bool I8, bool NEG = false>
 __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t done;
@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long l
     const uint32_t a = smem_u32(smem), b = a + 32768;
     const uint64_t da = sdesc_sw128(a, 16, 1024), db = sdesc_sw128(b, 16, 1024);
     const uint32_t idesc = I8 ? ((2u << 4) | (1u << 7) | (1u << 10) | (256u >> 3 << 17) | (256u >> 4 << 24))
-                              : idesc_bf16(256, 256, 0, 0);
+                              : (idesc_bf16(256, 256, 0, 0) | (NEG ? IDESC_NEGATE_A : 0u));
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (int i = 0; i < iters; ++i) {
 #pragma unroll
@@ -59,12 +59,12 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long l
   }
 }
 
-template <bool I8>
+template <bool I8, bool NEG = false>
 void run(int sms) {
   const int pairs = sms / 2, iters = 20000;
   unsigned long long* d;
   cudaMalloc(&d, pairs * 8);
-  cudaFuncSetAttribute(peak_kernel<I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cudaFuncSetAttribute(peak_kernel<I8, NEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(128);
@@ -82,7 +82,7 @@ void run(int sms) {
   float ms = 0;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    cudaLaunchKernelEx(&cfg, peak_kernel<I8>, iters, d);
+    cudaLaunchKernelEx(&cfg, peak_kernel<I8, NEG>, iters, d);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
@@ -90,7 +90,7 @@ void run(int sms) {
   const double k = I8 ? 32 : 16;
   const double ops = 2.0 * 256 * 256 * k * 8.0 * iters * pairs;
   printf("%s: %.3f ms, %.1f T%s/s dense (%d pairs, M=256 N=256 K=%d per instruction) err=%s\n",
-         I8 ? "kind::i8 " : "kind::f16", ms, ops / (ms * 1e-3) / 1e12, I8 ? "OP" : "FLOP", pairs, (int)k,
+         I8 ? "kind::i8 " : (NEG ? "kind::f16 negated A" : "kind::f16"), ms, ops / (ms * 1e-3) / 1e12, I8 ? "OP" : "FLOP", pairs, (int)k,
          cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -98,6 +98,7 @@ int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run<false>(sms);
+  run<false, true>(sms);
   run<true>(sms);
   run<false>(sms);
   run<true>(sms);
