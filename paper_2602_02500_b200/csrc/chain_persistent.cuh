@@ -99,7 +99,7 @@ constexpr int CHAIN_ROUNDS = CHAIN_MAX_ORDER + 2;
 constexpr double CHAIN_FIX = 8589934592.0;  // 2^33
 __device__ __forceinline__ void grid_arrive(unsigned long long* gbar, int round, double partial = 0.0) {
   const double c = fmin(fmax(partial, 0.0), 1.0);
-  __threadfence();
+  // no __threadfence(): the release is cumulative over the CTA's writes ordered before it by bar.sync
   red_release_gpu_add_u64(gbar + round, (1ull << 48) + static_cast<uint64_t>(c * CHAIN_FIX));
 }
 __device__ __forceinline__ uint64_t grid_wait(const unsigned long long* gbar, int round, unsigned count = 0) {
@@ -107,7 +107,7 @@ __device__ __forceinline__ uint64_t grid_wait(const unsigned long long* gbar, in
   const uint64_t T = count ? count : gridDim.x;
   uint64_t v;
   while (((v = ld_acquire_gpu_u64(gbar + round)) >> 48) < T) {
-    __nanosleep(64);
+    __nanosleep(20);
     if (clock64() - t0 > UNSO_WATCHDOG_CYCLES) __trap();
   }
   return v & ((1ull << 48) - 1);
@@ -132,23 +132,26 @@ __device__ __forceinline__ bool chain_truncate_before(const ChainParams& p, int 
   return chain_tail_bound(p.coef, p.order, k, static_cast<double>(sum) / CHAIN_FIX) <= p.trunc_tau;
 }
 
-// Sum of the launch-wide per-tile (x, y) partials of matrix `lb` by the 128 epilogue threads after the
+// Sum of the launch-wide per-tile (x, y) partials of one matrix by all 256 threads of the CTA after the
 // grid barrier: strided loads, fixed shuffle tree per warp, warps summed in order -- the same bits
-// on every CTA of the matrix.  Result in red[0][0] / red[1][0] after the trailing barrier.
-__device__ __forceinline__ void sum_tile_partials(const double* buf, int first, int n, int tid, double (*red)[4]) {
+// on every CTA of the matrix.  Result: sum of red[0][0..7] / red[1][0..7] after the trailing barrier.
+__device__ __forceinline__ void sum_tile_partials(const double* buf, int first, int n, double (*red)[8]) {
   double a = 0.0, c = 0.0;
-  for (int q = tid; q < n; q += 128) {
+  for (int q = threadIdx.x; q < n; q += 256) {
     a += __ldcg(&buf[(first + q) * 2 + 0]);
     c += __ldcg(&buf[(first + q) * 2 + 1]);
   }
   a = warp_sum(a);
   c = warp_sum(c);
-  named_bar_sync(1, 128);  // red[] free (its previous contents were consumed before the grid barrier)
-  if ((tid & 31) == 0) {
-    red[0][tid >> 5] = a;
-    red[1][tid >> 5] = c;
+  __syncthreads();  // red[] free
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a;
+    red[1][threadIdx.x >> 5] = c;
   }
-  named_bar_sync(1, 128);
+  __syncthreads();
+}
+__device__ __forceinline__ double sum8(const double* r) {
+  return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
 }
 
 constexpr int CH_STAGES = 3;
@@ -188,7 +191,9 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
   // Only the producer polls the global barrier words; it posts each step's decision (0 = run step k,
   // 1 = the chain of this slot's group stops before step k) for the MMA and epilogue roles.
   __shared__ int s_dec[CH_SLOTS][2];
-  __shared__ double red[2][4];
+  __shared__ double red[2][8];
+  __shared__ int s_steps[CH_SLOTS];
+  __shared__ unsigned s_last_round[CH_SLOTS];
   __shared__ double s_scale[CH_SLOTS][2];  // per slot: inv_s2 (later the shift d), inv_s
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -236,6 +241,156 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+
+
+  // ================================================================== phase A (all 8 warps)
+  // G tile = sum of split-K partials -> TMEM D region; tile norms; scale; C_1, D = 2 C_1, P.
+  // Warp w owns TMEM lanes 32 (w & 3) .. + 31 (row r of the tile per thread); warps 4-7 take the
+  // column chunks 0-1 of every tile and warps 0-3 the chunks 2-3 (the producer / MMA roles start after C_1).
+  const int ew = warp & 3;
+  const int r = ew * 32 + lane;
+  const int c0 = warp >= 4 ? 0 : 2;  // first of this warp's two 32-column chunks
+  const uint32_t lane_base = tmem + (static_cast<uint32_t>(ew * 32) << 16);
+  if (threadIdx.x == 128) CHAIN_TRACE(0, 0);
+  for (int s = 0; s < ns; ++s) {
+    const int ti = s_ti(s), tj = s_tj(s), b = s_b(s);
+    const int gr = ti * 128 + r;
+    const bool row_ok = gr < p.h;
+    double tr = 0.0, fr = 0.0;
+    const double wgt = (ti == tj) ? 1.0 : 2.0;
+    // both 32-column chunks of a split-K slice are loaded before any is summed (16 independent
+    // 16-byte loads in flight per thread, 256 threads: the phase is load-latency-bound)
+    float g2[2][32];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) g2[c][j] = 0.f;
+    if (row_ok) {
+      for (int sp = 0; sp < p.splits; ++sp) {
+        const float* src = p.part + (static_cast<int64_t>(sp) * p.batch + b) * p.part_mat +
+                           static_cast<int64_t>(gr) * p.part_ld + tj * 128 + c0 * 32;
+        float4 v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = __ldcg(reinterpret_cast<const float4*>(src) + q);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          float* gq = &g2[q >> 3][(q & 7) * 4];
+          gq[0] += v[q].x;
+          gq[1] += v[q].y;
+          gq[2] += v[q].z;
+          gq[3] += v[q].w;
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int gc0 = tj * 128 + (c0 + c) * 32;
+      uint32_t u[32];
+      float frc = 0.f;  // fp32 partial over the 32 columns, accumulated in fp64 across chunks
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const bool ok = row_ok && (gc0 + j) < p.h;
+        const float v = ok ? g2[c][j] : 0.f;
+        if (ok && gc0 + j == gr) tr += v;
+        frc = fmaf(v, v, frc);
+        u[j] = __float_as_uint(v);
+      }
+      fr += wgt * static_cast<double>(frc);
+      tmem_st32(lane_base + s * CH_SLOT + CH_D + (c0 + c) * 32, u);
+    }
+    tmem_wait_st();
+    tr = warp_sum(tr);
+    fr = warp_sum(fr);
+    __syncthreads();  // red[] free (slot 0's sums were consumed)
+    if (lane == 0) {
+      red[0][warp] = tr;
+      red[1][warp] = fr;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      p.normbuf[s_g(s) * 2 + 0] = sum8(red[0]);
+      p.normbuf[s_g(s) * 2 + 1] = sum8(red[1]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    CHAIN_TRACE(0, 1);
+    for (int s = 0; s < ns; ++s) grid_arrive(p.gbar + s * CHAIN_ROUNDS, 0);
+    for (int s = 0; s < ns; ++s) grid_wait(p.gbar + s * CHAIN_ROUNDS, 0, cnt(s));
+    CHAIN_TRACE(0, 2);
+  }
+  __syncthreads();  // every thread is past the grid barrier
+  for (int s = 0; s < ns; ++s) {
+    const int b = s_b(s);
+    sum_tile_partials(p.normbuf, s_lb(s) * p.tiles_per_mat, p.tiles_per_mat, red);
+    if (threadIdx.x == 0) {
+      const double s0 = sum8(red[0]);
+      const double s1 = sum8(red[1]);
+      if (s == 0) CHAIN_TRACE(0, 4);
+      double s2 = p.scal_mode == SM_PLAIN ? s0 : sqrt(s1);
+      if (p.scal_mode == SM_NONE) s2 = 1.0;
+      const double inv_s = 1.0 / sqrt(s2);
+      const bool bad = p.scal_mode != SM_NONE &&
+                       (!(s0 > 0.0) || !isfinite(s0) || !(s2 > 0.0) || !isfinite(s2) || !isfinite(inv_s));
+      s_scale[s][0] = 1.0 / s2;
+      s_scale[s][1] = inv_s;
+      if (s_t(s) == 0) {
+        double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
+        o[S_TRACE] = s0;
+        o[S_FRO2] = s1;
+        o[S_S2] = s2;
+        o[S_INV_S] = inv_s;
+        if (p.status) p.status[b] = bad ? 2 : 0;
+      }
+    }
+  }
+  __syncthreads();
+  {
+    const float alpha_f = static_cast<float>(p.alpha);
+    // ---- C_1 = G / s^2 (global buffer 0), D = 2 C_1, P = alpha I - coef_1 C_1 (TMEM)
+    for (int s = 0; s < ns; ++s) {
+      const int ti = s_ti(s), tj = s_tj(s);
+      const int gr = ti * 128 + r;
+      const bool row_ok = gr < p.h;
+      const int64_t mbase = static_cast<int64_t>(s_b(s)) * p.mat;
+      const float inv_s2 = static_cast<float>(s_scale[s][0]);
+      for (int c = c0; c < c0 + 2; ++c) {
+        const int gc0 = tj * 128 + c * 32;
+        uint32_t u[32], pu[32];
+        tmem_ld32(lane_base + s * CH_SLOT + CH_D + c * 32, u);
+        tmem_wait_ld();
+        __align__(16) __nv_bfloat16 hi[32];
+        __align__(16) __nv_bfloat16 lo[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float cv = __uint_as_float(u[j]) * inv_s2;  // fp32 arithmetic: the state is fp32 anyway
+          u[j] = __float_as_uint(2.0f * cv);
+          const float pv = fmaf(-p.coef[0], cv, (gr == gc0 + j && row_ok) ? alpha_f : 0.f);
+          pu[j] = __float_as_uint(pv);
+          split_bf16(cv, hi[j], lo[j]);
+        }
+        tmem_st32(lane_base + s * CH_SLOT + CH_D + c * 32, u);
+        tmem_st32(lane_base + s * CH_SLOT + CH_P + c * 32, pu);
+        if (row_ok && N > 1) {
+          const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            *reinterpret_cast<uint4*>(p.chi[0] + o + j) = *reinterpret_cast<const uint4*>(hi + j);
+            *reinterpret_cast<uint4*>(p.clo[0] + o + j) = *reinterpret_cast<const uint4*>(lo + j);
+          }
+        }
+      }
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    fence_proxy_async_global();
+    __syncthreads();
+    if (warp >= 4)
+      for (int s = 0; s < ns; ++s) mbar_arrive(&tempty[s]);  // D_s = 2 C_1 is in place for step 1's MMAs
+    if (threadIdx.x == 0) {
+      CHAIN_TRACE(0, 3);
+      for (int s = 0; s < ns; ++s) grid_arrive(p.gbar + s * CHAIN_ROUNDS, 1);  // group s: C_1 published
+    }
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -333,151 +488,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue warps
-    const int ew = warp - 4;
-    const int r = ew * 32 + lane;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(ew * 32) << 16);
     const int tid = threadIdx.x - 128;
-
-    // ---- phase A: G tile = sum of split-K partials -> TMEM D region; tile norms
-    if (tid == 0) CHAIN_TRACE(0, 0);
-    for (int s = 0; s < ns; ++s) {
-      const int ti = s_ti(s), tj = s_tj(s), b = s_b(s);
-      const int gr = ti * 128 + r;
-      const bool row_ok = gr < p.h;
-      double tr = 0.0, fr = 0.0;
-      const double wgt = (ti == tj) ? 1.0 : 2.0;
-      // all four 32-column chunks of a split-K slice are loaded before any is summed: 32 independent
-      // 16-byte loads in flight per thread (the phase was load-latency-bound chunk by chunk)
-      float g4[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int j = 0; j < 32; ++j) g4[c][j] = 0.f;
-      if (row_ok) {
-        for (int sp = 0; sp < p.splits; ++sp) {
-          const float* src = p.part + (static_cast<int64_t>(sp) * p.batch + b) * p.part_mat +
-                             static_cast<int64_t>(gr) * p.part_ld + tj * 128;
-          float4 v[32];
-#pragma unroll
-          for (int q = 0; q < 32; ++q) v[q] = __ldcg(reinterpret_cast<const float4*>(src) + q);
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            float* gq = &g4[q >> 3][(q & 7) * 4];
-            gq[0] += v[q].x;
-            gq[1] += v[q].y;
-            gq[2] += v[q].z;
-            gq[3] += v[q].w;
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int gc0 = tj * 128 + c * 32;
-        uint32_t u[32];
-        float frc = 0.f;  // fp32 partial over the 32 columns, accumulated in fp64 across chunks
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const bool ok = row_ok && (gc0 + j) < p.h;
-          const float v = ok ? g4[c][j] : 0.f;
-          if (ok && gc0 + j == gr) tr += v;
-          frc = fmaf(v, v, frc);
-          u[j] = __float_as_uint(v);
-        }
-        fr += wgt * static_cast<double>(frc);
-        tmem_st32(lane_base + s * CH_SLOT + CH_D + c * 32, u);
-      }
-      tmem_wait_st();
-      tr = warp_sum(tr);
-      fr = warp_sum(fr);
-      named_bar_sync(1, 128);  // red[] free (slot 0's sums were consumed)
-      if (lane == 0) {
-        red[0][ew] = tr;
-        red[1][ew] = fr;
-      }
-      named_bar_sync(1, 128);
-      if (tid == 0) {
-        p.normbuf[s_g(s) * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
-        p.normbuf[s_g(s) * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
-      }
-    }
-    if (tid == 0) {
-      CHAIN_TRACE(0, 1);
-      for (int s = 0; s < ns; ++s) grid_arrive(p.gbar + s * CHAIN_ROUNDS, 0);
-      for (int s = 0; s < ns; ++s) grid_wait(p.gbar + s * CHAIN_ROUNDS, 0, cnt(s));
-      CHAIN_TRACE(0, 2);
-    }
-    named_bar_sync(1, 128);  // every epilogue thread is past the grid barrier
-    for (int s = 0; s < ns; ++s) {
-      const int b = s_b(s);
-      sum_tile_partials(p.normbuf, s_lb(s) * p.tiles_per_mat, p.tiles_per_mat, tid, red);
-      if (tid == 0) {
-        const double s0 = red[0][0] + red[0][1] + red[0][2] + red[0][3];
-        const double s1 = red[1][0] + red[1][1] + red[1][2] + red[1][3];
-        if (s == 0) CHAIN_TRACE(0, 4);
-        double s2 = p.scal_mode == SM_PLAIN ? s0 : sqrt(s1);
-        if (p.scal_mode == SM_NONE) s2 = 1.0;
-        const double inv_s = 1.0 / sqrt(s2);
-        const bool bad = p.scal_mode != SM_NONE &&
-                         (!(s0 > 0.0) || !isfinite(s0) || !(s2 > 0.0) || !isfinite(s2) || !isfinite(inv_s));
-        s_scale[s][0] = 1.0 / s2;
-        s_scale[s][1] = inv_s;
-        if (s_t(s) == 0) {
-          double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
-          o[S_TRACE] = s0;
-          o[S_FRO2] = s1;
-          o[S_S2] = s2;
-          o[S_INV_S] = inv_s;
-          if (p.status) p.status[b] = bad ? 2 : 0;
-        }
-      }
-    }
-    named_bar_sync(1, 128);
-    const float alpha_f = static_cast<float>(p.alpha);
-
-    // ---- C_1 = G / s^2 (global buffer 0), D = 2 C_1, P = alpha I - coef_1 C_1 (TMEM)
-    for (int s = 0; s < ns; ++s) {
-      const int ti = s_ti(s), tj = s_tj(s);
-      const int gr = ti * 128 + r;
-      const bool row_ok = gr < p.h;
-      const int64_t mbase = static_cast<int64_t>(s_b(s)) * p.mat;
-      const float inv_s2 = static_cast<float>(s_scale[s][0]);
-      for (int c = 0; c < 4; ++c) {
-        const int gc0 = tj * 128 + c * 32;
-        uint32_t u[32], pu[32];
-        tmem_ld32(lane_base + s * CH_SLOT + CH_D + c * 32, u);
-        tmem_wait_ld();
-        __align__(16) __nv_bfloat16 hi[32];
-        __align__(16) __nv_bfloat16 lo[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float cv = __uint_as_float(u[j]) * inv_s2;  // fp32 arithmetic: the state is fp32 anyway
-          u[j] = __float_as_uint(2.0f * cv);
-          const float pv = fmaf(-p.coef[0], cv, (gr == gc0 + j && row_ok) ? alpha_f : 0.f);
-          pu[j] = __float_as_uint(pv);
-          split_bf16(cv, hi[j], lo[j]);
-        }
-        tmem_st32(lane_base + s * CH_SLOT + CH_D + c * 32, u);
-        tmem_st32(lane_base + s * CH_SLOT + CH_P + c * 32, pu);
-        if (row_ok && N > 1) {
-          const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            *reinterpret_cast<uint4*>(p.chi[0] + o + j) = *reinterpret_cast<const uint4*>(hi + j);
-            *reinterpret_cast<uint4*>(p.clo[0] + o + j) = *reinterpret_cast<const uint4*>(lo + j);
-          }
-        }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&tempty[s]);  // D_s = 2 C_1 is in place for step 1's MMAs
-      fence_proxy_async_global();
-      named_bar_sync(1, 128);
-      if (tid == 0) {
-        if (s == 0) CHAIN_TRACE(0, 3);
-        grid_arrive(p.gbar + s * CHAIN_ROUNDS, 1);  // group s: C_1 published
-      }
-    }
-
     // ---- phase B: squaring steps
     uint32_t acc_phase[CH_SLOTS] = {0, 0};
     int steps[CH_SLOTS] = {0, 0};
@@ -580,176 +591,186 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         }
       }
     }
-    // ---- final P: statistics -> identity shift d and the adaptive apply decision, then
-    //      R/s = (P - d I)/s split into bf16 hi/lo, written symmetric for the apply.
-    {
-      if (tid == 0) CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 0);
-      for (int s = 0; s < ns; ++s) {
-        const int ti = s_ti(s), tj = s_tj(s);
-        const int gr = ti * 128 + r;
-        const bool row_ok = gr < p.h;
-        const double wgt = (ti == tj) ? 1.0 : 2.0;
-        double trp = 0.0, sp2 = 0.0;
-        for (int c = 0; c < 4; ++c) {
+    if (tid == 0) {
+      for (int s = 0; s < CH_SLOTS; ++s) {
+        s_steps[s] = steps[s];
+        s_last_round[s] = last_round[s];
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();  // every role is done: P is final in TMEM, the pipeline stages are idle
+  tc_fence_after();
+  // ================================================================== final P (all 8 warps, column
+  // chunks split as in phase A): statistics -> identity shift d and the adaptive apply decision, then
+  // R/s = (P - d I)/s split into bf16 hi/lo, written symmetric for the apply.
+  {
+    if (threadIdx.x == 128) CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 0);
+    for (int s = 0; s < ns; ++s) {
+      const int ti = s_ti(s), tj = s_tj(s);
+      const int gr = ti * 128 + r;
+      const bool row_ok = gr < p.h;
+      const double wgt = (ti == tj) ? 1.0 : 2.0;
+      double trp = 0.0, sp2 = 0.0;
+      for (int c = c0; c < c0 + 2; ++c) {
+        const int gc0 = tj * 128 + c * 32;
+        uint32_t up[32];
+        tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);
+        tmem_wait_ld();
+        float s2c = 0.f;  // fp32 partial over 32 columns, fp64 across chunks
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const bool ok = row_ok && gc0 + j < p.h;
+          const float v = ok ? __uint_as_float(up[j]) : 0.f;
+          if (ok && gc0 + j == gr) trp += v;
+          s2c = fmaf(v, v, s2c);
+        }
+        sp2 += wgt * static_cast<double>(s2c);
+      }
+      trp = warp_sum(trp);
+      sp2 = warp_sum(sp2);
+      __syncthreads();  // red[] free
+      if (lane == 0) {
+        red[0][warp] = trp;
+        red[1][warp] = sp2;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        p.pstat[s_g(s) * 2 + 0] = sum8(red[0]);
+        p.pstat[s_g(s) * 2 + 1] = sum8(red[1]);
+      }
+    }
+    if (threadIdx.x == 0) {
+      CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 1);
+      grid_arrive(p.gbar, static_cast<int>(s_last_round[0]) + 1);
+      if (ns > 1) grid_arrive(p.gbar + CHAIN_ROUNDS, static_cast<int>(s_last_round[1]) + 1);
+      grid_wait(p.gbar, static_cast<int>(s_last_round[0]) + 1, cnt(0));
+      if (ns > 1) grid_wait(p.gbar + CHAIN_ROUNDS, static_cast<int>(s_last_round[1]) + 1, cnt(1));
+      CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 2);
+    }
+    __syncthreads();
+    for (int s = 0; s < ns; ++s) {
+      const int b = s_b(s);
+      sum_tile_partials(p.pstat, s_lb(s) * p.tiles_per_mat, p.tiles_per_mat, red);
+      if (threadIdx.x == 0) {
+        const double tp = sum8(red[0]);
+        const double s2p = sum8(red[1]);
+        const double d = tp / p.h;
+        const double r2 = fmax(s2p - tp * tp / p.h, 0.0);
+        // ||X (R_hat - R)||_F <= ||X||_2 2^-9 ||R||_F with ||X||_2 <= 1 (gram/plain scaling), and
+        // ||Y||_F >= min_sigma f(sigma)/sigma * ||X||_F = sqrt(tr C_1) (min f(s)/s = f(1) = 1).
+        const double trc =
+            fmax(s_scale[s][0] * __ldcg(&p.scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_TRACE]), 0.0);
+        const double bound = ldexp(sqrt(r2), -9) / fmax(sqrt(trc), 1e-300);
+        const bool single = p.adaptive && bound <= p.tau;
+        s_scale[s][0] = d;
+        if (s_t(s) == 0) {
+          double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
+          o[S_SHIFT] = static_cast<double>(static_cast<float>(d)) * s_scale[s][1];  // the shift R was formed with
+          o[S_MODE] = single ? 1.0 : 0.0;
+          o[S_BOUND] = bound;
+          o[S_STEPS] = s_steps[s];
+        }
+      }
+    }
+    __syncthreads();
+    for (int s = 0; s < ns; ++s) {
+      const int ti = s_ti(s), tj = s_tj(s);
+      const int gr = ti * 128 + r;
+      const bool row_ok = gr < p.h;
+      const int64_t mbase = static_cast<int64_t>(s_b(s)) * p.mat;
+      const float d_f = static_cast<float>(s_scale[s][0]), inv_s_f = static_cast<float>(s_scale[s][1]);
+      if ((p.h & 31) == 0) {
+        // Whole 32 x 32 blocks: every lane stores its row segment with 16-byte vector stores, and
+        // the mirror block goes through a per-warp shared-memory transpose (the pipeline stages
+        // are idle now), so every global store is a run of whole sectors.
+        uint32_t* tb = reinterpret_cast<uint32_t*>(smem) + warp * 32 * 33;
+        const int gr0 = ti * 128 + ew * 32;
+        for (int c = c0; c < c0 + 2; ++c) {
           const int gc0 = tj * 128 + c * 32;
           uint32_t up[32];
-          tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);
+          tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);  // warp-collective: every lane
           tmem_wait_ld();
-          float s2c = 0.f;  // fp32 partial over 32 columns, fp64 across chunks
+          const bool diag = ti == tj && c == ew;        // block straddling the diagonal
+          if (gr0 >= p.h || gc0 >= p.h || (ti == tj && c < ew)) continue;  // warp-uniform
+          uint32_t hl[32];                              // (hi << 16) | lo of row gr, columns gc0 + j
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const bool ok = row_ok && gc0 + j < p.h;
-            const float v = ok ? __uint_as_float(up[j]) : 0.f;
-            if (ok && gc0 + j == gr) trp += v;
-            s2c = fmaf(v, v, s2c);
+            const float rv = __uint_as_float(up[j]) - (gc0 + j == gr ? d_f : 0.f);
+            __nv_bfloat16 hi, lo;
+            split_bf16(rv * inv_s_f, hi, lo);
+            hl[j] = (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16) | __bfloat16_as_ushort(lo);
           }
-          sp2 += wgt * static_cast<double>(s2c);
-        }
-        trp = warp_sum(trp);
-        sp2 = warp_sum(sp2);
-        named_bar_sync(1, 128);  // red[] free
-        if (lane == 0) {
-          red[0][ew] = trp;
-          red[1][ew] = sp2;
-        }
-        named_bar_sync(1, 128);
-        if (tid == 0) {
-          p.pstat[s_g(s) * 2 + 0] = red[0][0] + red[0][1] + red[0][2] + red[0][3];
-          p.pstat[s_g(s) * 2 + 1] = red[1][0] + red[1][1] + red[1][2] + red[1][3];
-        }
-      }
-      if (tid == 0) {
-        CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 1);
-        grid_arrive(p.gbar, static_cast<int>(last_round[0]) + 1);
-        if (ns > 1) grid_arrive(p.gbar + CHAIN_ROUNDS, static_cast<int>(last_round[1]) + 1);
-        grid_wait(p.gbar, static_cast<int>(last_round[0]) + 1, cnt(0));
-        if (ns > 1) grid_wait(p.gbar + CHAIN_ROUNDS, static_cast<int>(last_round[1]) + 1, cnt(1));
-        CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 2);
-      }
-      named_bar_sync(1, 128);
-      for (int s = 0; s < ns; ++s) {
-        const int b = s_b(s);
-        sum_tile_partials(p.pstat, s_lb(s) * p.tiles_per_mat, p.tiles_per_mat, tid, red);
-        if (tid == 0) {
-          const double tp = red[0][0] + red[0][1] + red[0][2] + red[0][3];
-          const double s2p = red[1][0] + red[1][1] + red[1][2] + red[1][3];
-          const double d = tp / p.h;
-          const double r2 = fmax(s2p - tp * tp / p.h, 0.0);
-          // ||X (R_hat - R)||_F <= ||X||_2 2^-9 ||R||_F with ||X||_2 <= 1 (gram/plain scaling), and
-          // ||Y||_F >= min_sigma f(sigma)/sigma * ||X||_F = sqrt(tr C_1) (min f(s)/s = f(1) = 1).
-          const double trc =
-              fmax(s_scale[s][0] * __ldcg(&p.scal[static_cast<int64_t>(b) * SCAL_STRIDE + S_TRACE]), 0.0);
-          const double bound = ldexp(sqrt(r2), -9) / fmax(sqrt(trc), 1e-300);
-          const bool single = p.adaptive && bound <= p.tau;
-          s_scale[s][0] = d;
-          if (s_t(s) == 0) {
-            double* o = p.scal + static_cast<int64_t>(b) * SCAL_STRIDE;
-            o[S_SHIFT] = static_cast<double>(static_cast<float>(d)) * s_scale[s][1];  // the shift R was formed with
-            o[S_MODE] = single ? 1.0 : 0.0;
-            o[S_BOUND] = bound;
-            o[S_STEPS] = s == 0 ? steps[0] : steps[1];
-          }
-        }
-      }
-      named_bar_sync(1, 128);
-      for (int s = 0; s < ns; ++s) {
-        const int ti = s_ti(s), tj = s_tj(s);
-        const int gr = ti * 128 + r;
-        const bool row_ok = gr < p.h;
-        const int64_t mbase = static_cast<int64_t>(s_b(s)) * p.mat;
-        const float d_f = static_cast<float>(s_scale[s][0]), inv_s_f = static_cast<float>(s_scale[s][1]);
-        if ((p.h & 31) == 0) {
-          // Whole 32 x 32 blocks: every lane stores its row segment with 16-byte vector stores, and
-          // the mirror block goes through a per-warp shared-memory transpose (the pipeline stages
-          // are idle now), so every global store is a run of whole sectors.
-          uint32_t* tb = reinterpret_cast<uint32_t*>(smem) + ew * 32 * 33;
-          const int gr0 = ti * 128 + ew * 32;
-          for (int c = 0; c < 4; ++c) {
-            const int gc0 = tj * 128 + c * 32;
-            uint32_t up[32];
-            tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);  // warp-collective: every lane
-            tmem_wait_ld();
-            const bool diag = ti == tj && c == ew;        // block straddling the diagonal
-            if (gr0 >= p.h || gc0 >= p.h || (ti == tj && c < ew)) continue;  // warp-uniform
-            uint32_t hl[32];                              // (hi << 16) | lo of row gr, columns gc0 + j
 #pragma unroll
+          for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = hl[j];
+          __syncwarp();
+          if (diag) {  // lower half of the block from the transposed upper half: exact symmetry
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < lane) hl[j] = tb[j * 33 + lane];
+          }
+          const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            uint4 vh, vl;
+            vh.x = (hl[j] >> 16) | (hl[j + 1] & 0xFFFF0000u);
+            vh.y = (hl[j + 2] >> 16) | (hl[j + 3] & 0xFFFF0000u);
+            vh.z = (hl[j + 4] >> 16) | (hl[j + 5] & 0xFFFF0000u);
+            vh.w = (hl[j + 6] >> 16) | (hl[j + 7] & 0xFFFF0000u);
+            vl.x = (hl[j] & 0xFFFFu) | (hl[j + 1] << 16);
+            vl.y = (hl[j + 2] & 0xFFFFu) | (hl[j + 3] << 16);
+            vl.z = (hl[j + 4] & 0xFFFFu) | (hl[j + 5] << 16);
+            vl.w = (hl[j + 6] & 0xFFFFu) | (hl[j + 7] << 16);
+            *reinterpret_cast<uint4*>(p.phi + o + j) = vh;
+            *reinterpret_cast<uint4*>(p.plo + o + j) = vl;
+          }
+          if (!diag) {  // mirror: lane writes row gc0 + lane, columns gr0 .. gr0 + 31
+            const int64_t om = mbase + static_cast<int64_t>(gc0 + lane) * p.ld + gr0;
+#pragma unroll
+            for (int m = 0; m < 32; m += 8) {
+              uint32_t w[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) w[e] = tb[(m + e) * 33 + lane];
+              uint4 vh, vl;
+              vh.x = (w[0] >> 16) | (w[1] & 0xFFFF0000u);
+              vh.y = (w[2] >> 16) | (w[3] & 0xFFFF0000u);
+              vh.z = (w[4] >> 16) | (w[5] & 0xFFFF0000u);
+              vh.w = (w[6] >> 16) | (w[7] & 0xFFFF0000u);
+              vl.x = (w[0] & 0xFFFFu) | (w[1] << 16);
+              vl.y = (w[2] & 0xFFFFu) | (w[3] << 16);
+              vl.z = (w[4] & 0xFFFFu) | (w[5] << 16);
+              vl.w = (w[6] & 0xFFFFu) | (w[7] << 16);
+              *reinterpret_cast<uint4*>(p.phi + om + m) = vh;
+              *reinterpret_cast<uint4*>(p.plo + om + m) = vl;
+            }
+          }
+          __syncwarp();
+        }
+      } else {
+        for (int c = c0; c < c0 + 2; ++c) {
+          const int gc0 = tj * 128 + c * 32;
+          uint32_t up[32];
+          tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);  // warp-collective: every lane, row_ok or not
+          tmem_wait_ld();
+          if (row_ok) {
             for (int j = 0; j < 32; ++j) {
-              const float rv = __uint_as_float(up[j]) - (gc0 + j == gr ? d_f : 0.f);
+              const int gc = gc0 + j;
+              if (gc >= p.h || (ti == tj && gc < gr)) continue;
+              const float rv = __uint_as_float(up[j]) - (gc == gr ? d_f : 0.f);
               __nv_bfloat16 hi, lo;
               split_bf16(rv * inv_s_f, hi, lo);
-              hl[j] = (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16) | __bfloat16_as_ushort(lo);
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = hl[j];
-            __syncwarp();
-            if (diag) {  // lower half of the block from the transposed upper half: exact symmetry
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j < lane) hl[j] = tb[j * 33 + lane];
-            }
-            const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 vh, vl;
-              vh.x = (hl[j] >> 16) | (hl[j + 1] & 0xFFFF0000u);
-              vh.y = (hl[j + 2] >> 16) | (hl[j + 3] & 0xFFFF0000u);
-              vh.z = (hl[j + 4] >> 16) | (hl[j + 5] & 0xFFFF0000u);
-              vh.w = (hl[j + 6] >> 16) | (hl[j + 7] & 0xFFFF0000u);
-              vl.x = (hl[j] & 0xFFFFu) | (hl[j + 1] << 16);
-              vl.y = (hl[j + 2] & 0xFFFFu) | (hl[j + 3] << 16);
-              vl.z = (hl[j + 4] & 0xFFFFu) | (hl[j + 5] << 16);
-              vl.w = (hl[j + 6] & 0xFFFFu) | (hl[j + 7] << 16);
-              *reinterpret_cast<uint4*>(p.phi + o + j) = vh;
-              *reinterpret_cast<uint4*>(p.plo + o + j) = vl;
-            }
-            if (!diag) {  // mirror: lane writes row gc0 + lane, columns gr0 .. gr0 + 31
-              const int64_t om = mbase + static_cast<int64_t>(gc0 + lane) * p.ld + gr0;
-#pragma unroll
-              for (int m = 0; m < 32; m += 8) {
-                uint32_t w[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) w[e] = tb[(m + e) * 33 + lane];
-                uint4 vh, vl;
-                vh.x = (w[0] >> 16) | (w[1] & 0xFFFF0000u);
-                vh.y = (w[2] >> 16) | (w[3] & 0xFFFF0000u);
-                vh.z = (w[4] >> 16) | (w[5] & 0xFFFF0000u);
-                vh.w = (w[6] >> 16) | (w[7] & 0xFFFF0000u);
-                vl.x = (w[0] & 0xFFFFu) | (w[1] << 16);
-                vl.y = (w[2] & 0xFFFFu) | (w[3] << 16);
-                vl.z = (w[4] & 0xFFFFu) | (w[5] << 16);
-                vl.w = (w[6] & 0xFFFFu) | (w[7] << 16);
-                *reinterpret_cast<uint4*>(p.phi + om + m) = vh;
-                *reinterpret_cast<uint4*>(p.plo + om + m) = vl;
-              }
-            }
-            __syncwarp();
-          }
-        } else {
-          for (int c = 0; c < 4; ++c) {
-            const int gc0 = tj * 128 + c * 32;
-            uint32_t up[32];
-            tmem_ld32(lane_base + s * CH_SLOT + CH_P + c * 32, up);  // warp-collective: every lane, row_ok or not
-            tmem_wait_ld();
-            if (row_ok) {
-              for (int j = 0; j < 32; ++j) {
-                const int gc = gc0 + j;
-                if (gc >= p.h || (ti == tj && gc < gr)) continue;
-                const float rv = __uint_as_float(up[j]) - (gc == gr ? d_f : 0.f);
-                __nv_bfloat16 hi, lo;
-                split_bf16(rv * inv_s_f, hi, lo);
-                const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
-                const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
-                p.phi[o] = hi;
-                p.plo[o] = lo;
-                p.phi[om] = hi;
-                p.plo[om] = lo;
-              }
+              const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc;
+              const int64_t om = mbase + static_cast<int64_t>(gc) * p.ld + gr;
+              p.phi[o] = hi;
+              p.plo[o] = lo;
+              p.phi[om] = hi;
+              p.plo[om] = lo;
             }
           }
         }
       }
-      if (tid == 0) CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 3);
     }
+    if (threadIdx.x == 128) CHAIN_TRACE(CHAIN_MAX_ORDER - 1, 3);
   }
   __syncthreads();
   if (warp == 2) {
