@@ -418,11 +418,15 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
             mbar_wait(&empty[stage], phase ^ 1);
             if (s == 0) CHAIN_KB(k, 1, kt);
             uint8_t* st = smem + stage * CH_STAGE_BYTES;
-            mbar_arrive_expect_tx(&full[stage], hi_only ? 2 * CH_TILE : CH_STAGE_BYTES);
+            // diagonal tiles: the B row block is the A row block (one copy in shared memory serves both)
+            const int nblk = (ti == tj ? 1 : 2) * (hi_only ? 1 : 2);
+            mbar_arrive_expect_tx(&full[stage], nblk * CH_TILE);
             ch_load_block(maps, buf, 0, &full[stage], st, ti, kt, b);
             if (!hi_only) ch_load_block(maps, buf, 1, &full[stage], st + CH_TILE, ti, kt, b);
-            ch_load_block(maps, buf, 0, &full[stage], st + 2 * CH_TILE, tj, kt, b);
-            if (!hi_only) ch_load_block(maps, buf, 1, &full[stage], st + 3 * CH_TILE, tj, kt, b);
+            if (ti != tj) {
+              ch_load_block(maps, buf, 0, &full[stage], st + 2 * CH_TILE, tj, kt, b);
+              if (!hi_only) ch_load_block(maps, buf, 1, &full[stage], st + 3 * CH_TILE, tj, kt, b);
+            }
             if (++stage == CH_STAGES) {
               stage = 0;
               phase ^= 1;
@@ -462,14 +466,13 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
           const bool a_mn = kb < ti, b_mn = kb < tj;
           const uint32_t idesc = idesc_bf16(128, 128, a_mn ? 1 : 0, b_mn ? 1 : 0) | IDESC_NEGATE_A;
           const uint32_t st = smem_u32(smem + stage * CH_STAGE_BYTES);
+          const uint32_t sb = ti == tj ? st : st + 2 * CH_TILE;  // diagonal tile: B = A
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ah = a_mn ? operand_desc<true>(st, ks) : operand_desc<false>(st, ks);
             const uint64_t al = a_mn ? operand_desc<true>(st + CH_TILE, ks) : operand_desc<false>(st + CH_TILE, ks);
-            const uint64_t bh = b_mn ? operand_desc<true>(st + 2 * CH_TILE, ks)
-                                     : operand_desc<false>(st + 2 * CH_TILE, ks);
-            const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * CH_TILE, ks)
-                                     : operand_desc<false>(st + 3 * CH_TILE, ks);
+            const uint64_t bh = b_mn ? operand_desc<true>(sb, ks) : operand_desc<false>(sb, ks);
+            const uint64_t bl = b_mn ? operand_desc<true>(sb + CH_TILE, ks) : operand_desc<false>(sb + CH_TILE, ks);
             umma_bf16_warp(d_tmem, ah, bh, idesc, 1u);
             if (k > p.hi_only) {
               umma_bf16_warp(d_tmem, ah, bl, idesc, 1u);
