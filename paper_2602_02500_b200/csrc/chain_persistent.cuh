@@ -161,6 +161,9 @@ constexpr int CH_SMEM = CH_STAGES * CH_STAGE_BYTES + 256 + 1024;
 // TMEM columns of tile slot s: [256 s, 256 s + 128) the state D, [256 s + 128, 256 s + 256) P.
 constexpr uint32_t CH_SLOT = 256, CH_D = 0, CH_P = 128;
 constexpr int CH_SLOTS = 2;
+constexpr int CH_GT_LD = 132;                    // phase A: row pitch (floats) of a staged 128 x 128 Gram tile
+constexpr int CH_GT_FLOATS = 128 * CH_GT_LD;      // one staged tile per slot in the (still idle) pipeline stages
+static_assert(CH_SLOTS * CH_GT_FLOATS * 4 <= CH_STAGES * CH_STAGE_BYTES, "staged Gram tiles must fit the stages");
 
 __device__ __forceinline__ void ch_load_block(const ChainMaps& maps, int buf, int hl, uint64_t* bar, uint8_t* dst,
                                               int blk, int kt, int b) {
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
 
 
   // ================================================================== phase A (all 8 warps)
-  // G tile = sum of split-K partials -> TMEM D region; tile norms; scale; C_1, D = 2 C_1, P.
+  // G tile = sum of split-K partials -> shared memory; tile norms; scale; C_1, D = 2 C_1, P -> TMEM.
   // Warp w owns TMEM lanes 32 (w & 3) .. + 31 (row r of the tile per thread); warps 4-7 take the
   // column chunks 0-1 of every tile and warps 0-3 the chunks 2-3 (the producer / MMA roles start after C_1).
   const int ew = warp & 3;
@@ -252,53 +255,51 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
   const int c0 = warp >= 4 ? 0 : 2;  // first of this warp's two 32-column chunks
   const uint32_t lane_base = tmem + (static_cast<uint32_t>(ew * 32) << 16);
   if (threadIdx.x == 128) CHAIN_TRACE(0, 0);
+  // The split-K partials of a tile are read row by row, one 512-byte row per warp request (coalesced;
+  // 16 rows x splits independent loads in flight per lane), summed, and staged in shared memory (the
+  // pipeline stages are idle until C_1 is published) for the row-per-thread TMEM layout of the C_1 step.
   for (int s = 0; s < ns; ++s) {
     const int ti = s_ti(s), tj = s_tj(s), b = s_b(s);
-    const int gr = ti * 128 + r;
-    const bool row_ok = gr < p.h;
     double tr = 0.0, fr = 0.0;
     const double wgt = (ti == tj) ? 1.0 : 2.0;
-    // both 32-column chunks of a split-K slice are loaded before any is summed (16 independent
-    // 16-byte loads in flight per thread, 256 threads: the phase is load-latency-bound)
-    float g2[2][32];
+    float* gt = reinterpret_cast<float*>(smem) + s * CH_GT_FLOATS;
+    float4 acc[16];
 #pragma unroll
-    for (int c = 0; c < 2; ++c)
+    for (int q = 0; q < 16; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int sp = 0; sp < p.splits; ++sp) {
+      const float* base = p.part + (static_cast<int64_t>(sp) * p.batch + b) * p.part_mat + tj * 128 + lane * 4;
+      float4 v[16];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) g2[c][j] = 0.f;
-    if (row_ok) {
-      for (int sp = 0; sp < p.splits; ++sp) {
-        const float* src = p.part + (static_cast<int64_t>(sp) * p.batch + b) * p.part_mat +
-                           static_cast<int64_t>(gr) * p.part_ld + tj * 128 + c0 * 32;
-        float4 v[16];
+      for (int q = 0; q < 16; ++q) {
+        const int gr = ti * 128 + warp * 16 + q;
+        v[q] = gr < p.h ? __ldcg(reinterpret_cast<const float4*>(base + static_cast<int64_t>(gr) * p.part_ld))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = __ldcg(reinterpret_cast<const float4*>(src) + q);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          float* gq = &g2[q >> 3][(q & 7) * 4];
-          gq[0] += v[q].x;
-          gq[1] += v[q].y;
-          gq[2] += v[q].z;
-          gq[3] += v[q].w;
-        }
+      for (int q = 0; q < 16; ++q) {
+        acc[q].x += v[q].x;
+        acc[q].y += v[q].y;
+        acc[q].z += v[q].z;
+        acc[q].w += v[q].w;
       }
     }
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int gc0 = tj * 128 + (c0 + c) * 32;
-      uint32_t u[32];
-      float frc = 0.f;  // fp32 partial over the 32 columns, accumulated in fp64 across chunks
+    for (int q = 0; q < 16; ++q) {
+      const int i = warp * 16 + q;
+      const int gr = ti * 128 + i, gc = tj * 128 + lane * 4;
+      const bool row_ok = gr < p.h;
+      float e[4] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w};
+      float frc = 0.f;  // fp32 partial over this lane's 4 columns, accumulated in fp64 across rows
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const bool ok = row_ok && (gc0 + j) < p.h;
-        const float v = ok ? g2[c][j] : 0.f;
-        if (ok && gc0 + j == gr) tr += v;
-        frc = fmaf(v, v, frc);
-        u[j] = __float_as_uint(v);
+      for (int j = 0; j < 4; ++j) {
+        const bool ok = row_ok && (gc + j) < p.h;
+        e[j] = ok ? e[j] : 0.f;
+        if (ok && gc + j == gr) tr += e[j];
+        frc = fmaf(e[j], e[j], frc);
       }
       fr += wgt * static_cast<double>(frc);
-      tmem_st32(lane_base + s * CH_SLOT + CH_D + (c0 + c) * 32, u);
+      *reinterpret_cast<float4*>(gt + i * CH_GT_LD + lane * 4) = make_float4(e[0], e[1], e[2], e[3]);
     }
-    tmem_wait_st();
     tr = warp_sum(tr);
     fr = warp_sum(fr);
     __syncthreads();  // red[] free (slot 0's sums were consumed)
@@ -353,11 +354,13 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
       const bool row_ok = gr < p.h;
       const int64_t mbase = static_cast<int64_t>(s_b(s)) * p.mat;
       const float inv_s2 = static_cast<float>(s_scale[s][0]);
+      const float* gt = reinterpret_cast<const float*>(smem) + s * CH_GT_FLOATS + r * CH_GT_LD;
       for (int c = c0; c < c0 + 2; ++c) {
         const int gc0 = tj * 128 + c * 32;
         uint32_t u[32], pu[32];
-        tmem_ld32(lane_base + s * CH_SLOT + CH_D + c * 32, u);
-        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)  // row r of the staged tile: pitch 132 floats, conflict-free per quarter warp
+          *reinterpret_cast<float4*>(&u[j]) = *reinterpret_cast<const float4*>(gt + c * 32 + j);
         __align__(16) __nv_bfloat16 hi[32];
         __align__(16) __nv_bfloat16 lo[32];
 #pragma unroll
@@ -383,6 +386,7 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
     tmem_wait_st();
     tc_fence_before();
     fence_proxy_async_global();
+    fence_proxy_async_shared();  // the staged tiles (generic proxy) are done before TMA refills the stages
     __syncthreads();
     if (warp >= 4)
       for (int s = 0; s < ns; ++s) mbar_arrive(&tempty[s]);  // D_s = 2 C_1 is in place for step 1's MMAs
