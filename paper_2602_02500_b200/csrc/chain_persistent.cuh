@@ -272,8 +272,10 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int gr = ti * 128 + warp * 16 + q;
-        v[q] = gr < p.h ? __ldcg(reinterpret_cast<const float4*>(base + static_cast<int64_t>(gr) * p.part_ld))
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        // (a dense Gram read in place has part_ld = h, a multiple of 4: no read past the end of a row)
+        v[q] = (gr < p.h && tj * 128 + lane * 4 < p.part_ld)
+                   ? __ldcg(reinterpret_cast<const float4*>(base + static_cast<int64_t>(gr) * p.part_ld))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
