@@ -762,6 +762,32 @@ def run_e2e_muon(work, steps, dev):
         "on three streams")
 
 
+def recorded_chain_phases(h, hbm_peak):
+    """The reduction / normalisation phases of configs[3] run inside the persistent chain kernel, so the
+    stage events cannot time them; this reports their durations from the committed phase timeline of
+    the timing build (tools/chain_trace.py -> profiles/round2_end_chain_trace_cfg4.txt; a recorded
+    figure, not measured in this run) against their algorithmic bytes (L2-resident data)."""
+    path = os.path.join(REPO, "profiles", "round2_end_chain_trace_cfg4.txt")
+    out = {"source": "profiles/round2_end_chain_trace_cfg4.txt (timing build, recorded; not measured in this run)"}
+    try:
+        import re
+        line = next(ln for ln in open(path) if "phase A:" in ln)
+        us_a = float(re.search(r"partials\+norms ([0-9.]+) us", line).group(1))
+        us_p = float(re.search(r"P split\+mirror ([0-9.]+)", line).group(1))
+    except Exception:  # noqa: BLE001
+        return None
+    nt = (h + 127) // 128
+    tiles = nt * (nt + 1) // 2
+    splits = 2
+    a_bytes = tiles * 128 * 128 * 4 * splits                # split-K fp32 Gram partials in (upper tiles)
+    p_bytes = h * h * 2 * 2                                 # P/s as bf16 hi + lo, both triangles, out
+    out["split_k_sum_and_norms"] = {"bytes": a_bytes, "us": us_a, "GB/s": a_bytes / us_a / 1e3,
+                                    "frac_of_hbm_peak": a_bytes / us_a / 1e3 / hbm_peak}
+    out["p_split_and_mirror"] = {"bytes": p_bytes, "us": us_p, "GB/s": p_bytes / us_p / 1e3,
+                                 "frac_of_hbm_peak": p_bytes / us_p / 1e3 / hbm_peak}
+    return out
+
+
 # ----------------------------------------------------------------------------- main
 
 def main(argv=None):
@@ -938,6 +964,8 @@ def main(argv=None):
             else:
                 hbm[k] = {"fused": "into the persistent chain kernel (no stand-alone launch)",
                           "ms_per_step": stages.get(k)}
+        if wl == "cfg4" and work.h == 2048 and work.precision == "bf16":
+            hbm["chain_phases_recorded"] = recorded_chain_phases(work.h, hbm_peak)
 
     # ---- cfg4: per-rank critical path of an N-way row shard, measured on this GPU
     projection = None
