@@ -747,19 +747,60 @@ def run_e2e_muon(work, steps, dev):
 
     one_step()  # warm-up (allocations, pointer lists)
     torch.cuda.synchronize()
+    if os.environ.get("UNSO_BENCH_E2E_TRACE"):  # developer: per-group timeline of two pipelined steps (stderr)
+        tr = []
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record(s_h2d)
+        for st in range(2):
+            for g in range(ng):
+                marks = {}
+                for name, strm in (("h2d", s_h2d), ("cmp", s_cmp), ("d2h", s_d2h)):
+                    marks[name] = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                with torch.cuda.stream(s_h2d):
+                    s_h2d.wait_event(ev_cmp[g])
+                    marks["h2d"][0].record(s_h2d)
+                    for gh, p in zip(grads_h[g], plist[g]):
+                        p.grad.copy_(gh, non_blocking=True)
+                    marks["h2d"][1].record(s_h2d)
+                    ev_h2d[g].record(s_h2d)
+                with torch.cuda.stream(s_cmp):
+                    s_cmp.wait_event(ev_h2d[g])
+                    s_cmp.wait_event(ev_d2h[g])
+                    marks["cmp"][0].record(s_cmp)
+                    opts[g].step()
+                    marks["cmp"][1].record(s_cmp)
+                    ev_cmp[g].record(s_cmp)
+                with torch.cuda.stream(s_d2h):
+                    s_d2h.wait_event(ev_cmp[g])
+                    marks["d2h"][0].record(s_d2h)
+                    for ph, p in zip(params_h[g], plist[g]):
+                        ph.copy_(p.detach(), non_blocking=True)
+                    marks["d2h"][1].record(s_d2h)
+                    ev_d2h[g].record(s_d2h)
+                tr.append((st, g, marks))
+        torch.cuda.synchronize()
+        for st, g, marks in tr:
+            print(f"[e2e trace] step {st} group {g} ({len(plist[g])} x {tuple(plist[g][0].shape)}): " + ", ".join(
+                f"{k} {t0.elapsed_time(a):.0f}-{t0.elapsed_time(b):.0f} ms" for k, (a, b) in marks.items()),
+                file=sys.stderr)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    done = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     e0.record(s_h2d)
-    for _ in range(steps):
+    for i in range(steps):
         one_step()
+        done[i].record(s_d2h)  # the step's last parameters are back on the host
     s_d2h.wait_stream(s_cmp)
     s_d2h.wait_stream(s_h2d)
     e1.record(s_d2h)
     torch.cuda.synchronize()
     nbytes = sum(p.numel() * p.element_size() for p in work.params)
-    return e0.elapsed_time(e1) / steps, nbytes, nbytes, (
-        "gradients pinned host -> device, Muon.step per shape group (grouped orthogonalize), updated "
-        "parameters device -> pinned host; the copies of neighbouring groups overlap each group's step "
-        "on three streams")
+    how = ("gradients pinned host -> device, Muon.step per shape group (grouped orthogonalize), updated "
+           "parameters device -> pinned host; the copies of neighbouring groups overlap each group's step "
+           "on three streams")
+    if steps > 1:  # whole-run average includes the pipeline's fill (first H2D) and drain (last D2H)
+        steady = done[0].elapsed_time(done[-1]) / (steps - 1)
+        how += f"; steady state (completion to completion of consecutive steps): {steady:.1f} ms per step"
+    return e0.elapsed_time(e1) / steps, nbytes, nbytes, how
 
 
 def recorded_chain_phases(h, hbm_peak):
