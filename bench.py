@@ -952,7 +952,7 @@ def main(argv=None):
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e_steps = args.e2e_steps or (1 if wl == "cfg3" else min(30, max(steps, 4)))
+        e_steps = args.e2e_steps or (4 if wl == "cfg3" else min(30, max(steps, 4)))  # cfg3: ~0.55 s per step
         barrier()
         r = run_e2e_muon(work, e_steps, dev) if wl == "cfg3" else run_e2e_matrix(work, e_steps, dev)
         if r is not None:
