@@ -378,9 +378,9 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
         if (row_ok && N > 1) {
           const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
 #pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            *reinterpret_cast<uint4*>(p.chi[0] + o + j) = *reinterpret_cast<const uint4*>(hi + j);
-            *reinterpret_cast<uint4*>(p.clo[0] + o + j) = *reinterpret_cast<const uint4*>(lo + j);
+          for (int j = 0; j < 32; j += 16) {  // 256-bit stores: whole sectors (ld % 256 == 0)
+            st_global_v8(p.chi[0] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(hi + j));
+            st_global_v8(p.clo[0] + o + j, *reinterpret_cast<const uint32_t(*)[8]>(lo + j));
           }
         }
       }
@@ -720,37 +720,30 @@ __global__ void __launch_bounds__(256, 1) chain_persistent_kernel(const __grid_c
           }
           const int64_t o = mbase + static_cast<int64_t>(gr) * p.ld + gc0;
 #pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            uint4 vh, vl;
-            vh.x = (hl[j] >> 16) | (hl[j + 1] & 0xFFFF0000u);
-            vh.y = (hl[j + 2] >> 16) | (hl[j + 3] & 0xFFFF0000u);
-            vh.z = (hl[j + 4] >> 16) | (hl[j + 5] & 0xFFFF0000u);
-            vh.w = (hl[j + 6] >> 16) | (hl[j + 7] & 0xFFFF0000u);
-            vl.x = (hl[j] & 0xFFFFu) | (hl[j + 1] << 16);
-            vl.y = (hl[j + 2] & 0xFFFFu) | (hl[j + 3] << 16);
-            vl.z = (hl[j + 4] & 0xFFFFu) | (hl[j + 5] << 16);
-            vl.w = (hl[j + 6] & 0xFFFFu) | (hl[j + 7] << 16);
-            *reinterpret_cast<uint4*>(p.phi + o + j) = vh;
-            *reinterpret_cast<uint4*>(p.plo + o + j) = vl;
+          for (int j = 0; j < 32; j += 16) {  // 256-bit stores (one sector per lane and array)
+            uint32_t vh[8], vl[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              vh[e] = (hl[j + 2 * e] >> 16) | (hl[j + 2 * e + 1] & 0xFFFF0000u);
+              vl[e] = (hl[j + 2 * e] & 0xFFFFu) | (hl[j + 2 * e + 1] << 16);
+            }
+            st_global_v8(p.phi + o + j, vh);
+            st_global_v8(p.plo + o + j, vl);
           }
           if (!diag) {  // mirror: lane writes row gc0 + lane, columns gr0 .. gr0 + 31
             const int64_t om = mbase + static_cast<int64_t>(gc0 + lane) * p.ld + gr0;
 #pragma unroll
-            for (int m = 0; m < 32; m += 8) {
-              uint32_t w[8];
+            for (int m = 0; m < 32; m += 16) {
+              uint32_t w[16], vh[8], vl[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) w[e] = tb[(m + e) * 33 + lane];
-              uint4 vh, vl;
-              vh.x = (w[0] >> 16) | (w[1] & 0xFFFF0000u);
-              vh.y = (w[2] >> 16) | (w[3] & 0xFFFF0000u);
-              vh.z = (w[4] >> 16) | (w[5] & 0xFFFF0000u);
-              vh.w = (w[6] >> 16) | (w[7] & 0xFFFF0000u);
-              vl.x = (w[0] & 0xFFFFu) | (w[1] << 16);
-              vl.y = (w[2] & 0xFFFFu) | (w[3] << 16);
-              vl.z = (w[4] & 0xFFFFu) | (w[5] << 16);
-              vl.w = (w[6] & 0xFFFFu) | (w[7] << 16);
-              *reinterpret_cast<uint4*>(p.phi + om + m) = vh;
-              *reinterpret_cast<uint4*>(p.plo + om + m) = vl;
+              for (int e = 0; e < 16; ++e) w[e] = tb[(m + e) * 33 + lane];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                vh[e] = (w[2 * e] >> 16) | (w[2 * e + 1] & 0xFFFF0000u);
+                vl[e] = (w[2 * e] & 0xFFFFu) | (w[2 * e + 1] << 16);
+              }
+              st_global_v8(p.phi + om + m, vh);
+              st_global_v8(p.plo + om + m, vl);
             }
           }
           __syncwarp();
