@@ -101,3 +101,26 @@ def test_two_slot_matches_one_slot_per_matrix():
         y1 = U.orthogonalize(m, UNSO, precision="bf16").y
         r = rel(yb[i].double().cpu().numpy(), y1.double().cpu().numpy())
         assert r <= 1e-2, (i, r)
+
+
+@pytest.mark.parametrize("variant", ["plain", "no_truncation", "two_term_apply"])
+def test_two_group_launch_with_spec_variants(variant):
+    """The same two-group launch under the other recipe knobs of the path: plain (trace) scaling
+    (ortho.py:153-154), the truncation switched off (every group runs all 13 squarings) and the forced
+    bf16x2 apply."""
+    w, h, nb = 1536, 512, 16
+    kw = {"plain": dict(scaling="plain"), "no_truncation": dict(truncate=False),
+          "two_term_apply": dict(apply_terms=2)}[variant]
+    spec = U.MethodSpec(U.MethodKind.UNSO, coeffs=U.default_coefficients(), **kw)
+    mats = [(well_conditioned if i % 2 else ill_conditioned)(w, h, 77 + i) for i in range(nb)]
+    x = torch.stack(mats).to(torch.bfloat16)
+    res = U.orthogonalize(x, spec, precision="bf16")
+    torch.cuda.synchronize()
+    assert torch.isfinite(res.y).all()
+    steps = [int(d["chain_steps"]) for d in res.info]
+    if variant == "no_truncation":
+        assert steps == [13] * nb, steps
+    for i in range(nb):
+        ref = O.run(x[i].double().cpu().numpy(), "unso", scaling="plain" if variant == "plain" else None)["y"]
+        r = rel(res.y[i].double().cpu().numpy(), ref)
+        assert r <= TOL + 2.0 ** -9, (variant, i, r)
