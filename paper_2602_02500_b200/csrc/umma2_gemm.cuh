@@ -101,6 +101,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // diagonal SYRK tiles of a same-tensor product can share one operand copy when A and B tiles have
+  // the same shape, major and count (each CTA's B half is then exactly its A half)
+  constexpr bool kDiagShare = Cfg::OPT == 0 && Cfg::A_MN == Cfg::B_MN && Cfg::NA == Cfg::NB &&
+                              Cfg::A_TILE == Cfg::B_TILE && Cfg::BM == Cfg::BN;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
@@ -155,7 +159,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         const int arow = tm * Cfg::BM + static_cast<int>(rank) * 128;
         const int brow = tn * Cfg::BN + static_cast<int>(rank) * Cfg::HB;
         const bool skip = Cfg::OPT != 0 && opt_skipped(work, b);
-        const uint32_t bytes = 2 * (Cfg::STAGE_BYTES - (skip ? (Cfg::OPT == 1 ? Cfg::B_TILE : Cfg::A_TILE) : 0));
+        const bool dshare = kDiagShare && work.diag_share && tm == tn;  // B rows = A rows: one copy
+        const uint32_t bytes = dshare ? 2 * Cfg::NA * Cfg::A_TILE
+                                      : 2 * (Cfg::STAGE_BYTES - (skip ? (Cfg::OPT == 1 ? Cfg::B_TILE : Cfg::A_TILE) : 0));
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
@@ -165,9 +171,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           if (Cfg::NA > 1 && !(skip && Cfg::OPT == 2))
             load_operand_tile_pair<Cfg::A_MN, 128>(&tmA1, lbar, st + Cfg::A_TILE, kt * 64, arow, b);
           uint8_t* sb = st + Cfg::NA * Cfg::A_TILE;
-          load_operand_tile_pair<Cfg::B_MN, Cfg::HB>(&tmB0, lbar, sb, kt * 64, brow, b);
-          if (Cfg::NB > 1 && !(skip && Cfg::OPT == 1))
-            load_operand_tile_pair<Cfg::B_MN, Cfg::HB>(&tmB1, lbar, sb + Cfg::B_TILE, kt * 64, brow, b);
+          if (!dshare) {
+            load_operand_tile_pair<Cfg::B_MN, Cfg::HB>(&tmB0, lbar, sb, kt * 64, brow, b);
+            if (Cfg::NB > 1 && !(skip && Cfg::OPT == 1))
+              load_operand_tile_pair<Cfg::B_MN, Cfg::HB>(&tmB1, lbar, sb + Cfg::B_TILE, kt * 64, brow, b);
+          }
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -187,6 +195,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         umma_decode(work, idx, b, split, tm, tn, kt0, kt1);
         if (filtered_out(work, b)) continue;
         const bool skip = Cfg::OPT != 0 && opt_skipped(work, b);
+        const bool dshare = kDiagShare && work.diag_share && tm == tn;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * Cfg::BN);
@@ -194,7 +203,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-          const uint32_t sb = st + Cfg::NA * Cfg::A_TILE;
+          const uint32_t sb = dshare ? st : st + Cfg::NA * Cfg::A_TILE;
 #pragma unroll
           for (int ks = 0; ks < Cfg::BK / 16; ++ks) {
 #pragma unroll

@@ -35,6 +35,9 @@ struct UmmaWork {
   // Squaring-chain kernels (chain_pair.cuh): 1 = accumulate the hi*hi product only (no lo / e4m3
   // cross terms, their operand tiles are not loaded) -- the first squarings of the chain.
   int no_cross = 0;
+  // SYRK launches whose A and B maps are the same tensor (the Gram X^T X): a diagonal tile's B rows
+  // are its A rows, so the pair engine loads one copy and points both descriptors at it.
+  int diag_share = 0;
 };
 
 // Non-SYRK tile order: groups of UMMA_GROUP_M row blocks, row block fastest within a group, so the

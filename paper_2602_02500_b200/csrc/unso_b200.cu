@@ -1116,6 +1116,13 @@ static int32_t ensure_bf16_x(const Problem& p, const Plan& pl, void* ws, const v
   return UNSO_OK;
 }
 
+// Gram launches (A and B maps are the same tensor): diagonal tiles share one operand copy (umma2_gemm.cuh).
+static UmmaWork gram_work2(int M, int N, int K, int BN, int batch, int splits) {
+  UmmaWork w = umma2_make_work(M, N, K, BN, batch, true, splits);
+  w.diag_share = 1;
+  return w;
+}
+
 static int32_t gram_bf16(const Problem& p, const Plan& pl, void* ws, const __nv_bfloat16* xb, int64_t ldx,
                          int64_t bsx, cudaStream_t st) {
   CUtensorMap mx;
@@ -1124,8 +1131,8 @@ static int32_t gram_bf16(const Problem& p, const Plan& pl, void* ws, const __nv_
   UEpiPartialF32 epi{at<float>(ws, pl.part), pl.hh, pl.ldc, static_cast<int>(p.batch), static_cast<int>(p.h)};
   cudaError_t e;
   const bool pair = use_pair_engine();
-  const UmmaWork w2 = umma2_make_work(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 256,
-                                      static_cast<int>(p.batch), true, pl.splits);
+  const UmmaWork w2 = gram_work2(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 256,
+                                 static_cast<int>(p.batch), pl.splits);
   if (p.tall) {
     if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
     e = pair ? launch_umma2<Cfg2GramMN>(mx, mx, mx, mx, w2, epi, st) : launch_umma<CfgGramMN>(mx, mx, mx, mx, w, epi, st);
@@ -1145,8 +1152,8 @@ static int32_t gram_bf16_split(const Problem& p, const Plan& pl, void* ws, const
   const int nt2 = static_cast<int>((p.h + 255) / 256);
   UEpiGramSplit epi{at<__nv_bfloat16>(ws, pl.Chi[0]), at<__nv_bfloat16>(ws, pl.Clo[0]), at<double>(ws, pl.mnorm),
                     pl.ldc, pl.hh, static_cast<int>(p.h), nt2};
-  const UmmaWork w2 = umma2_make_work(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 256,
-                                      static_cast<int>(p.batch), true, 1);
+  const UmmaWork w2 = gram_work2(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 256,
+                                 static_cast<int>(p.batch), 1);
   cudaError_t e;
   if (p.tall) {
     if (!umma_make_mnmajor_map(&mx, xb, p.rows, p.cols, ldx, p.batch, bsx)) return UNSO_ERR_CUDA;
@@ -1751,8 +1758,8 @@ static int32_t gram_bf16_x3(const Problem& p, const Plan& pl, void* ws, const __
                             const __nv_bfloat16* xl, int64_t ldx, int64_t bsx, cudaStream_t st) {
   CUtensorMap mh, ml;
   UEpiPartialF32 epi{at<float>(ws, pl.part), pl.hh, pl.ldc, static_cast<int>(p.batch), static_cast<int>(p.h)};
-  const UmmaWork w2 = umma2_make_work(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 256,
-                                      static_cast<int>(p.batch), true, pl.splits);
+  const UmmaWork w2 = gram_work2(static_cast<int>(p.h), static_cast<int>(p.h), static_cast<int>(p.w), 256,
+                                 static_cast<int>(p.batch), pl.splits);
   cudaError_t e;
   if (p.tall) {
     if (!umma_make_mnmajor_map(&mh, xh, p.rows, p.cols, ldx, p.batch, bsx) ||
@@ -2105,7 +2112,7 @@ int32_t unso_gram_push(const unso_matrix_desc* x, const void* x_ptr, const unso_
   UNSO_TRY(ensure_bf16_x(p, pl, workspace, x_ptr, xb, ldx, bsx, st));
   const int h = static_cast<int>(p.h);
   UEpiPushF32 epi{gp, rank, world, splits, gar_owned_max(h, world), h, (h + GAR_TILE - 1) / GAR_TILE};
-  const UmmaWork w2 = umma2_make_work(h, h, static_cast<int>(p.w), 256, 1, true, splits);
+  const UmmaWork w2 = gram_work2(h, h, static_cast<int>(p.w), 256, 1, splits);
   CUtensorMap mx;
   cudaError_t e;
   if (p.tall) {
