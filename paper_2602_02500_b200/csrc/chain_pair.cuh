@@ -90,11 +90,15 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * SC_STAGE_BYTES;
           const uint32_t lbar = lbar0 + stage * 8;
-          if (leader) mbar_arrive_expect_tx(&full[stage], work.no_cross ? SC_STAGE_BYTES : 2 * SC_STAGE_BYTES);
+          // diagonal pair tiles: each CTA's B rows are its A rows, one copy serves both operands
+          const uint32_t full_bytes = work.no_cross ? SC_STAGE_BYTES : 2 * SC_STAGE_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full[stage], tm == tn ? full_bytes / 2 : full_bytes);
           sc_load(&maps.hiK, &maps.hiMN, lbar, st, tm, arow, kt, b);
           if (!work.no_cross) sc_load(&maps.loK, &maps.loMN, lbar, st + SC_TILE, tm, arow, kt, b);
-          sc_load(&maps.hiK, &maps.hiMN, lbar, st + 2 * SC_TILE, tn, brow, kt, b);
-          if (!work.no_cross) sc_load(&maps.loK, &maps.loMN, lbar, st + 3 * SC_TILE, tn, brow, kt, b);
+          if (tm != tn) {
+            sc_load(&maps.hiK, &maps.hiMN, lbar, st + 2 * SC_TILE, tn, brow, kt, b);
+            if (!work.no_cross) sc_load(&maps.loK, &maps.loMN, lbar, st + 3 * SC_TILE, tn, brow, kt, b);
+          }
           if (++stage == SC_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -119,14 +123,13 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
           const bool a_mn = (kt >> 2) < tm, b_mn = (kt >> 2) < tn;
           const uint32_t idesc = idesc_bf16(256, 256, a_mn ? 1 : 0, b_mn ? 1 : 0);
           const uint32_t st = smem_u32(smem + stage * SC_STAGE_BYTES);
+          const uint32_t sb = tm == tn ? st : st + 2 * SC_TILE;  // diagonal pair tile: B = A
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ah = a_mn ? operand_desc<true>(st, ks) : operand_desc<false>(st, ks);
             const uint64_t al = a_mn ? operand_desc<true>(st + SC_TILE, ks) : operand_desc<false>(st + SC_TILE, ks);
-            const uint64_t bh = b_mn ? operand_desc<true>(st + 2 * SC_TILE, ks)
-                                     : operand_desc<false>(st + 2 * SC_TILE, ks);
-            const uint64_t bl = b_mn ? operand_desc<true>(st + 3 * SC_TILE, ks)
-                                     : operand_desc<false>(st + 3 * SC_TILE, ks);
+            const uint64_t bh = b_mn ? operand_desc<true>(sb, ks) : operand_desc<false>(sb, ks);
+            const uint64_t bl = b_mn ? operand_desc<true>(sb + SC_TILE, ks) : operand_desc<false>(sb + SC_TILE, ks);
             umma_bf16_pair_warp(d_tmem, ah, bh, idesc, (kt > kt0 || ks > 0) ? 1u : 0u);
             if (!work.no_cross) {
               umma_bf16_pair_warp(d_tmem, ah, bl, idesc, 1u);
@@ -333,12 +336,14 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * F8_STAGE_BYTES;
           const uint32_t lbar = lbar0 + stage * 8;
-          if (leader) mbar_arrive_expect_tx(&full[stage], work.no_cross ? 4 * SC_TILE : 2 * F8_STAGE_BYTES);
+          // diagonal pair tiles: each CTA's B rows are its A rows, one copy serves both operands
+          const uint32_t full_bytes = work.no_cross ? 4 * SC_TILE : 2 * F8_STAGE_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full[stage], tm == tn ? full_bytes / 2 : full_bytes);
           sc_load(&maps.hiK, &maps.hiMN, lbar, st, tm, arow, kt, b);
-          sc_load(&maps.hiK, &maps.hiMN, lbar, st + OFF_BH, tn, brow, kt, b);
+          if (tm != tn) sc_load(&maps.hiK, &maps.hiMN, lbar, st + OFF_BH, tn, brow, kt, b);
           if (!work.no_cross) {
             f8_load(maps, lbar, st + OFF_A8, tm, arow, kt, b);
-            f8_load(maps, lbar, st + OFF_B8, tn, brow, kt, b);
+            if (tm != tn) f8_load(maps, lbar, st + OFF_B8, tn, brow, kt, b);
           }
           if (++stage == F8_STAGES) {
             stage = 0;
@@ -365,17 +370,18 @@ __global__ void __launch_bounds__(SC_THREADS, 1)
           const uint32_t id16 = idesc_bf16(256, 256, a_mn ? 1 : 0, b_mn ? 1 : 0);
           const uint32_t id8 = idesc_e4m3(256, 256, a_mn ? 1 : 0, b_mn ? 1 : 0);
           const uint32_t st = smem_u32(smem + stage * F8_STAGE_BYTES);
+          const uint32_t off_bh = tm == tn ? 0 : OFF_BH, off_b8 = tm == tn ? OFF_A8 : OFF_B8;  // diagonal: B = A
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ah = a_mn ? operand_desc<true>(st, ks) : operand_desc<false>(st, ks);
-            const uint64_t bh = b_mn ? operand_desc<true>(st + OFF_BH, ks) : operand_desc<false>(st + OFF_BH, ks);
+            const uint64_t bh = b_mn ? operand_desc<true>(st + off_bh, ks) : operand_desc<false>(st + off_bh, ks);
             umma_bf16_pair_warp(d_tmem, ah, bh, id16, (kt > kt0 || ks > 0) ? 1u : 0u);
           }
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
             if (work.no_cross) break;
-            umma_f8_pair_warp(d_tmem, f8_desc(st + OFF_A8, a_mn, 0, ks), f8_desc(st + OFF_B8, b_mn, 1, ks), id8, 1u);
-            umma_f8_pair_warp(d_tmem, f8_desc(st + OFF_A8, a_mn, 1, ks), f8_desc(st + OFF_B8, b_mn, 0, ks), id8, 1u);
+            umma_f8_pair_warp(d_tmem, f8_desc(st + OFF_A8, a_mn, 0, ks), f8_desc(st + off_b8, b_mn, 1, ks), id8, 1u);
+            umma_f8_pair_warp(d_tmem, f8_desc(st + OFF_A8, a_mn, 1, ks), f8_desc(st + off_b8, b_mn, 0, ks), id8, 1u);
           }
           umma_commit_pair_warp(&empty[stage], 0x3);
           if (++stage == F8_STAGES) {
